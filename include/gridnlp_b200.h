@@ -1,0 +1,198 @@
+/* include/gridnlp_b200.h — the drop-in C-ABI of the B200 hot path.
+ *
+ * Pure C: opaque handles, plain pointers and sizes, int32 indices (the
+ * reference's index_t, common.hpp:14).  Every entry point returns an int
+ * status (GN_OK = 0) and, where it can fail, fills a caller-provided gn_error.
+ *
+ * Each function names the reference interface it replaces (paths relative to
+ * /root/reference/proj/include/gridnlp).  The C++ adapters that put this ABI
+ * back behind the reference's own classes are
+ *   include/gridnlp_b200/cuda_opf_nlp.hpp   -> ipm::NlpProblem   (ipm/nlp.hpp:15-39)
+ *   include/gridnlp_b200/shim/gridnlp/ipm/condensed.hpp
+ *                                           -> ipm::CondensedKkt (ipm/condensed.hpp:27-185)
+ * and INTEGRATION.md shows the bindings a maintainer adds.
+ *
+ * Memory modes (`mem` argument):
+ *   GN_MEM_HOST          pointers are host memory; the call copies H2D/D2H and
+ *                        returns after the result is on the host (the
+ *                        reference's std::span semantics).
+ *   GN_MEM_DEVICE        pointers are device memory on the context's device;
+ *                        the call synchronises the context stream and returns
+ *                        the evaluation status.
+ *   GN_MEM_DEVICE_ASYNC  device pointers, no synchronisation: kernels are only
+ *                        enqueued on the context stream; evaluation failures are
+ *                        latched on the device and reported by gn_ctx_status().
+ * OR-ing GN_IN_FULL into `mem` for a KKT created by gn_kkt_create_lifted() says
+ * the J/H inputs are the FULL (un-lifted) callback outputs; the lifted gather
+ * (lifted.hpp:249-264) is then fused into the KKT kernels.
+ */
+#ifndef GRIDNLP_B200_H
+#define GRIDNLP_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GN_ABI_VERSION 1
+
+enum {
+  GN_OK = 0,
+  GN_ERR_INVALID = 1,     /* bad shape/argument: the reference throws gridnlp::Error */
+  GN_ERR_EVAL = 2,        /* domain / non-finite result: the reference returns false */
+  GN_ERR_CUDA = 3,        /* CUDA runtime failure (no GPU, OOM, ...) */
+  GN_ERR_UNSUPPORTED = 4  /* input outside the supported OPF dialect (e.g. self-loop line) */
+};
+
+enum { GN_MEM_HOST = 0, GN_MEM_DEVICE = 1, GN_MEM_DEVICE_ASYNC = 2, GN_IN_FULL = 16 };
+
+/* Failure report.  For GN_ERR_EVAL, (pattern, record) is the lexicographically
+ * smallest failing (pattern id, record index) in registration order — the
+ * record the reference's EvalStatus names (pattern_model.hpp:16-25, 544-571). */
+typedef struct {
+  int32_t code;
+  int32_t pattern;
+  int32_t record;
+  char message[244];
+} gn_error;
+
+/* Per-unit network, the reference's NetworkData in SoA form (power/network.hpp:18-66).
+ * Element cross-references are 0-based indices.  line_smax / gen_ramp use +inf
+ * for "no rating" / "no ramp limit" exactly like the reference. */
+typedef struct {
+  int32_t n_bus, n_line, n_gen, n_load, reference_bus;
+  const double *bus_vmin, *bus_vmax, *vm_start, *va_start;               /* [n_bus]  */
+  const int32_t *line_from, *line_to;                                   /* [n_line] */
+  const double *line_g, *line_b, *line_smax, *line_amin, *line_amax;    /* [n_line] */
+  const int32_t *gen_bus;                                               /* [n_gen]  */
+  const double *gen_pmin, *gen_pmax, *gen_qmin, *gen_qmax, *gen_ramp;   /* [n_gen]  */
+  const double *gen_c2, *gen_c1, *gen_c0, *gen_pstart, *gen_qstart;     /* [n_gen]  */
+  const int32_t *load_bus;                                              /* [n_load] */
+  const double *load_p, *load_q;                                        /* [n_load] */
+} gn_network;
+
+/* Model sizes.  Full space = the NlpProblem the reference's PatternNlp exposes;
+ * lifted = after LiftedProblem's fixed-variable filter (lifted.hpp:25-100). */
+typedef struct {
+  int64_t n_vars, n_cons, jac_nnz, hess_nnz;       /* nlp.hpp:19-30 */
+  int64_t n_thermal, n_ramp_gens, periods;         /* OpfLayout (opf.hpp:29-30) */
+  int64_t n_free, jac_nnz_lifted, hess_nnz_lifted; /* valid after gn_lifted_create */
+} gn_sizes;
+
+typedef struct gn_ctx gn_ctx;
+typedef struct gn_kkt gn_kkt;
+
+int gn_abi_version(void);
+/* Number of CUDA kernels this library has launched (process-wide counter). */
+int64_t gn_launch_count(void);
+/* Reports whether a usable CUDA device is present (count into *n_devices). */
+int gn_device_count(int32_t* n_devices);
+
+/* ----------------------------------------------------------------- inputs */
+/* Demand multipliers, bit-identical to generate_load_profile
+ * (power/network.hpp:104-140; mt19937_64, top-53-bit mapping).  scale is
+ * periods x n_load, period-major (LoadProfile::scale).  Host-side utility. */
+int gn_load_profile(int32_t n_load, int32_t periods, double resolution_minutes,
+                    uint64_t seed, double amplitude, double noise, double* scale,
+                    gn_error* err);
+
+/* ---------------------------------------------------------------- context */
+/* Builds the multi-period OPF on the device: replaces
+ * power::build_multiperiod_opf (opf.hpp:100-355) + PatternModel::freeze
+ * (pattern_model.hpp:158-207) + ipm::PatternNlp (pattern_nlp.hpp:15-62).
+ * `scale` is the host T x n_load demand table (MultiPeriodCase::pd/qd,
+ * network.hpp:166-171).  Lines with from == to are rejected (GN_ERR_UNSUPPORTED). */
+int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale,
+                  int32_t device, gn_ctx** out, gn_error* err);
+int gn_ctx_destroy(gn_ctx* ctx);
+/* Use a caller-owned cudaStream_t (as void*) for every launch of this context. */
+int gn_ctx_set_stream(gn_ctx* ctx, void* cuda_stream);
+int gn_ctx_get_stream(gn_ctx* ctx, void** cuda_stream);
+/* Synchronises the stream, returns (and clears) the latched evaluation status. */
+int gn_ctx_status(gn_ctx* ctx, gn_error* err);
+int gn_ctx_sizes(gn_ctx* ctx, gn_sizes* out);
+
+/* NlpProblem::x_lower/x_upper/x_start/row_lower/row_upper (nlp.hpp:21-25).
+ * Host arrays of n_vars / n_cons; any pointer may be NULL. */
+int gn_ctx_bounds(gn_ctx* ctx, double* x_lower, double* x_upper, double* x_start,
+                  double* row_lower, double* row_upper);
+/* NlpProblem::jac_rows/jac_cols (nlp.hpp:27-28), freeze order. */
+int gn_jac_structure(gn_ctx* ctx, int32_t* rows, int32_t* cols, int mem);
+/* NlpProblem::hess_rows/hess_cols (nlp.hpp:29-30), (max,min) lower triangle. */
+int gn_hess_structure(gn_ctx* ctx, int32_t* rows, int32_t* cols, int mem);
+
+/* ------------------------------------------------------------- callbacks */
+/* NlpProblem::eval_f (nlp.hpp:32) / PatternModel::evaluate_objective
+ * (pattern_model.hpp:278-300).  In device modes `out` is a device double. */
+int gn_eval_f(gn_ctx* ctx, const double* x, double* out, int mem, gn_error* err);
+/* NlpProblem::eval_grad (nlp.hpp:33) / evaluate_gradient (:328-359). */
+int gn_eval_grad(gn_ctx* ctx, const double* x, double* out, int mem, gn_error* err);
+/* NlpProblem::eval_g (nlp.hpp:34) / evaluate_constraints (:302-326). */
+int gn_eval_g(gn_ctx* ctx, const double* x, double* out, int mem, gn_error* err);
+/* NlpProblem::eval_jac (nlp.hpp:35) / evaluate_jacobian (:361-388). */
+int gn_eval_jac(gn_ctx* ctx, const double* x, double* out, int mem, gn_error* err);
+/* NlpProblem::eval_hess (nlp.hpp:36-38) / evaluate_hessian (:393-436). */
+int gn_eval_hess(gn_ctx* ctx, const double* x, const double* row_weights,
+                 double obj_weight, double* out, int mem, gn_error* err);
+
+/* ---------------------------------------------------------------- lifted */
+/* LiftedProblem constructor filter (lifted.hpp:25-100): free map, slack
+ * boxes (relative relaxation), J/H picks.  Built on the device. */
+int gn_lifted_create(gn_ctx* ctx, double relax, gn_error* err);
+/* Any pointer may be NULL.  free_to_full[n_free]; jr/jc/jac_pick[jac_nnz_lifted];
+ * hr/hc/hess_pick[hess_nnz_lifted]; s_lower/s_upper[n_cons] (always host). */
+int gn_lifted_structure(gn_ctx* ctx, int32_t* free_to_full, int32_t* jac_rows,
+                        int32_t* jac_cols, int32_t* jac_pick, int32_t* hess_rows,
+                        int32_t* hess_cols, int32_t* hess_pick, double* s_lower,
+                        double* s_upper, int mem);
+/* LiftedProblem::eval_jac / eval_hess value gathers (lifted.hpp:249-264),
+ * full -> lifted, device or host. */
+int gn_lifted_gather_jac(gn_ctx* ctx, const double* jac_full, double* jac_lifted, int mem);
+int gn_lifted_gather_hess(gn_ctx* ctx, const double* hess_full, double* hess_lifted,
+                          int mem);
+
+/* ------------------------------------------------------------ condensed KKT */
+/* CondensedKkt constructor structure (condensed.hpp:29-90) on an arbitrary
+ * lifted COO (host arrays): CSR(A) + jac_slots, M = Hess U AtA U diag in CSC
+ * lower + hess/pair/diag slots — sorted on the device.  The LDL^T symbolic
+ * phase (ldlt.hpp:34-50) is not part of this object. */
+int gn_kkt_create(int32_t n, int32_t m, int64_t jac_nnz, const int32_t* jac_rows,
+                  const int32_t* jac_cols, int64_t hess_nnz, const int32_t* hess_rows,
+                  const int32_t* hess_cols, int32_t device, gn_kkt** out, gn_error* err);
+/* Same structure on the context's lifted problem (after gn_lifted_create);
+ * enables GN_IN_FULL inputs and the OPF-specialised assembly kernels.  The
+ * KKT shares the context's stream. */
+int gn_kkt_create_lifted(gn_ctx* ctx, gn_kkt** out, gn_error* err);
+int gn_kkt_destroy(gn_kkt* kkt);
+int gn_kkt_set_stream(gn_kkt* kkt, void* cuda_stream);
+/* dims = [dim, a_nnz, m_nnz, pair_count, jac_nnz, hess_nnz, n_rows] */
+int gn_kkt_dims(gn_kkt* kkt, int64_t* dims);
+/* jacobian_csr() / pattern() (condensed.hpp:93-95). Any pointer may be NULL. */
+int gn_kkt_structure(gn_kkt* kkt, int32_t* rowptr, int32_t* colidx, int32_t* colptr,
+                     int32_t* rowidx, int mem);
+/* The private slot maps jac_slots_/hess_slots_/pair_slots_/diag_slots_ (condensed.hpp:177-180). */
+int gn_kkt_slots(gn_kkt* kkt, int32_t* jac_slots, int32_t* hess_slots, int32_t* pair_slots,
+                 int32_t* diag_slots, int mem);
+/* CondensedKkt::set_jacobian (condensed.hpp:99-101): A = scatter(J). */
+int gn_kkt_set_jacobian(gn_kkt* kkt, const double* jac_vals, int mem);
+/* CondensedKkt::assemble (condensed.hpp:105-135): M = W + dw I + Sx + At D A,
+ * summed per slot in the reference's order (bit-exact given equal inputs). */
+int gn_kkt_assemble(gn_kkt* kkt, const double* hess_vals, const double* sigma_x,
+                    const double* sigma_s, double delta_w, double delta_c, int mem);
+/* jacobian_values() / values() (condensed.hpp:94-96). */
+int gn_kkt_values(gn_kkt* kkt, double* a_vals, double* m_vals, int mem);
+/* Selects the assembly algorithm: 0 = auto, 1 = generic contributor lists,
+ * 2 = OPF-specialised (lifted KKTs only). */
+int gn_kkt_set_algorithm(gn_kkt* kkt, int algo);
+
+/* compress_to_csc (sparse/matrix.hpp:45-81) of a host COO, on the device;
+ * returns the compressed nnz in *nnz_out.  colptr[ncols+1], rowidx/slot_map[nnz]. */
+int gn_compress_to_csc(int32_t nrows, int32_t ncols, int64_t nnz, const int32_t* rows,
+                       const int32_t* cols, int32_t* colptr, int32_t* rowidx,
+                       int32_t* slot_map, int32_t* nnz_out, gn_error* err);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GRIDNLP_B200_H */

@@ -1,0 +1,682 @@
+// C-ABI entry points (include/gridnlp_b200.h).  Host C++: argument checking,
+// memory modes, staging, error mapping.  All compute is in the kernels of
+// gn_ctx.cu / gn_eval.cu / gn_kkt.cu / gn_opf_kkt.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <random>
+
+#include "gn_kkt.cuh"
+
+using gnb::DBuf;
+using gnb::Error;
+
+namespace {
+
+int fail(gn_error* err, int code, const char* msg, int pattern = -1, int record = -1) {
+  if (err) {
+    err->code = code;
+    err->pattern = pattern;
+    err->record = record;
+    std::snprintf(err->message, sizeof err->message, "%s", msg);
+  }
+  return code;
+}
+int ok(gn_error* err) {
+  if (err) {
+    err->code = GN_OK;
+    err->pattern = -1;
+    err->record = -1;
+    err->message[0] = 0;
+  }
+  return GN_OK;
+}
+
+#define API_TRY try {
+#define API_CATCH(err)                                                   \
+  }                                                                      \
+  catch (const gnb::Error& e) {                                          \
+    return fail(err, e.code, e.what());                                  \
+  }                                                                      \
+  catch (const std::exception& e) {                                      \
+    return fail(err, GN_ERR_INVALID, e.what());                          \
+  }
+
+bool is_device(int mem) { return (mem & 0xf) != GN_MEM_HOST; }
+bool is_async(int mem) { return (mem & 0xf) == GN_MEM_DEVICE_ASYNC; }
+bool is_full(int mem) { return (mem & GN_IN_FULL) != 0; }
+
+void set_device(int dev) { GN_CK(cudaSetDevice(dev)); }
+
+template <class T>
+std::vector<T> vec(const T* p, int64_t n, const char* what) {
+  if (n > 0 && !p) throw Error(GN_ERR_INVALID, std::string("null array: ") + what);
+  return n > 0 ? std::vector<T>(p, p + n) : std::vector<T>();
+}
+
+// Read and clear the latched evaluation status.
+int take_status(gn_ctx* c, gn_error* err) {
+  unsigned long long st = gnb::kNoFail;
+  GN_CK(cudaMemcpyAsync(&st, c->status.p, sizeof st, cudaMemcpyDeviceToHost, c->stream));
+  GN_CK(cudaStreamSynchronize(c->stream));
+  if (st == gnb::kNoFail) return ok(err);
+  GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof st, c->stream));
+  GN_CK(cudaStreamSynchronize(c->stream));
+  return fail(err, GN_ERR_EVAL, "domain violation or non-finite result",
+              static_cast<int>(st >> 32), static_cast<int>(st & 0xffffffffu));
+}
+
+__global__ void k_gather(int64_t n, const int32_t* __restrict__ pick,
+                         const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[k] = in[pick[k]];
+}
+
+void copy_i32(int32_t* dst, const int32_t* src, int64_t n, int mem, cudaStream_t s) {
+  if (!dst || n <= 0) return;
+  GN_CK(cudaMemcpyAsync(dst, src, sizeof(int32_t) * n,
+                        is_device(mem) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+}
+
+}  // namespace
+
+extern "C" {
+
+int gn_abi_version(void) { return GN_ABI_VERSION; }
+int64_t gn_launch_count(void) { return gnb::launch_count(); }
+
+int gn_device_count(int32_t* n_devices) {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (n_devices) *n_devices = n;
+  return n > 0 ? GN_OK : GN_ERR_CUDA;
+}
+
+// generate_load_profile (network.hpp:104-140), bit-identical: mt19937_64 and
+// the top-53-bit mapping to [0,1).
+int gn_load_profile(int32_t n_load, int32_t periods, double resolution_minutes, uint64_t seed,
+                    double amplitude, double noise, double* scale, gn_error* err) {
+  if (periods < 1) return fail(err, GN_ERR_INVALID, "load profile: need at least one period");
+  if (resolution_minutes <= 0.0)
+    return fail(err, GN_ERR_INVALID, "load profile: resolution must be positive");
+  if (amplitude < 0.0 || amplitude >= 1.0)
+    return fail(err, GN_ERR_INVALID, "load profile: amplitude must lie in [0, 1)");
+  if (noise < 0.0) return fail(err, GN_ERR_INVALID, "load profile: noise must be nonnegative");
+  if (n_load > 0 && !scale) return fail(err, GN_ERR_INVALID, "null scale");
+  std::mt19937_64 rng(seed);
+  constexpr double kTwoPi = 6.283185307179586476925286766559;
+  for (int32_t t = 0; t < periods; ++t) {
+    const double phase = kTwoPi * static_cast<double>(t + 1) * resolution_minutes / 1440.0;
+    const double wave = 1.0 + amplitude * std::sin(phase);
+    for (int32_t j = 0; j < n_load; ++j) {
+      const double u01 = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+      const double u = 2.0 * u01 - 1.0;
+      scale[static_cast<size_t>(t) * n_load + j] = std::max(0.1, wave + noise * u);
+    }
+  }
+  return ok(err);
+}
+
+// ----------------------------------------------------------------- context
+int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale, int32_t device,
+                  gn_ctx** out, gn_error* err) {
+  if (!net || !out) return fail(err, GN_ERR_INVALID, "null argument");
+  *out = nullptr;
+  gn_ctx* c = nullptr;
+  API_TRY
+  const int32_t N = net->n_bus, L = net->n_line, G = net->n_gen, D = net->n_load;
+  const int32_t T = periods;
+  if (N < 0 || L < 0 || G < 0 || D < 0) throw Error(GN_ERR_INVALID, "negative element count");
+  if (net->reference_bus < 0 || net->reference_bus >= N)
+    throw Error(GN_ERR_INVALID, "opf: network has no reference bus");
+  if (T < 1) throw Error(GN_ERR_INVALID, "load profile: need at least one period");
+  if (D > 0 && !scale) throw Error(GN_ERR_INVALID, "opf: load profile does not match network loads");
+  set_device(device);
+  c = new gn_ctx();
+  c->device = device;
+  c->bus_vmin = vec(net->bus_vmin, N, "bus_vmin");
+  c->bus_vmax = vec(net->bus_vmax, N, "bus_vmax");
+  c->vm_start = vec(net->vm_start, N, "vm_start");
+  c->va_start = vec(net->va_start, N, "va_start");
+  c->line_from = vec(net->line_from, L, "line_from");
+  c->line_to = vec(net->line_to, L, "line_to");
+  c->line_g = vec(net->line_g, L, "line_g");
+  c->line_b = vec(net->line_b, L, "line_b");
+  c->line_smax = vec(net->line_smax, L, "line_smax");
+  c->line_amin = vec(net->line_amin, L, "line_amin");
+  c->line_amax = vec(net->line_amax, L, "line_amax");
+  c->gen_bus = vec(net->gen_bus, G, "gen_bus");
+  c->gen_pmin = vec(net->gen_pmin, G, "gen_pmin");
+  c->gen_pmax = vec(net->gen_pmax, G, "gen_pmax");
+  c->gen_qmin = vec(net->gen_qmin, G, "gen_qmin");
+  c->gen_qmax = vec(net->gen_qmax, G, "gen_qmax");
+  c->gen_ramp = vec(net->gen_ramp, G, "gen_ramp");
+  c->gen_c2 = vec(net->gen_c2, G, "gen_c2");
+  c->gen_c1 = vec(net->gen_c1, G, "gen_c1");
+  c->gen_c0 = vec(net->gen_c0, G, "gen_c0");
+  c->gen_pstart = vec(net->gen_pstart, G, "gen_pstart");
+  c->gen_qstart = vec(net->gen_qstart, G, "gen_qstart");
+  std::vector<int32_t> load_bus = vec(net->load_bus, D, "load_bus");
+  std::vector<double> load_p = vec(net->load_p, D, "load_p"), load_q = vec(net->load_q, D, "load_q");
+
+  // Reference validation (PatternModel::add_* throws on these; opf.hpp:105-108).
+  for (int32_t l = 0; l < L; ++l) {
+    const int32_t f = c->line_from[l], t = c->line_to[l];
+    if (f < 0 || f >= N || t < 0 || t >= N) throw Error(GN_ERR_INVALID, "line references unknown bus");
+    if (f == t)
+      throw Error(GN_ERR_UNSUPPORTED,
+                  "line " + std::to_string(l) + " is a self-loop (from == to), not supported");
+    if (c->line_amin[l] > c->line_amax[l])
+      throw Error(GN_ERR_INVALID, "constraint block angle: lower above upper");
+  }
+  for (int32_t g = 0; g < G; ++g) {
+    if (c->gen_bus[g] < 0 || c->gen_bus[g] >= N) throw Error(GN_ERR_INVALID, "generator references unknown bus");
+    if (c->gen_pmin[g] > c->gen_pmax[g]) throw Error(GN_ERR_INVALID, "variable block pg: lower above upper");
+    if (c->gen_qmin[g] > c->gen_qmax[g]) throw Error(GN_ERR_INVALID, "variable block qg: lower above upper");
+  }
+  for (int32_t n = 0; n < N; ++n)
+    if (c->bus_vmin[n] > c->bus_vmax[n]) throw Error(GN_ERR_INVALID, "variable block v: lower above upper");
+  for (int32_t j = 0; j < D; ++j)
+    if (load_bus[j] < 0 || load_bus[j] >= N) throw Error(GN_ERR_INVALID, "load references unknown bus");
+  const double inf = std::numeric_limits<double>::infinity();
+  for (int32_t l = 0; l < L; ++l)
+    if (c->line_smax[l] < inf) c->thermal_lines.push_back(l);
+  if (T >= 2)
+    for (int32_t g = 0; g < G; ++g)
+      if (c->gen_ramp[g] < inf) {
+        if (-c->gen_ramp[g] > c->gen_ramp[g])
+          throw Error(GN_ERR_INVALID, "constraint block ramp: lower above upper");
+        c->ramp_gens.push_back(g);
+      }
+  const int32_t LT = static_cast<int32_t>(c->thermal_lines.size());
+  const int32_t GR = static_cast<int32_t>(c->ramp_gens.size());
+  c->d = gnb::make_dims(T, N, L, G, D, LT, GR, net->reference_bus);
+
+  GN_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->own_stream = true;
+  cudaStream_t s = c->stream;
+
+  // SoA tables
+  std::vector<int32_t> l_therm(L, -1);
+  for (int32_t k = 0; k < LT; ++k) l_therm[c->thermal_lines[k]] = k;
+  c->lf.upload(c->line_from.data(), L, s);
+  c->lt.upload(c->line_to.data(), L, s);
+  c->lg.upload(c->line_g.data(), L, s);
+  c->lb.upload(c->line_b.data(), L, s);
+  c->l_therm.upload(l_therm.data(), L, s);
+  c->th_line.upload(c->thermal_lines.data(), LT, s);
+  c->gbus.upload(c->gen_bus.data(), G, s);
+  c->c2.upload(c->gen_c2.data(), G, s);
+  c->c1.upload(c->gen_c1.data(), G, s);
+  c->c0.upload(c->gen_c0.data(), G, s);
+  c->ramp_gen.upload(c->ramp_gens.data(), GR, s);
+  // demand pd(t,j) = load.p * scale[t*D+j] (network.hpp:166-171), entity-major
+  {
+    std::vector<double> pd(static_cast<size_t>(D) * T), qd(static_cast<size_t>(D) * T);
+    for (int32_t j = 0; j < D; ++j)
+      for (int32_t t = 0; t < T; ++t) {
+        const double sc = scale[static_cast<size_t>(t) * D + j];
+        pd[static_cast<size_t>(j) * T + t] = load_p[j] * sc;
+        qd[static_cast<size_t>(j) * T + t] = load_q[j] * sc;
+      }
+    c->pd.upload(pd.data(), pd.size(), s);
+    c->qd.upload(qd.data(), qd.size(), s);
+    GN_CK(cudaStreamSynchronize(s));
+  }
+  // bus incidence in the reference's accumulation order
+  {
+    std::vector<std::vector<int32_t>> bl(N), bg(N), bd(N);
+    for (int32_t l = 0; l < L; ++l) {
+      bl[c->line_to[l]].push_back(l << 1);          // to-record, s = +1
+      bl[c->line_from[l]].push_back((l << 1) | 1);  // from-record, s = -1
+    }
+    for (int32_t g = 0; g < G; ++g) bg[c->gen_bus[g]].push_back(g);
+    for (int32_t j = 0; j < D; ++j) bd[load_bus[j]].push_back(j);
+    auto flat = [&](std::vector<std::vector<int32_t>>& v, DBuf<int32_t>& ptr, DBuf<int32_t>& idx) {
+      std::vector<int32_t> p(N + 1, 0), x;
+      for (int32_t n = 0; n < N; ++n) {
+        p[n + 1] = p[n] + static_cast<int32_t>(v[n].size());
+        x.insert(x.end(), v[n].begin(), v[n].end());
+      }
+      ptr.upload(p.data(), p.size(), s);
+      idx.upload(x.data(), x.size(), s);
+      GN_CK(cudaStreamSynchronize(s));
+    };
+    flat(bl, c->bl_ptr, c->bl);
+    flat(bg, c->bg_ptr, c->bg);
+    flat(bd, c->bd_ptr, c->bd);
+  }
+  c->status.alloc(1);
+  GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof(unsigned long long), s));
+  c->fpart.alloc(gnb::fpart_size(c->d));
+  GN_CK(cudaStreamSynchronize(s));
+  *out = c;
+  return ok(err);
+  }
+  catch (const gnb::Error& e) {
+    delete c;
+    return fail(err, e.code, e.what());
+  }
+  catch (const std::exception& e) {
+    delete c;
+    return fail(err, GN_ERR_INVALID, e.what());
+  }
+}
+
+int gn_ctx_destroy(gn_ctx* c) {
+  if (!c) return GN_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  cudaStream_t s = c->stream;
+  const bool own = c->own_stream;
+  delete c;
+  if (own && s) cudaStreamDestroy(s);
+  return GN_OK;
+}
+
+int gn_ctx_set_stream(gn_ctx* c, void* stream) {
+  if (!c) return GN_ERR_INVALID;
+  API_TRY
+  set_device(c->device);
+  GN_CK(cudaStreamSynchronize(c->stream));
+  if (c->own_stream) cudaStreamDestroy(c->stream);
+  c->stream = static_cast<cudaStream_t>(stream);
+  c->own_stream = false;
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_ctx_get_stream(gn_ctx* c, void** stream) {
+  if (!c || !stream) return GN_ERR_INVALID;
+  *stream = c->stream;
+  return GN_OK;
+}
+
+int gn_ctx_status(gn_ctx* c, gn_error* err) {
+  if (!c) return fail(err, GN_ERR_INVALID, "null context");
+  API_TRY
+  set_device(c->device);
+  return take_status(c, err);
+  API_CATCH(err)
+}
+
+int gn_ctx_sizes(gn_ctx* c, gn_sizes* o) {
+  if (!c || !o) return GN_ERR_INVALID;
+  const auto& d = c->d;
+  o->n_vars = d.n;
+  o->n_cons = d.m;
+  o->jac_nnz = d.nj;
+  o->hess_nnz = d.nh;
+  o->n_thermal = d.LT;
+  o->n_ramp_gens = d.GR;
+  o->periods = d.T;
+  o->n_free = c->lifted ? c->n_free : -1;
+  o->jac_nnz_lifted = c->lifted ? c->nj_l : -1;
+  o->hess_nnz_lifted = c->lifted ? c->nh_l : -1;
+  return GN_OK;
+}
+
+int gn_ctx_bounds(gn_ctx* c, double* xl, double* xu, double* xs, double* rl, double* ru) {
+  if (!c) return GN_ERR_INVALID;
+  API_TRY
+  gnb::host_bounds(c, xl, xu, xs, rl, ru);
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+static int structure(gn_ctx* c, bool jac, int32_t* rows, int32_t* cols, int mem) {
+  if (!c) return GN_ERR_INVALID;
+  API_TRY
+  set_device(c->device);
+  const auto& d = c->d;
+  DBuf<int32_t> jr, jc, hr, hc;
+  jr.alloc(d.nj + 1); jc.alloc(d.nj + 1); hr.alloc(d.nh + 1); hc.alloc(d.nh + 1);
+  gnb::build_structure(c, jr.p, jc.p, hr.p, hc.p);
+  const int64_t n = jac ? d.nj : d.nh;
+  copy_i32(rows, jac ? jr.p : hr.p, n, mem, c->stream);
+  copy_i32(cols, jac ? jc.p : hc.p, n, mem, c->stream);
+  GN_CK(cudaStreamSynchronize(c->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+int gn_jac_structure(gn_ctx* c, int32_t* rows, int32_t* cols, int mem) {
+  return structure(c, true, rows, cols, mem);
+}
+int gn_hess_structure(gn_ctx* c, int32_t* rows, int32_t* cols, int mem) {
+  return structure(c, false, rows, cols, mem);
+}
+
+// ---------------------------------------------------------------- callbacks
+static int eval(gn_ctx* c, int mode, const double* x, const double* w, double ow, double* out,
+                int mem, gn_error* err) {
+  if (!c) return fail(err, GN_ERR_INVALID, "null context");
+  if (!x || !out || (mode == gnb::EV_H && !w)) return fail(err, GN_ERR_INVALID, "null array");
+  API_TRY
+  set_device(c->device);
+  const auto& d = c->d;
+  cudaStream_t s = c->stream;
+  const int64_t nout = mode == gnb::EV_F ? 1 : mode == gnb::EV_GRAD ? d.n
+                       : mode == gnb::EV_G ? d.m : mode == gnb::EV_J ? d.nj : d.nh;
+  const double* dx = x;
+  const double* dw = w;
+  double* dout = out;
+  if (!is_device(mem)) {
+    c->sx.upload(x, d.n, s);
+    dx = c->sx.p;
+    if (mode == gnb::EV_H) {
+      c->sw.upload(w, d.m, s);
+      dw = c->sw.p;
+    }
+    if (c->sout.n < static_cast<size_t>(nout)) c->sout.alloc(nout);
+    dout = c->sout.p;
+  }
+  if (!is_async(mem))
+    GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof(unsigned long long), s));
+  gnb::launch_eval(mode, d, c->net(), dx, dw, ow, dout, c->fpart.p, c->status.p, s);
+  if (is_async(mem)) return ok(err);
+  if (!is_device(mem))
+    GN_CK(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, s));
+  return take_status(c, err);
+  API_CATCH(err)
+}
+
+int gn_eval_f(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return eval(c, gnb::EV_F, x, nullptr, 0.0, out, mem, err);
+}
+int gn_eval_grad(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return eval(c, gnb::EV_GRAD, x, nullptr, 0.0, out, mem, err);
+}
+int gn_eval_g(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return eval(c, gnb::EV_G, x, nullptr, 0.0, out, mem, err);
+}
+int gn_eval_jac(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return eval(c, gnb::EV_J, x, nullptr, 0.0, out, mem, err);
+}
+int gn_eval_hess(gn_ctx* c, const double* x, const double* w, double ow, double* out, int mem,
+                 gn_error* err) {
+  return eval(c, gnb::EV_H, x, w, ow, out, mem, err);
+}
+
+// ------------------------------------------------------------------- lifted
+int gn_lifted_create(gn_ctx* c, double relax, gn_error* err) {
+  if (!c) return fail(err, GN_ERR_INVALID, "null context");
+  API_TRY
+  set_device(c->device);
+  gnb::build_lifted(c);
+  c->relax = relax;
+  return ok(err);
+  API_CATCH(err)
+}
+
+int gn_lifted_structure(gn_ctx* c, int32_t* free_to_full, int32_t* jr, int32_t* jc,
+                        int32_t* jpick, int32_t* hr, int32_t* hc, int32_t* hpick, double* sl,
+                        double* su, int mem) {
+  if (!c || !c->lifted) return GN_ERR_INVALID;
+  API_TRY
+  set_device(c->device);
+  cudaStream_t s = c->stream;
+  copy_i32(free_to_full, c->full_of_free.p, c->n_free, mem, s);
+  copy_i32(jr, c->jr_l.p, c->nj_l, mem, s);
+  copy_i32(jc, c->jc_l.p, c->nj_l, mem, s);
+  copy_i32(jpick, c->jpick.p, c->nj_l, mem, s);
+  copy_i32(hr, c->hr_l.p, c->nh_l, mem, s);
+  copy_i32(hc, c->hc_l.p, c->nh_l, mem, s);
+  copy_i32(hpick, c->hpick.p, c->nh_l, mem, s);
+  GN_CK(cudaStreamSynchronize(s));
+  if (sl || su) {  // slack boxes (lifted.hpp:160-176), host
+    const int32_t m = c->d.m;
+    std::vector<double> rl(m), ru(m);
+    gnb::host_bounds(c, nullptr, nullptr, nullptr, rl.data(), ru.data());
+    for (int32_t i = 0; i < m; ++i) {
+      const double lo = rl[i], hi = ru[i];
+      double a = lo, b = hi;
+      if (lo == hi) {
+        const double width = c->relax * std::max(1.0, std::abs(lo));
+        a = lo - width;
+        b = hi + width;
+      }
+      if (sl) sl[i] = a;
+      if (su) su[i] = b;
+    }
+  }
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+static int lifted_gather(gn_ctx* c, bool jac, const double* in, double* out, int mem) {
+  if (!c || !c->lifted || !in || !out) return GN_ERR_INVALID;
+  API_TRY
+  set_device(c->device);
+  cudaStream_t s = c->stream;
+  const int64_t nf = jac ? c->d.nj : c->d.nh, nl = jac ? c->nj_l : c->nh_l;
+  const int32_t* pick = jac ? c->jpick.p : c->hpick.p;
+  const double* din = in;
+  double* dout = out;
+  DBuf<double> a, b;
+  if (!is_device(mem)) {
+    a.upload(in, nf, s);
+    b.alloc(nl + 1);
+    din = a.p;
+    dout = b.p;
+  }
+  if (nl) {
+    k_gather<<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(nl, pick, din, dout);
+    gnb::count_launch();
+  }
+  if (!is_device(mem)) GN_CK(cudaMemcpyAsync(out, dout, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(s));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+int gn_lifted_gather_jac(gn_ctx* c, const double* in, double* out, int mem) {
+  return lifted_gather(c, true, in, out, mem);
+}
+int gn_lifted_gather_hess(gn_ctx* c, const double* in, double* out, int mem) {
+  return lifted_gather(c, false, in, out, mem);
+}
+
+// --------------------------------------------------------------------- KKT
+int gn_kkt_create(int32_t n, int32_t m, int64_t nj, const int32_t* jr, const int32_t* jc,
+                  int64_t nh, const int32_t* hr, const int32_t* hc, int32_t device,
+                  gn_kkt** out, gn_error* err) {
+  if (!out) return fail(err, GN_ERR_INVALID, "null argument");
+  *out = nullptr;
+  if (n < 0 || m < 0 || nj < 0 || nh < 0) return fail(err, GN_ERR_INVALID, "negative size");
+  if ((nj && (!jr || !jc)) || (nh && (!hr || !hc))) return fail(err, GN_ERR_INVALID, "null array");
+  gn_kkt* K = nullptr;
+  API_TRY
+  set_device(device);
+  K = new gn_kkt();
+  K->device = device;
+  K->n = n; K->m = m; K->nj = nj; K->nh = nh;
+  GN_CK(cudaStreamCreateWithFlags(&K->stream, cudaStreamNonBlocking));
+  K->own_stream = true;
+  DBuf<int32_t> djr, djc, dhr, dhc;
+  djr.upload(jr, nj, K->stream); djc.upload(jc, nj, K->stream);
+  dhr.upload(hr, nh, K->stream); dhc.upload(hc, nh, K->stream);
+  gnb::kkt_build(K, djr.p, djc.p, dhr.p, dhc.p);
+  *out = K;
+  return ok(err);
+  }
+  catch (const gnb::Error& e) {
+    if (K) gn_kkt_destroy(K);
+    return fail(err, e.code, e.what());
+  }
+  catch (const std::exception& e) {
+    if (K) gn_kkt_destroy(K);
+    return fail(err, GN_ERR_INVALID, e.what());
+  }
+}
+
+int gn_kkt_create_lifted(gn_ctx* c, gn_kkt** out, gn_error* err) {
+  if (!c || !out) return fail(err, GN_ERR_INVALID, "null argument");
+  if (!c->lifted) return fail(err, GN_ERR_INVALID, "gn_lifted_create must run first");
+  *out = nullptr;
+  gn_kkt* K = nullptr;
+  API_TRY
+  set_device(c->device);
+  K = new gn_kkt();
+  K->device = c->device;
+  K->ctx = c;
+  K->stream = c->stream;
+  K->own_stream = false;
+  K->n = c->n_free; K->m = c->d.m; K->nj = c->nj_l; K->nh = c->nh_l;
+  gnb::kkt_build(K, c->jr_l.p, c->jc_l.p, c->hr_l.p, c->hc_l.p);
+  *out = K;
+  return ok(err);
+  }
+  catch (const gnb::Error& e) {
+    if (K) gn_kkt_destroy(K);
+    return fail(err, e.code, e.what());
+  }
+  catch (const std::exception& e) {
+    if (K) gn_kkt_destroy(K);
+    return fail(err, GN_ERR_INVALID, e.what());
+  }
+}
+
+int gn_kkt_destroy(gn_kkt* K) {
+  if (!K) return GN_OK;
+  cudaSetDevice(K->device);
+  if (K->stream) cudaStreamSynchronize(K->stream);
+  cudaStream_t s = K->stream;
+  const bool own = K->own_stream;
+  delete K;
+  if (own && s) cudaStreamDestroy(s);
+  return GN_OK;
+}
+
+int gn_kkt_set_stream(gn_kkt* K, void* stream) {
+  if (!K) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  GN_CK(cudaStreamSynchronize(K->stream));
+  if (K->own_stream) cudaStreamDestroy(K->stream);
+  K->stream = static_cast<cudaStream_t>(stream);
+  K->own_stream = false;
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_dims(gn_kkt* K, int64_t* dims) {
+  if (!K || !dims) return GN_ERR_INVALID;
+  dims[0] = K->n; dims[1] = K->annz; dims[2] = K->mnnz; dims[3] = K->npair;
+  dims[4] = K->nj; dims[5] = K->nh; dims[6] = K->m;
+  return GN_OK;
+}
+
+int gn_kkt_structure(gn_kkt* K, int32_t* rowptr, int32_t* colidx, int32_t* colptr,
+                     int32_t* rowidx, int mem) {
+  if (!K) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  copy_i32(rowptr, K->A.ptr.p, (int64_t)K->m + 1, mem, K->stream);
+  copy_i32(colidx, K->A.idx.p, K->annz, mem, K->stream);
+  copy_i32(colptr, K->M.ptr.p, (int64_t)K->n + 1, mem, K->stream);
+  copy_i32(rowidx, K->M.idx.p, K->mnnz, mem, K->stream);
+  GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_slots(gn_kkt* K, int32_t* js, int32_t* hs, int32_t* ps, int32_t* ds, int mem) {
+  if (!K) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  copy_i32(js, K->A.slot.p, K->nj, mem, K->stream);
+  copy_i32(hs, K->M.slot.p, K->nh, mem, K->stream);
+  copy_i32(ps, K->M.slot.p + K->nh, K->npair, mem, K->stream);
+  copy_i32(ds, K->M.slot.p + K->nh + K->npair, K->n, mem, K->stream);
+  GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_set_jacobian(gn_kkt* K, const double* jv, int mem) {
+  if (!K || !jv) return GN_ERR_INVALID;
+  if (is_full(mem) && !K->ctx) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  const double* dj = jv;
+  if (!is_device(mem)) {
+    const int64_t n = is_full(mem) ? K->ctx->d.nj : K->nj;
+    K->sj.upload(jv, n, K->stream);
+    dj = K->sj.p;
+  }
+  gnb::kkt_set_jacobian(K, dj, is_full(mem));
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_assemble(gn_kkt* K, const double* hv, const double* sx, const double* ss, double dw,
+                    double dc, int mem) {
+  if (!K || !hv || !sx || !ss) return GN_ERR_INVALID;
+  if (is_full(mem) && !K->ctx) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  const double *dh = hv, *dsx = sx, *dss = ss;
+  if (!is_device(mem)) {
+    const int64_t n = is_full(mem) ? K->ctx->d.nh : K->nh;
+    K->sh.upload(hv, n, K->stream);
+    K->ssx.upload(sx, K->n, K->stream);
+    K->sss.upload(ss, K->m, K->stream);
+    dh = K->sh.p; dsx = K->ssx.p; dss = K->sss.p;
+  }
+  gnb::kkt_assemble(K, dh, dsx, dss, dw, dc, is_full(mem));
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
+  if (!K) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  const auto kind = is_device(mem) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  if (av && K->annz) GN_CK(cudaMemcpyAsync(av, K->avals.p, sizeof(double) * K->annz, kind, K->stream));
+  if (mv && K->mnnz) GN_CK(cudaMemcpyAsync(mv, K->mvals.p, sizeof(double) * K->mnnz, kind, K->stream));
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_set_algorithm(gn_kkt* K, int algo) {
+  if (!K || algo < 0 || algo > 2) return GN_ERR_INVALID;
+  if (algo == 2 && !K->ctx) return GN_ERR_INVALID;
+  K->algo = algo;
+  return GN_OK;
+}
+
+int gn_compress_to_csc(int32_t nrows, int32_t ncols, int64_t nnz, const int32_t* rows,
+                       const int32_t* cols, int32_t* colptr, int32_t* rowidx, int32_t* slot_map,
+                       int32_t* nnz_out, gn_error* err) {
+  if (nnz < 0 || nrows < 0 || ncols < 0) return fail(err, GN_ERR_INVALID, "negative size");
+  API_TRY
+  cudaStream_t s = nullptr;
+  GN_CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  struct Guard { cudaStream_t s; ~Guard() { cudaStreamDestroy(s); } } guard{s};
+  for (int64_t k = 0; k < nnz; ++k)
+    if (rows[k] < 0 || rows[k] >= nrows || cols[k] < 0 || cols[k] >= ncols)
+      throw Error(GN_ERR_INVALID, "compress_to_csc: coordinate out of range");
+  std::vector<uint64_t> key(static_cast<size_t>(nnz));
+  for (int64_t k = 0; k < nnz; ++k) key[k] = (uint64_t)cols[k] * (uint64_t)nrows + (uint64_t)rows[k];
+  DBuf<uint64_t> dk;
+  dk.upload(key.data(), key.size(), s);
+  gnb::Csc out;
+  gnb::compress_keys(dk.p, nnz, nrows, ncols, out, s);
+  if (colptr) GN_CK(cudaMemcpyAsync(colptr, out.ptr.p, sizeof(int32_t) * (ncols + 1), cudaMemcpyDeviceToHost, s));
+  if (rowidx && out.nnz) GN_CK(cudaMemcpyAsync(rowidx, out.idx.p, sizeof(int32_t) * out.nnz, cudaMemcpyDeviceToHost, s));
+  if (slot_map && nnz) GN_CK(cudaMemcpyAsync(slot_map, out.slot.p, sizeof(int32_t) * nnz, cudaMemcpyDeviceToHost, s));
+  GN_CK(cudaStreamSynchronize(s));
+  if (nnz_out) *nnz_out = out.nnz;
+  return ok(err);
+  API_CATCH(err)
+}
+
+}  // extern "C"

@@ -1,0 +1,448 @@
+// Per-element NLP callbacks: one kernel per element class (line x period,
+// generator x period, rated-line x period, ramping-generator x step,
+// bus x period), each writing its patterns' COO slots in the reference's
+// freeze order.  Closed-form derivatives of the 12 OPF patterns
+// replace the reference's interpreted tape AD
+// (model/tape.hpp); value expressions keep the tape's operation order and
+// the library is built with -fmad=false, so g and J agree with the reference
+// to the last bit except where CUDA's sin/cos differ from glibc's by an ulp.
+//
+//   evaluate_objective   pattern_model.hpp:278-300
+//   evaluate_constraints pattern_model.hpp:302-326
+//   evaluate_gradient    pattern_model.hpp:328-359
+//   evaluate_jacobian    pattern_model.hpp:361-388
+//   evaluate_hessian     pattern_model.hpp:393-436 (w == 0 -> zeros, :409-412)
+#include "gn_eval.cuh"
+
+namespace gnb {
+
+constexpr int kBS = 256;  // records per block (one per thread)
+
+__device__ __forceinline__ void report(unsigned long long* st, int pid, int64_t rec) {
+  atomicMin(st, (static_cast<unsigned long long>(pid) << 32) |
+                    static_cast<unsigned long long>(rec));
+}
+
+// Block-cooperative contiguous store of `nb` records x K values staged in smem:
+// the strided per-record writes become one coalesced stream.
+template <int K>
+__device__ __forceinline__ void stage_out(double* sm, const double (&v)[K], bool valid,
+                                          double* __restrict__ out, int nb) {
+  if (valid) {
+#pragma unroll
+    for (int s = 0; s < K; ++s) sm[threadIdx.x * K + s] = v[s];
+  }
+  __syncthreads();
+  const int total = nb * K;
+  for (int i = threadIdx.x; i < total; i += kBS) out[i] = sm[i];
+  __syncthreads();
+}
+
+// Contiguous region of nb records x K slots holding per-slot constants.
+template <int K>
+__device__ __forceinline__ void const_out(double* __restrict__ out, int nb,
+                                          const double (&c)[K]) {
+  const int total = nb * K;
+  for (int i = threadIdx.x; i < total; i += kBS) out[i] = c[i % K];
+}
+
+struct LineVals {
+  double vf, vt, Cs, Sn, vfvt, c, s;
+};
+
+// ---------------------------------------------------------------- lines
+// Patterns 1, 2 (balance-flow J/H), 7, 8 (flow definitions), 10 (angle).
+template <int MODE>
+__global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const double* __restrict__ x,
+                                              const double* __restrict__ w,
+                                              double* __restrict__ out,
+                                              unsigned long long* st) {
+  __shared__ double sm[kBS * 15];
+  const int64_t nrec = (int64_t)d.L * d.T;
+  const int64_t r0 = (int64_t)blockIdx.x * kBS;
+  const int64_t r = r0 + threadIdx.x;
+  const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
+  const bool valid = r < nrec;
+  double p = 0, q = 0, G = 0, B = 0, vf = 0, vt = 0, thf = 0, tht = 0;
+  if (valid) {
+    const int32_t l = (int32_t)(r / d.T), t = (int32_t)(r - (int64_t)l * d.T);
+    const int32_t f = __ldg(net.lf + l), to = __ldg(net.lt + l);
+    G = __ldg(net.lg + l);
+    B = __ldg(net.lb + l);
+    p = x[d.p0 + r];
+    q = x[d.q0 + r];
+    vf = x[d.v0 + (int64_t)f * d.T + t];
+    vt = x[d.v0 + (int64_t)to * d.T + t];
+    thf = x[d.th0 + (int64_t)f * d.T + t];
+    tht = x[d.th0 + (int64_t)to * d.T + t];
+  }
+  const double dth = thf - tht;
+  double sn, cs;
+  sincos(dth, &sn, &cs);
+  const double vfvt = vf * vt;
+  const double Cs = G * cs + B * sn;   // tape node 17 of flow_p
+  const double Sn = G * sn - B * cs;   // tape node 18 of flow_q
+
+  if constexpr (MODE == EV_G) {
+    if (valid) {
+      // opf.hpp:312-318 in tape order
+      const double gp = p - (G * (vf * vf) - vfvt * Cs);
+      const double gq = q - ((-B) * (vf * vf) - vfvt * Sn);
+      const double ga = thf - tht;
+      out[d.flow_p0 + r] = gp;
+      out[d.flow_q0 + r] = gq;
+      out[d.ang0 + r] = ga;
+      if (!isfinite(gp)) report(st, d.pid[K_FLOW_P], r);
+      if (!isfinite(gq)) report(st, d.pid[K_FLOW_Q], r);
+      if (!isfinite(ga)) report(st, d.pid[K_ANGLE], r);
+    }
+  } else if constexpr (MODE == EV_J) {
+    // balance flows: (+1 to-record, -1 from-record); angle: (1, -1)
+    const double pm[2] = {1.0, -1.0};
+    const_out<2>(out + d.jac_off[K_BAL_P_FLOW] + 2 * r0, nb, pm);
+    const_out<2>(out + d.jac_off[K_BAL_Q_FLOW] + 2 * r0, nb, pm);
+    const_out<2>(out + d.jac_off[K_ANGLE] + 2 * r0, nb, pm);
+    // flow_p reverse sweep (tape order): xbar = [1, Cs*vt + (-2G)*vf, Cs*vf, a, -a]
+    const double a11 = (vfvt * B) * cs - (vfvt * G) * sn;
+    double jp[5] = {1.0, Cs * vt + ((-G) * 2.0) * vf, Cs * vf, a11, -a11};
+    // flow_q: xbar = [1, Sn*vt + (2B)*vf, Sn*vf, a, -a]
+    const double a12 = (vfvt * B) * sn + (vfvt * G) * cs;
+    double jq[5] = {1.0, Sn * vt + (B * 2.0) * vf, Sn * vf, a12, -a12};
+    if (valid) {
+      bool okp = true, okq = true;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        okp = okp && isfinite(jp[i]);
+        okq = okq && isfinite(jq[i]);
+      }
+      if (!okp) report(st, d.pid[K_FLOW_P], r);
+      if (!okq) report(st, d.pid[K_FLOW_Q], r);
+    }
+    stage_out<5>(sm, jp, valid, out + d.jac_off[K_FLOW_P] + 5 * r0, nb);
+    stage_out<5>(sm, jq, valid, out + d.jac_off[K_FLOW_Q] + 5 * r0, nb);
+  } else {  // EV_H
+    const double z2[2] = {0.0, 0.0};
+    const double z3[3] = {0.0, 0.0, 0.0};
+    const_out<2>(out + d.hess_off[K_BAL_P_FLOW] + 2 * r0, nb, z2);
+    const_out<2>(out + d.hess_off[K_BAL_Q_FLOW] + 2 * r0, nb, z2);
+    const_out<3>(out + d.hess_off[K_ANGLE] + 3 * r0, nb, z3);
+    double wp = 0.0, wq = 0.0;
+    if (valid) {
+      wp = w[d.flow_p0 + r];
+      wq = w[d.flow_q0 + r];
+    }
+    // Lower triangle, local order (0,0)(1,0)..(4,0)(1,1)..(4,1)(2,2)..(4,4);
+    // fields [flow, v_f, v_t, th_f, th_t].  Row/column 0 is identically 0.
+    double hp[15], hq[15];
+    {
+      const double a = wp;
+      const double tS = vt * Sn, fS = vf * Sn, ffC = vfvt * Cs;
+      hp[0] = 0.0; hp[1] = 0.0; hp[2] = 0.0; hp[3] = 0.0; hp[4] = 0.0;
+      hp[5] = ((-2.0) * G) * a;   // (v_f, v_f)
+      hp[6] = Cs * a;             // (v_t, v_f)
+      hp[7] = -(tS * a);          // (th_f, v_f)
+      hp[8] = tS * a;             // (th_t, v_f)
+      hp[9] = 0.0;                // (v_t, v_t)
+      hp[10] = -(fS * a);         // (th_f, v_t)
+      hp[11] = fS * a;            // (th_t, v_t)
+      hp[12] = -(ffC * a);        // (th_f, th_f)
+      hp[13] = ffC * a;           // (th_t, th_f)
+      hp[14] = -(ffC * a);        // (th_t, th_t)
+      if (a == 0.0) {
+#pragma unroll
+        for (int i = 0; i < 15; ++i) hp[i] = 0.0;
+      }
+    }
+    {
+      const double a = wq;
+      const double tC = vt * Cs, fC = vf * Cs, ffS = vfvt * Sn;
+      hq[0] = 0.0; hq[1] = 0.0; hq[2] = 0.0; hq[3] = 0.0; hq[4] = 0.0;
+      hq[5] = (2.0 * B) * a;
+      hq[6] = Sn * a;
+      hq[7] = tC * a;
+      hq[8] = -(tC * a);
+      hq[9] = 0.0;
+      hq[10] = fC * a;
+      hq[11] = -(fC * a);
+      hq[12] = -(ffS * a);
+      hq[13] = ffS * a;
+      hq[14] = -(ffS * a);
+      if (a == 0.0) {
+#pragma unroll
+        for (int i = 0; i < 15; ++i) hq[i] = 0.0;
+      }
+    }
+    if (valid) {
+      bool okp = true, okq = true;
+#pragma unroll
+      for (int i = 0; i < 15; ++i) {
+        okp = okp && isfinite(hp[i]);
+        okq = okq && isfinite(hq[i]);
+      }
+      if (!okp) report(st, d.pid[K_FLOW_P], r);
+      if (!okq) report(st, d.pid[K_FLOW_Q], r);
+    }
+    stage_out<15>(sm, hp, valid, out + d.hess_off[K_FLOW_P] + 15 * r0, nb);
+    stage_out<15>(sm, hq, valid, out + d.hess_off[K_FLOW_Q] + 15 * r0, nb);
+  }
+}
+
+// ------------------------------------------------------------- generators
+// Pattern 0 (cost: f, grad, H) and 3, 4 (injections: J = 1, H = 0).
+template <int MODE>
+__global__ void __launch_bounds__(kBS) k_gen(OpfDims d, DevNet net, const double* __restrict__ x,
+                                             double ow, double* __restrict__ out,
+                                             double* __restrict__ fpart,
+                                             unsigned long long* st) {
+  __shared__ double red[kBS];
+  const int64_t nrec = (int64_t)d.G * d.T;
+  const int64_t r0 = (int64_t)blockIdx.x * kBS;
+  const int64_t r = r0 + threadIdx.x;
+  const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
+  const bool valid = r < nrec;
+  double pg = 0.0, c2 = 0.0, c1 = 0.0, c0 = 0.0;
+  if (valid) {
+    const int32_t g = (int32_t)(r / d.T);
+    pg = x[d.pg0 + r];
+    c2 = __ldg(net.c2 + g);
+    c1 = __ldg(net.c1 + g);
+    c0 = __ldg(net.c0 + g);
+  }
+  if constexpr (MODE == EV_F) {
+    // ((c2*pg^2) + (c1*pg)) + c0, opf.hpp:245; partial sums in a fixed tree
+    double v = 0.0;
+    if (valid) {
+      v = (c2 * (pg * pg) + c1 * pg) + c0;
+      if (!isfinite(v)) report(st, d.pid[K_COST], r);
+    }
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = kBS / 2; s > 0; s >>= 1) {
+      if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) fpart[blockIdx.x] = red[0];
+  } else if constexpr (MODE == EV_GRAD) {
+    if (valid) {
+      const double gr = c1 + (c2 * 2.0) * pg;  // reverse sweep order
+      out[d.pg0 + r] = gr;
+      if (!isfinite(gr)) report(st, d.pid[K_COST], r);
+    }
+  } else if constexpr (MODE == EV_J) {
+    if (valid) {
+      out[d.jac_off[K_BAL_P_INJ] + r] = 1.0;
+      out[d.jac_off[K_BAL_Q_INJ] + r] = 1.0;
+    }
+  } else if constexpr (MODE == EV_H) {
+    if (valid) {
+      double h = 0.0;
+      if (ow != 0.0) {
+        h = (ow * c2) * 2.0;
+        if (!isfinite(h) || !isfinite(pg)) report(st, d.pid[K_COST], r);
+      }
+      out[d.hess_off[K_COST] + r] = h;
+      out[d.hess_off[K_BAL_P_INJ] + r] = 0.0;
+      out[d.hess_off[K_BAL_Q_INJ] + r] = 0.0;
+    }
+  }
+  (void)nb;
+}
+
+// Fixed-order final sum of the objective partials (one block).
+__global__ void k_sum_partials(const double* __restrict__ part, int n, double* out) {
+  __shared__ double red[kBS];
+  double v = 0.0;
+  // each thread sums a contiguous chunk in order, then a fixed tree
+  const int chunk = (n + kBS - 1) / kBS;
+  const int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+  for (int i = lo; i < hi; ++i) v += part[i];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = kBS / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
+// ----------------------------------------------------------------- thermal
+// Pattern 9: p^2 + q^2 over rated lines (opf.hpp:323-332).
+template <int MODE>
+__global__ void __launch_bounds__(kBS) k_thermal(OpfDims d, DevNet net,
+                                                 const double* __restrict__ x,
+                                                 const double* __restrict__ w,
+                                                 double* __restrict__ out,
+                                                 unsigned long long* st) {
+  __shared__ double sm[kBS * 3];
+  const int64_t nrec = (int64_t)d.LT * d.T;
+  const int64_t r0 = (int64_t)blockIdx.x * kBS;
+  const int64_t r = r0 + threadIdx.x;
+  const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
+  const bool valid = r < nrec;
+  double p = 0.0, q = 0.0;
+  if (valid) {
+    const int32_t k = (int32_t)(r / d.T), t = (int32_t)(r - (int64_t)k * d.T);
+    const int32_t l = __ldg(net.th_line + k);
+    p = x[d.p0 + (int64_t)l * d.T + t];
+    q = x[d.q0 + (int64_t)l * d.T + t];
+  }
+  if constexpr (MODE == EV_G) {
+    if (valid) {
+      const double v = p * p + q * q;
+      out[d.therm0 + r] = v;
+      if (!isfinite(v)) report(st, d.pid[K_THERMAL], r);
+    }
+  } else if constexpr (MODE == EV_J) {
+    double j[2] = {2.0 * p, 2.0 * q};
+    if (valid && !(isfinite(j[0]) && isfinite(j[1]))) report(st, d.pid[K_THERMAL], r);
+    stage_out<2>(sm, j, valid, out + d.jac_off[K_THERMAL] + 2 * r0, nb);
+  } else {
+    const double a = valid ? w[d.therm0 + r] : 0.0;
+    double h[3] = {0.0, 0.0, 0.0};
+    if (a != 0.0) {
+      h[0] = (a * 2.0);
+      h[2] = (a * 2.0);
+      if (valid && !(isfinite(h[0]) && isfinite(p) && isfinite(q)))
+        report(st, d.pid[K_THERMAL], r);
+    }
+    stage_out<3>(sm, h, valid, out + d.hess_off[K_THERMAL] + 3 * r0, nb);
+  }
+}
+
+// -------------------------------------------------------------------- ramp
+// Pattern 11: pg(g,t) - pg(g,t-1), t = 1..T-1 (opf.hpp:343-351).
+template <int MODE>
+__global__ void __launch_bounds__(kBS) k_ramp(OpfDims d, DevNet net,
+                                              const double* __restrict__ x,
+                                              double* __restrict__ out,
+                                              unsigned long long* st) {
+  const int32_t Tm = d.T - 1;
+  const int64_t nrec = (int64_t)d.GR * Tm;
+  const int64_t r0 = (int64_t)blockIdx.x * kBS;
+  const int64_t r = r0 + threadIdx.x;
+  const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
+  if constexpr (MODE == EV_G) {
+    if (r < nrec) {
+      const int32_t k = (int32_t)(r / Tm), s = (int32_t)(r - (int64_t)k * Tm);
+      const int32_t g = __ldg(net.ramp_gen + k);
+      const int64_t i = d.pg0 + (int64_t)g * d.T + s + 1;
+      const double v = x[i] - x[i - 1];
+      out[d.ramp0 + r] = v;
+      if (!isfinite(v)) report(st, d.pid[K_RAMP], r);
+    }
+  } else if constexpr (MODE == EV_J) {
+    const double pm[2] = {1.0, -1.0};
+    const_out<2>(out + d.jac_off[K_RAMP] + 2 * r0, nb, pm);
+  } else {
+    const double z3[3] = {0.0, 0.0, 0.0};
+    const_out<3>(out + d.hess_off[K_RAMP] + 3 * r0, nb, z3);
+  }
+}
+
+// --------------------------------------------------------------------- bus
+// Balance rows (n,t): 0 (+) lines by ascending l (+) generators (+) loads —
+// exactly the order the reference's pattern-by-pattern `g[row] += contrib`
+// produces (pattern_model.hpp:307-324), so the sums are bit-identical.
+__global__ void __launch_bounds__(kBS) k_bus(OpfDims d, DevNet net, const double* __restrict__ x,
+                                             double* __restrict__ g, unsigned long long* st) {
+  const int64_t r = (int64_t)blockIdx.x * kBS + threadIdx.x;
+  if (r >= (int64_t)d.N * d.T) return;
+  const int32_t n = (int32_t)(r / d.T), t = (int32_t)(r - (int64_t)n * d.T);
+  double ap = 0.0, aq = 0.0;
+  const int32_t b0 = __ldg(net.bl_ptr + n), b1 = __ldg(net.bl_ptr + n + 1);
+  for (int32_t i = b0; i < b1; ++i) {
+    const int32_t e = __ldg(net.bl + i);
+    const int32_t l = e >> 1, side = e & 1;
+    const int64_t lt = (int64_t)l * d.T + t;
+    const double p = x[d.p0 + lt], q = x[d.q0 + lt];
+    const double sp = side ? -p : p, sq = side ? -q : q;  // real(0)*var(0), s = -/+1
+    ap += sp;
+    aq += sq;
+    if (!isfinite(sp)) report(st, d.pid[K_BAL_P_FLOW], 2 * lt + side);
+    if (!isfinite(sq)) report(st, d.pid[K_BAL_Q_FLOW], 2 * lt + side);
+  }
+  const int32_t g0 = __ldg(net.bg_ptr + n), g1 = __ldg(net.bg_ptr + n + 1);
+  for (int32_t i = g0; i < g1; ++i) {
+    const int64_t gt = (int64_t)__ldg(net.bg + i) * d.T + t;
+    const double pg = x[d.pg0 + gt], qg = x[d.qg0 + gt];
+    ap += pg;
+    aq += qg;
+    if (!isfinite(pg)) report(st, d.pid[K_BAL_P_INJ], gt);
+    if (!isfinite(qg)) report(st, d.pid[K_BAL_Q_INJ], gt);
+  }
+  const int32_t l0 = __ldg(net.bd_ptr + n), l1 = __ldg(net.bd_ptr + n + 1);
+  for (int32_t i = l0; i < l1; ++i) {
+    const int64_t jt = (int64_t)__ldg(net.bd + i) * d.T + t;
+    const double pd = -net.pd[jt], qd = -net.qd[jt];
+    ap += pd;
+    aq += qd;
+    if (!isfinite(pd)) report(st, d.pid[K_BAL_P_LOAD], jt);
+    if (!isfinite(qd)) report(st, d.pid[K_BAL_Q_LOAD], jt);
+  }
+  g[d.bal_p0 + r] = ap;
+  g[d.bal_q0 + r] = aq;
+}
+
+// ------------------------------------------------------------------ driver
+static unsigned nblk(int64_t n) { return (unsigned)((n + kBS - 1) / kBS); }
+
+void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
+                 const double* w, double ow, double* out, double* fpart,
+                 unsigned long long* st, cudaStream_t s) {
+  const int64_t nl = (int64_t)d.L * d.T, ng = (int64_t)d.G * d.T, nt = (int64_t)d.LT * d.T,
+                nr = d.pid[K_RAMP] >= 0 ? (int64_t)d.GR * (d.T - 1) : 0,
+                nb = (int64_t)d.N * d.T;
+  switch (mode) {
+    case EV_F: {
+      const unsigned blocks = nblk(ng);
+      if (blocks) {
+        k_gen<EV_F><<<blocks, kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
+        count_launch();
+        k_sum_partials<<<1, kBS, 0, s>>>(fpart, (int)blocks, out);
+        count_launch();
+      } else {
+        GN_CK(cudaMemsetAsync(out, 0, sizeof(double), s));
+      }
+      break;
+    }
+    case EV_GRAD:
+      // zero the non-generator blocks, then the cost gradient over pg
+      if (d.n > d.qg0) GN_CK(cudaMemsetAsync(out + d.qg0, 0, sizeof(double) * (d.n - d.qg0), s));
+      if (ng) { k_gen<EV_GRAD><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st); count_launch(); }
+      break;
+    case EV_G:
+      if (nb) { k_bus<<<nblk(nb), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
+      if (nl) { k_line<EV_G><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
+      if (nt) { k_thermal<EV_G><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
+      if (nr) { k_ramp<EV_G><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
+      break;
+    case EV_J:
+    case EV_H:
+      if (nl) {
+        if (mode == EV_J) k_line<EV_J><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st);
+        else k_line<EV_H><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st);
+        count_launch();
+      }
+      if (ng) {
+        if (mode == EV_J) k_gen<EV_J><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
+        else k_gen<EV_H><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
+        count_launch();
+      }
+      if (nt) {
+        if (mode == EV_J) k_thermal<EV_J><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st);
+        else k_thermal<EV_H><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st);
+        count_launch();
+      }
+      if (nr) {
+        if (mode == EV_J) k_ramp<EV_J><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st);
+        else k_ramp<EV_H><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st);
+        count_launch();
+      }
+      break;
+  }
+  GN_CK(cudaGetLastError());
+}
+
+size_t fpart_size(const OpfDims& d) { return nblk((int64_t)d.G * d.T) + 1; }
+
+}  // namespace gnb

@@ -1,0 +1,21 @@
+#pragma once
+#include "gn_internal.cuh"
+
+namespace gnb {
+
+enum EvalMode { EV_F = 0, EV_GRAD = 1, EV_G = 2, EV_J = 3, EV_H = 4 };
+
+// Enqueue one callback on stream s; failures are latched into *st.
+void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
+                 const double* w, double ow, double* out, double* fpart,
+                 unsigned long long* st, cudaStream_t s);
+size_t fpart_size(const OpfDims& d);
+
+void build_structure(gn_ctx* c, int32_t* jr, int32_t* jc, int32_t* hr, int32_t* hc);
+void build_lifted(gn_ctx* c);
+void host_bounds(const gn_ctx* c, double* xl, double* xu, double* xs, double* rl,
+                 double* ru);
+int32_t exclusive_scan(const int32_t* flag, int32_t* pos, int64_t n, cudaStream_t s);
+int64_t launch_count();
+
+}  // namespace gnb

@@ -1,0 +1,45 @@
+#pragma once
+#include "gn_eval.cuh"
+
+namespace gnb {
+
+// A compressed (CSC-ordered) pattern plus its scatter/gather maps.
+struct Csc {
+  int32_t nnz = 0;
+  DBuf<int32_t> ptr;   // [ncols + 1]
+  DBuf<int32_t> idx;   // [nnz] row index per slot
+  DBuf<int32_t> seg;   // [nnz + 1] first sorted position of each slot
+  DBuf<int32_t> src;   // [coo] COO index at each sorted position (contributor lists)
+  DBuf<int32_t> slot;  // [coo] slot_map: compressed slot of each COO entry
+};
+
+// Sort 64-bit (col * nrows + row) keys and compress (matrix.hpp:45-81).  keys is clobbered.
+void compress_keys(uint64_t* keys, int64_t nnz, int32_t nrows, int32_t ncols, Csc& out,
+                   cudaStream_t s);
+
+}  // namespace gnb
+
+struct gn_kkt {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  gn_ctx* ctx = nullptr;  // set for gn_kkt_create_lifted
+  int32_t n = 0, m = 0;
+  int64_t nj = 0, nh = 0, npair = 0;
+  int32_t annz = 0, mnnz = 0;
+  int algo = 0;
+  gnb::Csc A;                    // CSR(A) (as CSC of A^T): ptr = rowptr, idx = colidx, slot = jac_slots
+  gnb::Csc M;                    // M lower CSC: ptr = colptr, idx = rowidx, slot = [hess|pair|diag]
+  gnb::DBuf<int32_t> pka, pkb;   // per pair: CSR positions ka, kb
+  gnb::DBuf<int32_t> arow;       // per CSR(A) entry: its row
+  gnb::DBuf<double> avals, mvals;
+  gnb::DBuf<double> sj, sh, ssx, sss;  // host-mode staging
+};
+
+namespace gnb {
+void kkt_build(gn_kkt* K, const int32_t* jr, const int32_t* jc, const int32_t* hr,
+               const int32_t* hc);
+void kkt_set_jacobian(gn_kkt* K, const double* J, bool full);
+void kkt_assemble(gn_kkt* K, const double* H, const double* sx, const double* ss, double dw,
+                  double dc, bool full);
+}  // namespace gnb

@@ -1,0 +1,329 @@
+"""Python mirror of the reference interfaces over the C-ABI (test/bench host).
+
+`OpfNlp` mirrors ipm::PatternNlp / NlpProblem (ipm/nlp.hpp:15-39,
+ipm/pattern_nlp.hpp:15-62): the same method names, the same argument meaning,
+and the same error behaviour (construction mistakes raise, evaluation
+failures return False and are described by `last_failure`).  `CondensedKkt`
+mirrors ipm::CondensedKkt (ipm/condensed.hpp:27-185) minus factorize/solve.
+
+Arrays may be numpy (host mode: GN_MEM_HOST) or CUDA torch tensors / raw
+device pointers (device mode).  Every call goes to the CUDA library; there is
+no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import abi
+from .abi import GN_IN_FULL, GN_MEM_DEVICE, GN_MEM_DEVICE_ASYNC, GN_MEM_HOST, GnError, GnSizes
+from .network import Network
+
+
+class GridError(RuntimeError):
+    """A construction/shape error (the reference throws gridnlp::Error)."""
+
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+def _check(rc: int, err: GnError | None = None, what: str = ""):
+    if rc != abi.GN_OK:
+        msg = err.message.decode() if err is not None else ""
+        raise GridError(rc, f"{what}: {msg} (code {rc})")
+
+
+def _f64(a):
+    """Pointer for a float64 numpy array, CUDA tensor, or int device address."""
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return C.cast(C.c_void_p(a), abi.f64p)
+    if hasattr(a, "data_ptr"):
+        return C.cast(C.c_void_p(a.data_ptr()), abi.f64p)
+    assert a.dtype == np.float64 and a.flags.c_contiguous
+    return a.ctypes.data_as(abi.f64p)
+
+
+def _i32(a):
+    if a is None:
+        return None
+    if isinstance(a, int):
+        return C.cast(C.c_void_p(a), abi.i32p)
+    if hasattr(a, "data_ptr"):
+        return C.cast(C.c_void_p(a.data_ptr()), abi.i32p)
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(abi.i32p)
+
+
+def load_profile(n_load: int, periods: int, resolution: float = 60.0, seed: int = 1,
+                 amplitude: float = 0.2, noise: float = 0.02) -> np.ndarray:
+    """generate_load_profile (network.hpp:104-140), T x n_load, bit-identical."""
+    out = np.empty(periods * max(n_load, 1), dtype=np.float64)
+    err = GnError()
+    _check(abi.lib().gn_load_profile(n_load, periods, resolution, seed, amplitude, noise,
+                                     _f64(out), C.byref(err)), err, "load profile")
+    return out[: periods * n_load].reshape(periods, n_load)
+
+
+class OpfNlp:
+    """Multi-period OPF on one B200 — the NlpProblem the reference's PatternNlp exposes."""
+
+    def __init__(self, net: Network, periods: int, scale: np.ndarray, device: int = 0):
+        self.lib = abi.lib()
+        self.net = net
+        self._cnet = net.to_c()
+        self._scale = np.ascontiguousarray(scale, dtype=np.float64).reshape(-1)
+        if self._scale.size != periods * net.n_load:
+            raise GridError(abi.GN_ERR_INVALID, "opf: load profile does not match network loads")
+        h = C.c_void_p()
+        err = GnError()
+        _check(self.lib.gn_ctx_create(C.byref(self._cnet), periods, _f64(self._scale), device,
+                                      C.byref(h), C.byref(err)), err, "gn_ctx_create")
+        self.h = h
+        self.device = device
+        self.last_failure = ""
+        self.last_error = (-1, -1)
+        self._sizes()
+
+    def _sizes(self):
+        s = GnSizes()
+        self.lib.gn_ctx_sizes(self.h, C.byref(s))
+        self.sizes = s
+        return s
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.gn_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- NlpProblem sizes / bounds / structure (nlp.hpp:19-30)
+    def n_vars(self) -> int:
+        return self.sizes.n_vars
+
+    def n_cons(self) -> int:
+        return self.sizes.n_cons
+
+    def bounds(self):
+        n, m = self.n_vars(), self.n_cons()
+        xl, xu, xs = (np.empty(n) for _ in range(3))
+        rl, ru = np.empty(m), np.empty(m)
+        _check(self.lib.gn_ctx_bounds(self.h, _f64(xl), _f64(xu), _f64(xs), _f64(rl), _f64(ru)))
+        return xl, xu, xs, rl, ru
+
+    def x_lower(self):
+        return self.bounds()[0]
+
+    def x_upper(self):
+        return self.bounds()[1]
+
+    def x_start(self):
+        return self.bounds()[2]
+
+    def row_lower(self):
+        return self.bounds()[3]
+
+    def row_upper(self):
+        return self.bounds()[4]
+
+    def jac_structure(self):
+        nj = self.sizes.jac_nnz
+        r, c = np.empty(nj, np.int32), np.empty(nj, np.int32)
+        _check(self.lib.gn_jac_structure(self.h, _i32(r), _i32(c), GN_MEM_HOST))
+        return r, c
+
+    def hess_structure(self):
+        nh = self.sizes.hess_nnz
+        r, c = np.empty(nh, np.int32), np.empty(nh, np.int32)
+        _check(self.lib.gn_hess_structure(self.h, _i32(r), _i32(c), GN_MEM_HOST))
+        return r, c
+
+    # ---- callbacks (nlp.hpp:32-38).  Host numpy in/out; returns bool.
+    def _record(self, rc: int, err: GnError) -> bool:
+        if rc == abi.GN_ERR_EVAL:
+            self.last_failure = err.message.decode()
+            self.last_error = (err.pattern, err.record)
+            return False
+        _check(rc, err, "evaluation")
+        return True
+
+    def eval_f(self, x: np.ndarray):
+        out = np.zeros(1)
+        err = GnError()
+        ok = self._record(self.lib.gn_eval_f(self.h, _f64(x), _f64(out), GN_MEM_HOST,
+                                             C.byref(err)), err)
+        return ok, float(out[0])
+
+    def _eval_vec(self, fn, x, size, *extra):
+        out = np.empty(size)
+        err = GnError()
+        ok = self._record(fn(self.h, _f64(x), *extra, _f64(out), GN_MEM_HOST, C.byref(err)), err)
+        return ok, out
+
+    def eval_grad(self, x):
+        return self._eval_vec(self.lib.gn_eval_grad, x, self.n_vars())
+
+    def eval_g(self, x):
+        return self._eval_vec(self.lib.gn_eval_g, x, self.n_cons())
+
+    def eval_jac(self, x):
+        return self._eval_vec(self.lib.gn_eval_jac, x, self.sizes.jac_nnz)
+
+    def eval_hess(self, x, row_weights, obj_weight: float):
+        out = np.empty(self.sizes.hess_nnz)
+        err = GnError()
+        ok = self._record(self.lib.gn_eval_hess(self.h, _f64(x), _f64(row_weights),
+                                                float(obj_weight), _f64(out), GN_MEM_HOST,
+                                                C.byref(err)), err)
+        return ok, out
+
+    # ---- device-resident variants (pointers to device memory)
+    def eval_device(self, which: str, x, out, w=None, ow: float = 1.0, sync: bool = True):
+        mem = GN_MEM_DEVICE if sync else GN_MEM_DEVICE_ASYNC
+        err = GnError()
+        L = self.lib
+        if which == "f":
+            rc = L.gn_eval_f(self.h, _f64(x), _f64(out), mem, C.byref(err))
+        elif which == "grad":
+            rc = L.gn_eval_grad(self.h, _f64(x), _f64(out), mem, C.byref(err))
+        elif which == "g":
+            rc = L.gn_eval_g(self.h, _f64(x), _f64(out), mem, C.byref(err))
+        elif which == "jac":
+            rc = L.gn_eval_jac(self.h, _f64(x), _f64(out), mem, C.byref(err))
+        elif which == "hess":
+            rc = L.gn_eval_hess(self.h, _f64(x), _f64(w), float(ow), _f64(out), mem,
+                                C.byref(err))
+        else:
+            raise ValueError(which)
+        return self._record(rc, err)
+
+    def status(self):
+        err = GnError()
+        return self._record(self.lib.gn_ctx_status(self.h, C.byref(err)), err)
+
+    def set_stream(self, stream_handle: int):
+        _check(self.lib.gn_ctx_set_stream(self.h, C.c_void_p(stream_handle)))
+
+    # ---- lifted problem (lifted.hpp:25-100)
+    def lift(self, relax: float):
+        err = GnError()
+        _check(self.lib.gn_lifted_create(self.h, relax, C.byref(err)), err, "gn_lifted_create")
+        self._sizes()
+        return self
+
+    def lifted_structure(self):
+        s = self.sizes
+        n, m = s.n_free, s.n_cons
+        nj, nh = s.jac_nnz_lifted, s.hess_nnz_lifted
+        f2f = np.empty(n, np.int32)
+        jr, jc, jp = (np.empty(nj, np.int32) for _ in range(3))
+        hr, hc, hp = (np.empty(nh, np.int32) for _ in range(3))
+        sl, su = np.empty(m), np.empty(m)
+        _check(self.lib.gn_lifted_structure(self.h, _i32(f2f), _i32(jr), _i32(jc), _i32(jp),
+                                            _i32(hr), _i32(hc), _i32(hp), _f64(sl), _f64(su),
+                                            GN_MEM_HOST))
+        return dict(free_to_full=f2f, jac_rows=jr, jac_cols=jc, jac_pick=jp, hess_rows=hr,
+                    hess_cols=hc, hess_pick=hp, s_lower=sl, s_upper=su)
+
+
+class CondensedKkt:
+    """ipm::CondensedKkt structure + set_jacobian + assemble on the device."""
+
+    def __init__(self, n=None, m=None, jac_rows=None, jac_cols=None, hess_rows=None,
+                 hess_cols=None, device: int = 0, nlp: OpfNlp | None = None):
+        self.lib = abi.lib()
+        h = C.c_void_p()
+        err = GnError()
+        if nlp is not None:
+            rc = self.lib.gn_kkt_create_lifted(nlp.h, C.byref(h), C.byref(err))
+            self._nlp = nlp
+        else:
+            jr = np.ascontiguousarray(jac_rows, np.int32)
+            jc = np.ascontiguousarray(jac_cols, np.int32)
+            hr = np.ascontiguousarray(hess_rows, np.int32)
+            hc = np.ascontiguousarray(hess_cols, np.int32)
+            rc = self.lib.gn_kkt_create(n, m, len(jr), _i32(jr), _i32(jc), len(hr), _i32(hr),
+                                        _i32(hc), device, C.byref(h), C.byref(err))
+        _check(rc, err, "gn_kkt_create")
+        self.h = h
+        d = (C.c_int64 * 7)()
+        self.lib.gn_kkt_dims(h, d)
+        self.dim, self.a_nnz, self.m_nnz, self.pair_count, self.jac_nnz, self.hess_nnz, \
+            self.n_rows = list(d)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.gn_kkt_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def structure(self):
+        rp = np.empty(self.n_rows + 1, np.int32)
+        ci = np.empty(self.a_nnz, np.int32)
+        cp = np.empty(self.dim + 1, np.int32)
+        ri = np.empty(self.m_nnz, np.int32)
+        _check(self.lib.gn_kkt_structure(self.h, _i32(rp), _i32(ci), _i32(cp), _i32(ri),
+                                         GN_MEM_HOST))
+        return rp, ci, cp, ri
+
+    def slots(self):
+        js = np.empty(self.jac_nnz, np.int32)
+        hs = np.empty(self.hess_nnz, np.int32)
+        ps = np.empty(self.pair_count, np.int32)
+        ds = np.empty(self.dim, np.int32)
+        _check(self.lib.gn_kkt_slots(self.h, _i32(js), _i32(hs), _i32(ps), _i32(ds),
+                                     GN_MEM_HOST))
+        return js, hs, ps, ds
+
+    def set_algorithm(self, algo: int):
+        _check(self.lib.gn_kkt_set_algorithm(self.h, algo))
+
+    def set_jacobian(self, jvals, mem: int = GN_MEM_HOST):
+        _check(self.lib.gn_kkt_set_jacobian(self.h, _f64(jvals), mem))
+
+    def assemble(self, hvals, sigma_x, sigma_s, delta_w: float, delta_c: float,
+                 mem: int = GN_MEM_HOST):
+        _check(self.lib.gn_kkt_assemble(self.h, _f64(hvals), _f64(sigma_x), _f64(sigma_s),
+                                        float(delta_w), float(delta_c), mem))
+
+    def values(self):
+        a = np.empty(self.a_nnz)
+        m = np.empty(self.m_nnz)
+        _check(self.lib.gn_kkt_values(self.h, _f64(a), _f64(m), GN_MEM_HOST))
+        return a, m
+
+    def values_device(self, a_out, m_out, sync: bool = True):
+        _check(self.lib.gn_kkt_values(self.h, _f64(a_out), _f64(m_out),
+                                      GN_MEM_DEVICE if sync else GN_MEM_DEVICE_ASYNC))
+
+
+def compress_to_csc(nrows, ncols, rows, cols):
+    rows = np.ascontiguousarray(rows, np.int32)
+    cols = np.ascontiguousarray(cols, np.int32)
+    nnz = len(rows)
+    cp = np.empty(ncols + 1, np.int32)
+    ri = np.empty(max(nnz, 1), np.int32)
+    sm = np.empty(max(nnz, 1), np.int32)
+    out = C.c_int32()
+    err = GnError()
+    _check(abi.lib().gn_compress_to_csc(nrows, ncols, nnz, _i32(rows), _i32(cols), _i32(cp),
+                                        _i32(ri), _i32(sm), C.byref(out), C.byref(err)), err,
+           "compress_to_csc")
+    return cp, ri[: out.value], sm[:nnz]
+
+
+__all__ = ["OpfNlp", "CondensedKkt", "GridError", "load_profile", "compress_to_csc",
+           "GN_MEM_HOST", "GN_MEM_DEVICE", "GN_MEM_DEVICE_ASYNC", "GN_IN_FULL"]
