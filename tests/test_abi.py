@@ -1,0 +1,76 @@
+"""CPU: the C-ABI library loads and exports every symbol include/*.h declares;
+host-only utilities (load profile, network conversion) match the reference."""
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from helpers import assert_bitexact, golden_eval, golden_meta, golden_network
+from oracle import bindings as B
+from paper_2405_14032_b200 import abi
+from paper_2405_14032_b200.network import CONFIG_SIZES, synthetic_case
+from paper_2405_14032_b200.opf import load_profile
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "gridnlp_b200.h"
+
+
+def declared():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(gn_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = abi.load()
+    names = declared()
+    assert len(names) >= 30
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(names) == set(abi.EXPORTED), set(names) ^ set(abi.EXPORTED)
+    assert lib.gn_abi_version() == 1
+
+
+def test_library_is_sm100a_cuda():
+    data = abi.LIB_PATH.read_bytes()
+    assert b"sm_100a" in data or b"compute_100a" in data
+
+
+def test_device_count_is_safe_without_gpu():
+    n = ctypes.c_int32(-1)
+    abi.lib().gn_device_count(ctypes.byref(n))
+    assert n.value >= 0
+
+
+@pytest.mark.parametrize("fx", list(golden_meta()["fixtures"]))
+def test_load_profile_bit_identical_to_reference(fx):
+    meta = golden_meta()["fixtures"][fx]
+    net = golden_network(meta["case"])
+    got = load_profile(net.n_load, meta["periods"], meta["resolution"], seed=1)
+    assert_bitexact(got, golden_eval(fx)["scale"], "scale")
+
+
+def test_load_profile_rejects_bad_arguments():
+    from paper_2405_14032_b200.opf import GridError
+    with pytest.raises(GridError):
+        load_profile(3, 0)
+    with pytest.raises(GridError):
+        load_profile(3, 2, amplitude=1.0)
+
+
+def test_synthetic_topology_properties():
+    raw = synthetic_case(200, 320, 40, 170, seed=3)
+    net = raw.network()
+    assert (net.n_bus, net.n_line, net.n_gen, net.n_load) == (200, 320, 40, 170)
+    assert np.all(net.line_from != net.line_to)
+    pairs = {(min(a, b), max(a, b)) for a, b in zip(net.line_from, net.line_to)}
+    assert len(pairs) == net.n_line  # no parallel lines by default
+    assert net.reference_bus == 0 and 0 in set(net.gen_bus.tolist())
+    assert np.all(np.isfinite(net.line_smax)) and np.all(np.abs(net.line_b) < 40)
+    assert set(CONFIG_SIZES) >= {"case1354pegase", "synthetic30k"}
+
+
+@pytest.mark.skipif(not B.ref_available(), reason="oracle/_ref not built here")
+def test_matpower_emission_parses_bit_identically():
+    raw = synthetic_case(60, 100, 15, 50, seed=9, parallel_lines=3, shared_gens=2)
+    assert raw.network().equal(B.ref_parse_matpower(raw.to_matpower()))

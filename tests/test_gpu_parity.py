@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference's golden
+fixtures and the bit-exact oracle.
+
+Bar (BASELINE.json north_star): structures and scatter maps bit-exact; values
+within 1e-12 relative with a 1e-14 absolute floor (helpers.REL/ABS); sums with
+no transcendental (balance rows, gradient, A, M given equal inputs) bit-exact.
+"""
+import numpy as np
+import pytest
+
+from helpers import (DELTAS, assert_bitexact, assert_close, golden_eval, golden_meta,
+                     golden_network, interior_point, row_weights, sigmas)
+from oracle import bindings as B
+from paper_2405_14032_b200.abi import GN_IN_FULL, GN_MEM_DEVICE
+from paper_2405_14032_b200.network import synthetic_case
+from paper_2405_14032_b200.opf import CondensedKkt, GridError, OpfNlp, compress_to_csc
+
+pytestmark = pytest.mark.gpu
+FIXTURES = list(golden_meta()["fixtures"])
+
+
+def _nlp(fx):
+    meta = golden_meta()["fixtures"][fx]
+    z = golden_eval(fx)
+    net = golden_network(meta["case"])
+    return OpfNlp(net, meta["periods"], z["scale"]), z, meta, net
+
+
+def _bal_rows(meta, net):
+    T = meta["periods"]
+    return np.arange(2 * net.n_bus * T)  # balance_p then balance_q blocks
+
+
+@pytest.mark.parametrize("fx", FIXTURES)
+def test_structure_and_bounds_bitexact(gpu, fx):
+    nlp, z, meta, _ = _nlp(fx)
+    s = nlp.sizes
+    assert [s.n_vars, s.n_cons, s.jac_nnz, s.hess_nnz, s.n_thermal, s.n_ramp_gens] == meta["sizes"]
+    for got, key in zip(nlp.bounds(), ("xl", "xu", "xs", "rl", "ru")):
+        assert_bitexact(got, z[key], key)
+    jr, jc = nlp.jac_structure()
+    hr, hc = nlp.hess_structure()
+    assert_bitexact(jr, z["jr"], "jac_rows")
+    assert_bitexact(jc, z["jc"], "jac_cols")
+    assert_bitexact(hr, z["hr"], "hess_rows")
+    assert_bitexact(hc, z["hc"], "hess_cols")
+
+
+@pytest.mark.parametrize("fx", FIXTURES)
+def test_callbacks_match_reference(gpu, fx):
+    nlp, z, meta, net = _nlp(fx)
+    x, w, ow = z["x"], z["w"], float(z["ow"])
+    ok, f = nlp.eval_f(x)
+    assert ok
+    assert_close([f], [float(z["f"])], what="f")
+    ok, grad = nlp.eval_grad(x)
+    assert ok
+    assert_bitexact(grad, z["grad"], "grad")  # c1 + (2 c2) pg, same rounding
+    ok, g = nlp.eval_g(x)
+    assert ok
+    assert_close(g, z["g"], what="g")
+    bal = _bal_rows(meta, net)
+    assert_bitexact(g[bal], z["g"][bal], "balance rows (canonical order)")
+    ok, jac = nlp.eval_jac(x)
+    assert ok
+    assert_close(jac, z["jac"], what="jac")
+    ok, hess = nlp.eval_hess(x, w, ow)
+    assert ok
+    assert_close(hess, z["hess"], what="hess")
+    # w == 0 (and -0.0) rows: every slot of those records is +0.0 (pattern_model.hpp:409-412)
+    assert np.all(hess[z["hess"] == 0.0] == 0.0)
+
+
+@pytest.mark.parametrize("fx", FIXTURES)
+def test_lifted_filter_bitexact(gpu, fx):
+    nlp, z, meta, net = _nlp(fx)
+    nlp.lift(1e-4)
+    s = nlp.sizes
+    assert [s.n_free, s.n_cons, s.jac_nnz_lifted, s.hess_nnz_lifted] == meta["lifted"]
+    L = nlp.lifted_structure()
+    for k in ("free_to_full", "jac_rows", "jac_cols", "hess_rows", "hess_cols", "s_lower",
+              "s_upper"):
+        assert_bitexact(L[k], z["l_" + k], k)
+    orc = B.OracleModel(net, meta["periods"], z["scale"])
+    lo = orc.lift(1e-4)
+    assert_bitexact(L["jac_pick"], lo["jac_pick"], "jac_pick")
+    assert_bitexact(L["hess_pick"], lo["hess_pick"], "hess_pick")
+
+
+@pytest.mark.parametrize("fx", FIXTURES)
+@pytest.mark.parametrize("mode", ["lifted-host", "full-host", "generic"])
+def test_kkt_structure_slots_and_values_bitexact(gpu, fx, mode):
+    nlp, z, meta, net = _nlp(fx)
+    nlp.lift(1e-4)
+    if mode == "generic":
+        K = CondensedKkt(meta["lifted"][0], meta["sizes"][1], z["l_jac_rows"], z["l_jac_cols"],
+                         z["l_hess_rows"], z["l_hess_cols"])
+    else:
+        K = CondensedKkt(nlp=nlp)
+    assert [K.dim, K.a_nnz, K.m_nnz] == meta["kkt"]
+    for got, key in zip(K.structure(), ("rowptr", "colidx", "colptr", "rowidx")):
+        assert_bitexact(got, z[key], key)
+    orc = B.OracleModel(net, meta["periods"], z["scale"])
+    orc.lift(1e-4)
+    OK = orc.kkt()
+    for got, ref, name in zip(K.slots(), OK.slots(), ("jac", "hess", "pair", "diag")):
+        assert_bitexact(got, ref, name + "_slots")
+    if mode == "full-host":
+        K.set_jacobian(z["jac"], mem=GN_IN_FULL)
+    else:
+        K.set_jacobian(z["jac_l"])
+    for i, (dw, dc) in enumerate(DELTAS):
+        if mode == "full-host":
+            K.assemble(z["hess"], z["sx"], z["ss"], dw, dc, mem=GN_IN_FULL)
+        else:
+            K.assemble(z["hess_l"], z["sx"], z["ss"], dw, dc)
+        a, m = K.values()
+        assert_bitexact(a, z["avals"], "A values")
+        assert_bitexact(m, z[f"mvals{i}"], f"M values delta#{i}")
+
+
+def test_device_resident_path_matches_host(gpu):
+    import torch
+    nlp, z, meta, net = _nlp("case118_T4")
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    dev = torch.device("cuda", 0)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)  # noqa: E731
+    x, w = t(z["x"]), t(z["w"])
+    s = nlp.sizes
+    f = torch.zeros(1, dtype=torch.float64, device=dev)
+    grad = torch.empty(s.n_vars, dtype=torch.float64, device=dev)
+    g = torch.empty(s.n_cons, dtype=torch.float64, device=dev)
+    J = torch.empty(s.jac_nnz, dtype=torch.float64, device=dev)
+    H = torch.empty(s.hess_nnz, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    assert nlp.eval_device("f", x, f)
+    assert nlp.eval_device("grad", x, grad)
+    assert nlp.eval_device("g", x, g)
+    assert nlp.eval_device("jac", x, J)
+    assert nlp.eval_device("hess", x, H, w=w, ow=float(z["ow"]))
+    for got, name in [(grad, "grad"), (g, "g"), (J, "jac"), (H, "hess")]:
+        ok, ref = getattr(nlp, "eval_" + name)(z["x"]) if name != "hess" else \
+            nlp.eval_hess(z["x"], z["w"], float(z["ow"]))
+        assert_bitexact(got.cpu().numpy(), ref, name)
+    sx, ss = t(z["sx"]), t(z["ss"])
+    K.set_jacobian(J, mem=GN_MEM_DEVICE | GN_IN_FULL)
+    K.assemble(H, sx, ss, 0.0, 0.0, mem=GN_MEM_DEVICE | GN_IN_FULL)
+    a, m = K.values()
+    assert_close(m, z["mvals0"], what="M from device-resident callbacks")
+
+
+def test_async_status_and_failure_report(gpu):
+    nlp, z, meta, net = _nlp("synth_T3")
+    orc = B.OracleModel(net, meta["periods"], z["scale"])
+    x = z["x"].copy()
+    n = meta["sizes"][0]
+    for idx in (n // 2, n - 3, 5):  # a flow, an angle, a generator
+        xb = x.copy()
+        xb[idx] = np.nan
+        for name, args in [("eval_f", (xb,)), ("eval_grad", (xb,)), ("eval_g", (xb,)),
+                           ("eval_jac", (xb,)), ("eval_hess", (xb, z["w"], 0.7))]:
+            okg, _ = getattr(nlp, name)(*args)
+            oko, _, fail = getattr(orc, name)(*args)
+            assert okg == oko, (name, idx)
+            if not okg:
+                assert nlp.last_error == fail, (name, idx, nlp.last_error, fail)
+    ok, _ = nlp.eval_g(x)
+    assert ok  # status cleared after a failure
+
+
+def test_self_loop_rejected(gpu):
+    raw = synthetic_case(10, 14, 3, 6, seed=1)
+    net = raw.network()
+    net.line_to[3] = net.line_from[3]
+    with pytest.raises(GridError) as e:
+        OpfNlp(net, 2, np.ones((2, net.n_load)))
+    assert e.value.code == 4
+
+
+def test_compress_to_csc_known_answer_gpu(gpu):
+    cp, ri, sm = compress_to_csc(3, 2, [0, 1, 0, 2], [0, 0, 0, 1])
+    assert cp.tolist() == [0, 2, 3] and ri.tolist() == [0, 1, 2] and sm.tolist() == [0, 1, 0, 2]
+    with pytest.raises(GridError):
+        compress_to_csc(2, 2, [0, 2], [0, 0])
+
+
+@pytest.mark.parametrize("size,T", [((300, 470, 60, 250), 24), ((1354, 1991, 260, 1137), 6)])
+def test_synthetic_vs_oracle(gpu, size, T):
+    raw = synthetic_case(*size, seed=17, parallel_lines=5, shared_gens=7)
+    net = raw.network()
+    from paper_2405_14032_b200.opf import load_profile
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale)
+    orc = B.OracleModel(net, T, scale)
+    assert [nlp.sizes.n_vars, nlp.sizes.n_cons, nlp.sizes.jac_nnz, nlp.sizes.hess_nnz] == \
+        orc.sizes[:4]
+    for a, b in zip((*nlp.jac_structure(), *nlp.hess_structure()), orc.structure()):
+        assert_bitexact(a, b)
+    xl, xu, xs, _, _ = orc.bounds()
+    x = interior_point(xl, xu, xs, 3)
+    w = row_weights(orc.sizes[1], 4, zero_every=13)
+    for name, args in [("eval_f", (x,)), ("eval_grad", (x,)), ("eval_g", (x,)),
+                       ("eval_jac", (x,)), ("eval_hess", (x, w, 1.0))]:
+        okg, got = getattr(nlp, name)(*args)
+        oko, ref, _ = getattr(orc, name)(*args)
+        assert okg and oko
+        assert_close(np.atleast_1d(got), np.atleast_1d(ref), what=name)
+    nlp.lift(1e-4)
+    lo = orc.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    OK = orc.kkt()
+    for a, b in zip(K.structure(), OK.structure()):
+        assert_bitexact(a, b)
+    _, jv, _ = orc.eval_jac(x)
+    _, hv, _ = orc.eval_hess(x, w, 1.0)
+    sx, ss = sigmas(len(lo["free_to_full"]), orc.sizes[1], 5)
+    K.set_jacobian(jv, mem=GN_IN_FULL)
+    OK.set_jacobian(jv[lo["jac_pick"]])
+    for dw, dc in DELTAS:
+        K.assemble(hv, sx, ss, dw, dc, mem=GN_IN_FULL)
+        OK.assemble(hv[lo["hess_pick"]], sx, ss, dw, dc)
+        for a, b in zip(K.values(), OK.values()):
+            assert_bitexact(a, b)
