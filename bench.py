@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""bench.py — callback + condensed-KKT-assembly throughput on B200.
+
+One *step* = one IPM iteration's hot-path unit of work over
+the whole (per-rank) horizon:
+    eval_f, eval_grad, eval_g, eval_jac, eval_hess(x, w = -y, 1)
+    + set_jacobian(J) + assemble(H, Sigma_x, Sigma_s, dw, dc)
+Workload at N=1: BASELINE.json configs[4], the synthetic 30k-bus network x 96
+periods (15.26M variables).  Under torchrun each rank owns 96 consecutive
+periods of a 96*N-period horizon (weak scaling; period sharding).
+
+`value` is nnz/s: (J + H + M nonzeros produced per step, summed over ranks)
+divided by the max-over-ranks device time per step.  `e2e` is the same metric
+through the public C-ABI with HOST buffers (every step copies its inputs H2D
+from pinned memory and its outputs D2H), i.e. the reference's std::span
+drop-in.  `--impl reference` times the reference's own CPU implementation
+(oracle/_ref) on the host cores instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+METRIC = "callback+KKT-assembly nnz/s (J+H+M per IPM iteration)"
+UNIT = "nnz/s"
+PERIODS_PER_RANK = 96
+CONFIG = "synthetic30k"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def inputs(nlp_bounds, m, n_free, seed_shift=0):
+    from helpers import interior_point, row_weights, sigmas
+    xl, xu, xs = nlp_bounds
+    x = interior_point(xl, xu, xs, 1234 + seed_shift)
+    w = row_weights(m, 7 + seed_shift)
+    sx, ss = sigmas(n_free, m, 11 + seed_shift)
+    return x, w, sx, ss
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [c.strip() for c in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def build_workload(rank: int, world: int, periods: int, config: str):
+    from paper_2405_14032_b200.network import config_case
+    from paper_2405_14032_b200.opf import load_profile
+    raw = config_case(config, seed=1)
+    net = raw.network()
+    scale = load_profile(net.n_load, periods * world, seed=1)
+    return raw, net, np.ascontiguousarray(scale[rank * periods:(rank + 1) * periods])
+
+
+def alg_bytes(s, kkt):
+    """SURVEY §8(d) B_alg per unit of work (index/scatter maps excluded)."""
+    n, m, J, H = s.n_vars, s.n_cons, s.jac_nnz, s.hess_nnz
+    Jl, Hl, nl, M = s.jac_nnz_lifted, s.hess_nnz_lifted, s.n_free, kkt.m_nnz
+    return 8 * (2 * n + 2 * m + 1 + J + H) + 8 * (Jl + Hl + nl + m + M)
+
+
+def stage_bytes(s, kkt, net, periods):
+    """Algorithmic bytes per call (contract inputs read once + outputs written once)."""
+    n, m, J, H = s.n_vars, s.n_cons, s.jac_nnz, s.hess_nnz
+    GT = net.n_gen * periods
+    return {
+        "f": 8 * (GT + 1),
+        "grad": 8 * (n + GT),
+        "g": 8 * (n + m),
+        "jac": 8 * (n + J),
+        "hess": 8 * (n + m + H),
+        "set_jacobian": 8 * (s.jac_nnz_lifted + kkt.a_nnz),
+        "assemble": 8 * (s.hess_nnz_lifted + kkt.a_nnz + s.n_free + m + kkt.m_nnz),
+    }
+
+
+def run_ours(args, rank, world, local_rank, dist):
+    import torch
+    from paper_2405_14032_b200 import abi
+    from paper_2405_14032_b200.abi import GN_IN_FULL, GN_MEM_DEVICE_ASYNC, GN_MEM_HOST
+    from paper_2405_14032_b200.opf import CondensedKkt, OpfNlp
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    raw, net, scale = build_workload(rank, world, args.periods, args.config)
+    t0 = time.time()
+    nlp = OpfNlp(net, args.periods, scale, device=local_rank)
+    stream = torch.cuda.Stream(device=dev)
+    nlp.set_stream(stream.cuda_stream)
+    nlp.lift(1e-4)
+    kkt = CondensedKkt(nlp=nlp)
+    setup_s = time.time() - t0
+    s = nlp.sizes
+    xl, xu, xs, _, _ = nlp.bounds()
+    x, w, sx, ss = inputs((xl, xu, xs), s.n_cons, s.n_free, seed_shift=rank)
+    del xl, xu, xs
+    f64 = dict(dtype=torch.float64, device=dev)
+    dx = torch.from_numpy(x).to(dev)
+    dwt = torch.from_numpy(w).to(dev)
+    dsx = torch.from_numpy(sx).to(dev)
+    dss = torch.from_numpy(ss).to(dev)
+    f = torch.zeros(1, **f64)
+    grad = torch.empty(s.n_vars, **f64)
+    g = torch.empty(s.n_cons, **f64)
+    J = torch.empty(s.jac_nnz, **f64)
+    H = torch.empty(s.hess_nnz, **f64)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > L2
+    torch.cuda.synchronize()
+    dw_reg, dc_reg = 1e-4, 1e-8 * 0.1 ** 0.25  # retry-variant regularization
+    A = GN_MEM_DEVICE_ASYNC
+    L = abi.lib()
+    stages = ["f", "grad", "g", "jac", "hess", "set_jacobian", "assemble"]
+
+    def step(ev=None):
+        def mark(i):
+            if ev is not None:
+                ev[i].record(stream)
+        mark(0)
+        nlp.eval_device("f", dx, f, sync=False)
+        mark(1)
+        nlp.eval_device("grad", dx, grad, sync=False)
+        mark(2)
+        nlp.eval_device("g", dx, g, sync=False)
+        mark(3)
+        nlp.eval_device("jac", dx, J, sync=False)
+        mark(4)
+        nlp.eval_device("hess", dx, H, w=dwt, ow=1.0, sync=False)
+        mark(5)
+        kkt.set_jacobian(J, mem=A | GN_IN_FULL)
+        mark(6)
+        kkt.assemble(H, dsx, dss, dw_reg, dc_reg, mem=A | GN_IN_FULL)
+        mark(7)
+
+    for _ in range(args.warmup):
+        step()
+    assert nlp.status(), f"evaluation failed during warm-up: {nlp.last_failure} {nlp.last_error}"
+    torch.cuda.synchronize()
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(8)] for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = Clocks(local_rank)
+    launches0 = L.gn_launch_count()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between timed steps, outside the step's events
+        step(events[k])
+    torch.cuda.synchronize()
+    launches = L.gn_launch_count() - launches0
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    assert nlp.status(), "evaluation failed in the timed region"
+    per_step = np.array([ev[0].elapsed_time(ev[7]) for ev in events])  # ms
+    per_stage = {st: float(np.mean([ev[i].elapsed_time(ev[i + 1]) for ev in events]))
+                 for i, st in enumerate(stages)}
+    ms = float(per_step.mean())
+    if dist:
+        import torch.distributed as tdist
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        ms = float(t.item())
+    nnz_step = s.jac_nnz + s.hess_nnz + kkt.m_nnz
+    value = nnz_step * world / (ms * 1e-3)
+
+    # roofline: dominant call (one kernel: the KKT assembly / else the largest stage)
+    peak, peak_kind = peaks()
+    sb = stage_bytes(s, kkt, net, args.periods)
+    dom = max(per_stage, key=per_stage.get)
+    achieved = sb[dom] / (per_stage[dom] * 1e-3) / 1e9
+    unit_bytes = alg_bytes(s, kkt)
+    unit_gbs = unit_bytes / (ms * 1e-3) / 1e9
+
+    # ---------------------------------------------------------- e2e (host API)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda k: torch.empty(k, dtype=torch.float64, pin_memory=True).numpy()  # noqa
+        hx, hw, hsx, hss = pin(s.n_vars), pin(s.n_cons), pin(s.n_free), pin(s.n_cons)
+        hx[:], hw[:], hsx[:], hss[:] = x, w, sx, ss
+        hf, hgrad, hg = pin(1), pin(s.n_vars), pin(s.n_cons)
+        hJ, hH = pin(s.jac_nnz), pin(s.hess_nnz)
+        hA, hM = pin(kkt.a_nnz), pin(kkt.m_nnz)
+
+        def e2e_step():
+            assert nlp.eval_f(hx, out=hf)[0]
+            assert nlp.eval_grad(hx, out=hgrad)[0]
+            assert nlp.eval_g(hx, out=hg)[0]
+            assert nlp.eval_jac(hx, out=hJ)[0]
+            assert nlp.eval_hess(hx, hw, 1.0, out=hH)[0]
+            kkt.set_jacobian(hJ, mem=GN_MEM_HOST | GN_IN_FULL)
+            kkt.assemble(hH, hsx, hss, dw_reg, dc_reg, mem=GN_MEM_HOST | GN_IN_FULL)
+            kkt.values(hA, hM)
+
+        e2e_step()
+        ksteps = max(1, min(args.steps, args.e2e_steps))
+        if dist:
+            dist.barrier()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(ksteps):
+            e2e_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = ev0.elapsed_time(ev1) / ksteps
+        if dist:
+            import torch.distributed as tdist
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = 8 * (5 * s.n_vars + s.n_cons + s.jac_nnz + s.hess_nnz + s.n_free + s.n_cons)
+        d2h = 8 * (1 + s.n_vars + s.n_cons + s.jac_nnz + s.hess_nnz + kkt.a_nnz + kkt.m_nnz)
+        e2e = {"value": nnz_step * world / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
+               "steps": ksteps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "path": "C-ABI GN_MEM_HOST calls (pinned host buffers), NlpProblem-style"}
+
+    # -------------------------------------------------------- CPU baseline
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference(raw, args, budget_s=args.cpu_budget)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} x {args.periods} periods per GPU "
+                               f"(BASELINE configs[4]; {s.n_vars} vars/GPU)",
+                   "network": {"buses": net.n_bus, "lines": net.n_line, "gens": net.n_gen,
+                               "loads": net.n_load},
+                   "periods_per_gpu": args.periods, "periods_total": args.periods * world,
+                   "parallelism": f"period-shard x{world}",
+                   "nnz_per_step_per_gpu": {"J": s.jac_nnz, "H": s.hess_nnz, "M": kkt.m_nnz},
+                   "l2": "256 MB buffer rewritten between timed steps (outside step events); "
+                         "per-step working set ~5.8 GB >> 126 MB L2",
+                   "delta_w": dw_reg, "delta_c": dc_reg},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "alg_bytes_per_launch": sb[dom], "traffic": None},
+        "unit_roofline": {"alg_bytes": unit_bytes, "achieved": unit_gbs, "peak": peak,
+                          "frac": unit_gbs / peak, "unit": "GB/s"},
+        "stages_ms": per_stage,
+        "setup_s": setup_s,
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    if args.traffic_json and Path(args.traffic_json).exists():
+        tr = json.loads(Path(args.traffic_json).read_text())
+        line["roofline"]["traffic"] = tr.get(dom)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------- reference CPU
+def cpu_reference(raw, args, budget_s=15.0, periods=None, steps=None, warmup=0):
+    """Time the reference's own CPU path (oracle/_ref) on a bounded sample of the
+    same workload: same network, `periods` periods (default 2), set_threads(nproc)."""
+    from oracle import bindings as B
+    from paper_2405_14032_b200.opf import load_profile
+    periods = periods or args.cpu_periods
+    kind = "reference" if B.ref_available() else "port"
+    nthreads = os.cpu_count() or 1
+    text = raw.to_matpower()
+    net = raw.network()
+    scale = load_profile(net.n_load, periods, seed=1)
+    if kind == "reference":
+        M = B.RefModel(text, periods, scale)
+        M.set_threads(nthreads)
+    else:
+        M = B.OracleModel(net, periods, scale)
+        nthreads = 1
+    xl, xu, xs, _, _ = M.bounds()
+    n, m, nj, nh = M.sizes[:4]
+    lift = M.lift(1e-4)
+    f2f = lift["free_to_full"]
+    x, w, sx, ss = inputs((xl, xu, xs), m, len(f2f))
+    xfree = np.ascontiguousarray(x[f2f])
+    if kind == "reference":
+        dims = M.kkt_create()
+        mnnz = dims[2]
+        jl = np.empty(M.lifted_sizes[2])
+        hl = np.empty(M.lifted_sizes[3])
+    else:
+        K = M.kkt()
+        mnnz = K.m_nnz
+    dw_reg, dc_reg = 1e-4, 1e-8 * 0.1 ** 0.25
+
+    def unit():
+        assert M.eval_f(x)[0]
+        assert M.eval_grad(x)[0]
+        assert M.eval_g(x)[0]
+        if kind == "reference":
+            # LiftedProblem::eval_jac/eval_hess = full callback + pick gather (lifted.hpp:249-264)
+            assert M.L.gnr_lifted_eval_jac(M.h, B._f(xfree), B._f(jl))
+            assert M.L.gnr_lifted_eval_hess(M.h, B._f(xfree), B._f(w), 1.0, B._f(hl))
+            M.kkt_set_jacobian(jl)
+            M.kkt_assemble(hl, sx, ss, dw_reg, dc_reg)
+        else:
+            _, jv, _ = M.eval_jac(x)
+            _, hv, _ = M.eval_hess(x, w, 1.0)
+            K.set_jacobian(jv[lift["jac_pick"]])
+            K.assemble(hv[lift["hess_pick"]], sx, ss, dw_reg, dc_reg)
+
+    for _ in range(warmup):
+        unit()
+    times = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        unit()
+        times.append(time.perf_counter() - t0)
+        if steps is not None and len(times) >= steps:
+            break
+        if steps is None and (time.perf_counter() - t_start > budget_s or len(times) >= 200):
+            break
+    t_unit = float(np.median(times))
+    nnz = nj + nh + mnnz
+    return {"value": nnz / t_unit, "unit": UNIT, "cores": nthreads, "kind": kind,
+            "ms_per_unit": t_unit * 1e3, "units_timed": len(times),
+            "sample": f"{args.config} network x {periods} periods (n={n}, J={nj}, H={nh}, "
+                      f"M={mnnz}); PatternModel::set_threads({nthreads}) callbacks + "
+                      f"LiftedProblem gathers + CondensedKkt set_jacobian/assemble "
+                      f"(single-threaded by design); median of {len(times)} units"}
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    raw, net, _ = build_workload(0, 1, args.periods, args.config)
+    cpu = cpu_reference(raw, args, periods=args.cpu_periods, steps=args.steps,
+                        warmup=args.warmup)
+    line = {
+        "metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["ms_per_unit"],
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{args.config} network x {args.cpu_periods} periods "
+                               "(bounded CPU sample of the 96-period workload)",
+                   "parallelism": "host threads"},
+        "cpu_baseline": cpu,
+        "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default=CONFIG)
+    ap.add_argument("--periods", type=int, default=PERIODS_PER_RANK)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-periods", type=int, default=2)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    try:
+        run_ours(args, rank, world, local_rank, dist)
+    finally:
+        if dist:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

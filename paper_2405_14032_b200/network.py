@@ -178,7 +178,7 @@ CONFIG_SIZES = {
 
 
 def synthetic_case(n_bus: int, n_line: int, n_gen: int, n_load: int, seed: int = 1,
-                   parallel_lines: int = 0, shared_gens: int = 0) -> RawCase:
+                   parallel_lines: int = 0, shared_gens: int = 0, max_span: int = 20) -> RawCase:
     """Ring + seeded chords (no self-loops), case118-fixture statistics.
 
     `parallel_lines` adds that many duplicate-terminal lines and `shared_gens`
@@ -192,12 +192,14 @@ def synthetic_case(n_bus: int, n_line: int, n_gen: int, n_load: int, seed: int =
     to = [(i + 1) % N for i in range(N)]
     seen = {(min(a, b), max(a, b)) for a, b in zip(fr, to)}
     need = n_line - N - parallel_lines
+    # chords span 2..max_span ring positions, like the fixture (case118 spans 2..20)
     while need > 0:
         a = rng.integers(0, N, size=2 * need + 16)
-        b = rng.integers(0, N, size=2 * need + 16)
-        for u, v in zip(a.tolist(), b.tolist()):
+        span = rng.integers(2, max_span + 1, size=a.size)
+        for u, sp in zip(a.tolist(), span.tolist()):
             if need == 0:
                 break
+            v = (u + sp) % N
             key = (min(u, v), max(u, v))
             if u == v or key in seen:
                 continue

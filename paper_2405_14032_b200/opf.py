@@ -155,30 +155,30 @@ class OpfNlp:
         _check(rc, err, "evaluation")
         return True
 
-    def eval_f(self, x: np.ndarray):
-        out = np.zeros(1)
+    def eval_f(self, x: np.ndarray, out=None):
+        out = np.zeros(1) if out is None else out
         err = GnError()
         ok = self._record(self.lib.gn_eval_f(self.h, _f64(x), _f64(out), GN_MEM_HOST,
                                              C.byref(err)), err)
         return ok, float(out[0])
 
-    def _eval_vec(self, fn, x, size, *extra):
-        out = np.empty(size)
+    def _eval_vec(self, fn, x, size, *extra, out=None):
+        out = np.empty(size) if out is None else out
         err = GnError()
         ok = self._record(fn(self.h, _f64(x), *extra, _f64(out), GN_MEM_HOST, C.byref(err)), err)
         return ok, out
 
-    def eval_grad(self, x):
-        return self._eval_vec(self.lib.gn_eval_grad, x, self.n_vars())
+    def eval_grad(self, x, out=None):
+        return self._eval_vec(self.lib.gn_eval_grad, x, self.n_vars(), out=out)
 
-    def eval_g(self, x):
-        return self._eval_vec(self.lib.gn_eval_g, x, self.n_cons())
+    def eval_g(self, x, out=None):
+        return self._eval_vec(self.lib.gn_eval_g, x, self.n_cons(), out=out)
 
-    def eval_jac(self, x):
-        return self._eval_vec(self.lib.gn_eval_jac, x, self.sizes.jac_nnz)
+    def eval_jac(self, x, out=None):
+        return self._eval_vec(self.lib.gn_eval_jac, x, self.sizes.jac_nnz, out=out)
 
-    def eval_hess(self, x, row_weights, obj_weight: float):
-        out = np.empty(self.sizes.hess_nnz)
+    def eval_hess(self, x, row_weights, obj_weight: float, out=None):
+        out = np.empty(self.sizes.hess_nnz) if out is None else out
         err = GnError()
         ok = self._record(self.lib.gn_eval_hess(self.h, _f64(x), _f64(row_weights),
                                                 float(obj_weight), _f64(out), GN_MEM_HOST,
@@ -299,9 +299,9 @@ class CondensedKkt:
         _check(self.lib.gn_kkt_assemble(self.h, _f64(hvals), _f64(sigma_x), _f64(sigma_s),
                                         float(delta_w), float(delta_c), mem))
 
-    def values(self):
-        a = np.empty(self.a_nnz)
-        m = np.empty(self.m_nnz)
+    def values(self, a=None, m=None):
+        a = np.empty(self.a_nnz) if a is None else a
+        m = np.empty(self.m_nnz) if m is None else m
         _check(self.lib.gn_kkt_values(self.h, _f64(a), _f64(m), GN_MEM_HOST))
         return a, m
 
