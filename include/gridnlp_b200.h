@@ -166,7 +166,9 @@ int gn_kkt_create(int32_t n, int32_t m, int64_t jac_nnz, const int32_t* jac_rows
 int gn_kkt_create_lifted(gn_ctx* ctx, gn_kkt** out, gn_error* err);
 int gn_kkt_destroy(gn_kkt* kkt);
 int gn_kkt_set_stream(gn_kkt* kkt, void* cuda_stream);
-/* dims = [dim, a_nnz, m_nnz, pair_count, jac_nnz, hess_nnz, n_rows] */
+/* dims = [dim, a_nnz, m_nnz, pair_count, jac_nnz, hess_nnz, n_rows, opf_ready]
+ * (opf_ready = 1 when the OPF-specialised kernels verified against the generic
+ * structure at creation and serve GN_IN_FULL inputs). */
 int gn_kkt_dims(gn_kkt* kkt, int64_t* dims);
 /* jacobian_csr() / pattern() (condensed.hpp:93-95). Any pointer may be NULL. */
 int gn_kkt_structure(gn_kkt* kkt, int32_t* rowptr, int32_t* colidx, int32_t* colptr,

@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <limits>
 #include <random>
 
@@ -527,6 +528,8 @@ int gn_kkt_create_lifted(gn_ctx* c, gn_kkt** out, gn_error* err) {
   K->own_stream = false;
   K->n = c->n_free; K->m = c->d.m; K->nj = c->nj_l; K->nh = c->nh_l;
   gnb::kkt_build(K, c->jr_l.p, c->jc_l.p, c->hr_l.p, c->hc_l.p);
+  const char* env = std::getenv("GRIDNLP_B200_GENERIC_KKT");
+  if (!(env && env[0] == '1')) gnb::opf_kkt_prepare(K);
   *out = K;
   return ok(err);
   }
@@ -546,6 +549,7 @@ int gn_kkt_destroy(gn_kkt* K) {
   if (K->stream) cudaStreamSynchronize(K->stream);
   cudaStream_t s = K->stream;
   const bool own = K->own_stream;
+  gnb::opf_kkt_free(K);
   delete K;
   if (own && s) cudaStreamDestroy(s);
   return GN_OK;
@@ -567,6 +571,7 @@ int gn_kkt_dims(gn_kkt* K, int64_t* dims) {
   if (!K || !dims) return GN_ERR_INVALID;
   dims[0] = K->n; dims[1] = K->annz; dims[2] = K->mnnz; dims[3] = K->npair;
   dims[4] = K->nj; dims[5] = K->nh; dims[6] = K->m;
+  dims[7] = gnb::opf_kkt_ready(K) ? 1 : 0;
   return GN_OK;
 }
 

@@ -267,6 +267,7 @@ void build_lifted(gn_ctx* c) {
   for (int32_t n = 0; n < d.N; ++n) fixed[e++] = c->bus_vmin[n] == c->bus_vmax[n];
   for (int32_t n = 0; n < d.N; ++n) fixed[e++] = (n == d.ref);  // th_ref box [0, 0]
   c->var_fixed.upload(fixed.data(), fixed.size(), s);
+  c->fixed_ent.assign(fixed.begin(), fixed.begin() + (fixed.size() - 1));
 
   DBuf<int32_t> flag, pos;
   flag.alloc(static_cast<size_t>(d.n) + 1);

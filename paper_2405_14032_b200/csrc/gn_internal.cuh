@@ -123,7 +123,8 @@ struct gn_ctx {
   // device tables
   gnb::DBuf<int32_t> lf, lt, l_therm, th_line, gbus, ramp_gen, bl_ptr, bl, bg_ptr, bg, bd_ptr, bd;
   gnb::DBuf<double> lg, lb, c2, c1, c0, pd, qd;
-  gnb::DBuf<uint8_t> var_fixed;  // [6 * max entity] flags, see DevNet
+  gnb::DBuf<uint8_t> var_fixed;  // per-entity fixed flags (block order), see DevNet
+  std::vector<uint8_t> fixed_ent;  // host copy
   gnb::DBuf<unsigned long long> status;
   gnb::DBuf<double> fpart;       // objective partial sums
   // host-mode staging

@@ -3,6 +3,8 @@
 
 namespace gnb {
 
+struct OpfKkt;
+
 // A compressed (CSC-ordered) pattern plus its scatter/gather maps.
 struct Csc {
   int32_t nnz = 0;
@@ -34,6 +36,7 @@ struct gn_kkt {
   gnb::DBuf<int32_t> arow;       // per CSR(A) entry: its row
   gnb::DBuf<double> avals, mvals;
   gnb::DBuf<double> sj, sh, ssx, sss;  // host-mode staging
+  gnb::OpfKkt* opf = nullptr;    // OPF-specialised tables (gn_kkt_create_lifted)
 };
 
 namespace gnb {
@@ -42,4 +45,10 @@ void kkt_build(gn_kkt* K, const int32_t* jr, const int32_t* jc, const int32_t* h
 void kkt_set_jacobian(gn_kkt* K, const double* J, bool full);
 void kkt_assemble(gn_kkt* K, const double* H, const double* sx, const double* ss, double dw,
                   double dc, bool full);
+bool opf_kkt_prepare(gn_kkt* K);
+void opf_kkt_free(gn_kkt* K);
+bool opf_kkt_ready(const gn_kkt* K);
+void opf_set_jacobian(gn_kkt* K, const double* Jfull);
+void opf_assemble(gn_kkt* K, const double* Hfull, const double* sx, const double* ss, double dw,
+                  double dc);
 }  // namespace gnb

@@ -1,0 +1,41 @@
+#pragma once
+#include "gn_kkt.cuh"
+
+namespace gnb {
+
+// Column / row blocks of the lifted OPF variables, in variable order.
+enum ColType { C_PG = 0, C_QG, C_P, C_Q, C_V, C_TH, C_TYPES };
+
+// Small per-entity tables (L2-resident) that let one thread enumerate an M
+// column's slots and each slot's contributors in the reference's summation
+// order without any per-contributor index map.
+struct OpfKktTab {
+  int32_t T, N, L, G;
+  int32_t bal_p0, bal_q0, flow_p0, flow_q0, therm0, ang0, ramp0;
+  int64_t ho[K_COUNT], jo[K_COUNT];
+  const int32_t* lent;                  // [2G+2L+2N] free-entity rank (lifted var = lent*T + t) or -1
+  const int32_t* cols;                  // free entities, grouped by type, in variable order
+  int32_t col_off[C_TYPES + 1];         // per type into cols
+  int32_t tile_off[C_TYPES + 1];        // CTA tiles per period, per type
+  const int32_t *lf, *lt, *l_therm;     // [L]
+  const int8_t* fpos;                   // [5L] flow-row positions of (p, v_f, v_t, th_f, th_t) or -1
+  const int8_t* apos;                   // [2L] angle-row positions of (th_f, th_t) or -1
+  const int32_t *lidx_to, *lidx_from;   // [L] rank of l among its bus's incident lines
+  const int32_t *gbus, *ppos, *qpos, *g_ramp;  // [G]
+  const int32_t *ngp, *ngq;             // [N] free pg / qg generators at the bus
+  const int32_t *bl_ptr, *bl;           // [N+1] incident lines sorted by l: l<<1 | is_from
+  const int32_t *bg_ptr, *bg;           // [N+1] generators at the bus, ascending
+  const int32_t *nb_ptr, *nb;           // [N+1] incident lines sorted by (other bus, l): l<<1|is_from
+  const int32_t *lnb_ptr, *lnb;         // [L+1] lines l' > l sharing a bus: (l' , shared-bus bits)
+  const int32_t *rowptr, *colptr;       // CSR(A) / CSC(M) from the generic build
+};
+
+struct OpfKkt {
+  bool ready = false;
+  OpfKktTab t{};
+  DBuf<int32_t> lent, cols, lf, lt, l_therm, lidx_to, lidx_from, gbus, ppos, qpos, g_ramp, ngp,
+      ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb;
+  DBuf<int8_t> fpos, apos;
+};
+
+}  // namespace gnb

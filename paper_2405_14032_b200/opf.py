@@ -254,10 +254,10 @@ class CondensedKkt:
                                         _i32(hc), device, C.byref(h), C.byref(err))
         _check(rc, err, "gn_kkt_create")
         self.h = h
-        d = (C.c_int64 * 7)()
+        d = (C.c_int64 * 8)()
         self.lib.gn_kkt_dims(h, d)
         self.dim, self.a_nnz, self.m_nnz, self.pair_count, self.jac_nnz, self.hess_nnz, \
-            self.n_rows = list(d)
+            self.n_rows, self.opf_ready = list(d)
 
     def close(self):
         if getattr(self, "h", None):

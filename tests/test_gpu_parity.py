@@ -222,3 +222,49 @@ def test_synthetic_vs_oracle(gpu, size, T):
         OK.assemble(hv[lo["hess_pick"]], sx, ss, dw, dc)
         for a, b in zip(K.values(), OK.values()):
             assert_bitexact(a, b)
+
+
+def _edge_network(seed=21):
+    """Parallel lines, several generators per bus, fixed generators (pmin == pmax,
+    qmin == qmax) and fixed voltages (vmin == vmax): every lifted-filter branch."""
+    raw = synthetic_case(400, 640, 90, 330, seed=seed, parallel_lines=9, shared_gens=12)
+    net = raw.network()
+    net.gen_pmin[3] = net.gen_pmax[3]
+    net.gen_qmin[7] = net.gen_qmax[7]
+    net.gen_pmin[11] = net.gen_pmax[11]
+    net.gen_qmin[11] = net.gen_qmax[11]
+    for b in (5, 17, 200):
+        net.bus_vmin[b] = net.bus_vmax[b]
+    net.gen_ramp[20] = np.inf  # a non-ramping generator
+    net.line_smax[[2, 50, 51]] = np.inf  # unrated lines
+    return net
+
+
+@pytest.mark.parametrize("T", [1, 2, 7])
+def test_specialised_kkt_equals_generic_and_oracle(gpu, T):
+    from paper_2405_14032_b200.opf import load_profile
+    net = _edge_network()
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale)
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    assert K.opf_ready == 1, "specialised enumeration did not verify"
+    orc = B.OracleModel(net, T, scale)
+    lo = orc.lift(1e-4)
+    assert nlp.sizes.n_free == len(lo["free_to_full"])
+    xl, xu, xs, _, _ = orc.bounds()
+    x = interior_point(xl, xu, xs, 9)
+    w = row_weights(orc.sizes[1], 10, zero_every=7)
+    _, jv, _ = orc.eval_jac(x)
+    _, hv, _ = orc.eval_hess(x, w, 1.0)
+    sx, ss = sigmas(len(lo["free_to_full"]), orc.sizes[1], 12)
+    OK = orc.kkt()
+    OK.set_jacobian(jv[lo["jac_pick"]])
+    for algo in (2, 1):  # specialised, then generic contributor lists
+        K.set_algorithm(algo)
+        K.set_jacobian(jv, mem=GN_IN_FULL)
+        for dw, dc in DELTAS:
+            K.assemble(hv, sx, ss, dw, dc, mem=GN_IN_FULL)
+            OK.assemble(hv[lo["hess_pick"]], sx, ss, dw, dc)
+            for a, b, nm in zip(K.values(), OK.values(), ("A", "M")):
+                assert_bitexact(a, b, f"{nm} algo={algo} dw={dw}")
