@@ -442,18 +442,23 @@ __device__ void col_gen(const OpfKktTab& t, const In& in, int32_t g, int32_t tt,
   }
 }
 
+// One warp per (entity, 32 consecutive periods): control flow and the per-entity
+// table reads are warp-uniform; sigma, rowptr and the M columns of the warp are
+// contiguous.  Work items are ordered by network locality (key bus) so that all
+// consumers of a line's H records / A rows run close together and hit in L2.
 template <bool STRUCT>
 __global__ void __launch_bounds__(kMB) k_opf_assemble(OpfKktTab t, In in, double* __restrict__ M,
                                                       int32_t* __restrict__ rows,
                                                       int32_t* __restrict__ bad) {
-  const int32_t tiles = t.tile_off[C_TYPES];
-  const int32_t tt = blockIdx.x / tiles;  // period-major CTA order
-  const int32_t tile = blockIdx.x - tt * tiles;
-  int type = 0;
-  while (type < C_TYPES - 1 && tile >= t.tile_off[type + 1]) ++type;
-  const int32_t idx = (tile - t.tile_off[type]) * kMB + threadIdx.x;
-  if (idx >= t.col_off[type + 1] - t.col_off[type]) return;
-  const int32_t e = __ldg(t.cols + t.col_off[type] + idx);
+  const int64_t w = ((int64_t)blockIdx.x * kMB + threadIdx.x) >> 5;
+  const int32_t lane = threadIdx.x & 31;
+  const int64_t item = w / t.tchunks;
+  if (item >= t.n_items) return;
+  const int32_t tt = (int32_t)(w - item * t.tchunks) * 32 + lane;
+  if (tt >= t.T) return;
+  const int32_t code = __ldg(t.items + item);
+  const int type = code >> 28;
+  const int32_t e = code & 0x0fffffff;
   const int32_t c = lv(t, type, e, tt);
   Out<STRUCT> o{M, rows, __ldg(t.colptr + c)};
   switch (type) {
@@ -465,6 +470,11 @@ __global__ void __launch_bounds__(kMB) k_opf_assemble(OpfKktTab t, In in, double
     default: col_th<STRUCT>(t, in, e, tt, o); break;
   }
   if (STRUCT && o.base + o.j != __ldg(t.colptr + c + 1)) atomicOr(bad, 1);
+}
+
+static int64_t assemble_blocks(const OpfKktTab& t) {
+  const int64_t warps = (int64_t)t.n_items * t.tchunks;
+  return (warps * 32 + kMB - 1) / kMB;
 }
 
 // ------------------------------------------------------------ set_jacobian
@@ -561,16 +571,25 @@ bool opf_kkt_prepare(gn_kkt* K) {
   for (size_t e = 0; e < fixed.size(); ++e) lent[e] = fixed[e] ? -1 : rank++;
   const int32_t offs[C_TYPES + 1] = {0, G, 2 * G, 2 * G + L, 2 * G + 2 * L, 2 * G + 2 * L + N,
                                      2 * G + 2 * L + 2 * N};
-  std::vector<int32_t> cols;
-  for (int ty = 0; ty < C_TYPES; ++ty) {
-    t.col_off[ty] = static_cast<int32_t>(cols.size());
-    for (int32_t e = 0; e < offs[ty + 1] - offs[ty]; ++e)
-      if (!fixed[offs[ty] + e]) cols.push_back(e);
-  }
-  t.col_off[C_TYPES] = static_cast<int32_t>(cols.size());
-  t.tile_off[0] = 0;
+  // work items in network-locality order: (key bus, type, entity)
+  std::vector<std::pair<int64_t, int32_t>> order;
+  int64_t nfree_ent = 0;
   for (int ty = 0; ty < C_TYPES; ++ty)
-    t.tile_off[ty + 1] = t.tile_off[ty] + (t.col_off[ty + 1] - t.col_off[ty] + kMB - 1) / kMB;
+    for (int32_t e = 0; e < offs[ty + 1] - offs[ty]; ++e) {
+      if (fixed[offs[ty] + e]) continue;
+      ++nfree_ent;
+      int32_t key;
+      if (ty == C_PG || ty == C_QG) key = c->gen_bus[e];
+      else if (ty == C_P || ty == C_Q) key = std::min(c->line_from[e], c->line_to[e]);
+      else key = e;
+      order.push_back({((int64_t)key * C_TYPES + ty) * (1ll << 31) + e, (ty << 28) | e});
+    }
+  std::sort(order.begin(), order.end());
+  std::vector<int32_t> items;
+  items.reserve(order.size());
+  for (auto& pr : order) items.push_back(pr.second);
+  t.n_items = static_cast<int32_t>(items.size());
+  t.tchunks = (d.T + 31) / 32;
   auto vfree = [&](int32_t n) { return !fixed[offs[C_V] + n]; };
   auto tfree = [&](int32_t n) { return !fixed[offs[C_TH] + n]; };
   // per-bus incidence (ascending l), generator ranks
@@ -652,14 +671,14 @@ bool opf_kkt_prepare(gn_kkt* K) {
     }
     lnb_ptr[l + 1] = static_cast<int32_t>(lnb.size());
   }
-  up(X->lent, lent, s); up(X->cols, cols, s);
+  up(X->lent, lent, s); up(X->items, items, s);
   up(X->lf, c->line_from, s); up(X->lt, c->line_to, s); up(X->l_therm, l_therm, s);
   up(X->fpos, fpos, s); up(X->apos, apos, s); up(X->lidx_to, lidx_to, s); up(X->lidx_from, lidx_from, s);
   up(X->gbus, c->gen_bus, s); up(X->ppos, ppos, s); up(X->qpos, qpos, s); up(X->g_ramp, g_ramp, s);
   up(X->ngp, ngp, s); up(X->ngq, ngq, s); up(X->bl_ptr, bl_ptr, s); up(X->bl, bl, s);
   up(X->bg_ptr, bg_ptr, s); up(X->bg, bg, s); up(X->nb_ptr, nb_ptr, s); up(X->nb, nb, s);
   up(X->lnb_ptr, lnb_ptr, s); up(X->lnb, lnb, s);
-  t.lent = X->lent.p; t.cols = X->cols.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
+  t.lent = X->lent.p; t.items = X->items.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
   t.fpos = X->fpos.p; t.apos = X->apos.p; t.lidx_to = X->lidx_to.p; t.lidx_from = X->lidx_from.p;
   t.gbus = X->gbus.p; t.ppos = X->ppos.p; t.qpos = X->qpos.p; t.g_ramp = X->g_ramp.p;
   t.ngp = X->ngp.p; t.ngq = X->ngq.p; t.bl_ptr = X->bl_ptr.p; t.bl = X->bl.p;
@@ -669,8 +688,8 @@ bool opf_kkt_prepare(gn_kkt* K) {
   GN_CK(cudaStreamSynchronize(s));
 
   // Verify the enumeration against the generic CSC (row index of every slot).
-  const int64_t blocks = (int64_t)t.tile_off[C_TYPES] * d.T;
-  bool ok = static_cast<int64_t>(cols.size()) * d.T == K->n;
+  const int64_t blocks = assemble_blocks(t);
+  bool ok = nfree_ent * d.T == K->n;
   if (ok && blocks > 0) {
     DBuf<int32_t> rows, bad;
     rows.alloc(static_cast<size_t>(K->mnnz) + 1);
@@ -716,7 +735,7 @@ void opf_set_jacobian(gn_kkt* K, const double* Jfull) {
 void opf_assemble(gn_kkt* K, const double* Hfull, const double* sx, const double* ss, double dw,
                   double dc) {
   const OpfKktTab& t = K->opf->t;
-  const int64_t blocks = (int64_t)t.tile_off[C_TYPES] * t.T;
+  const int64_t blocks = assemble_blocks(t);
   if (blocks <= 0) return;
   In in{Hfull, K->avals.p, sx, ss, dw, dc};
   k_opf_assemble<false><<<(unsigned)blocks, kMB, 0, K->stream>>>(t, in, K->mvals.p, nullptr, nullptr);

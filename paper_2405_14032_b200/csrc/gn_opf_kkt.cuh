@@ -14,9 +14,9 @@ struct OpfKktTab {
   int32_t bal_p0, bal_q0, flow_p0, flow_q0, therm0, ang0, ramp0;
   int64_t ho[K_COUNT], jo[K_COUNT];
   const int32_t* lent;                  // [2G+2L+2N] free-entity rank (lifted var = lent*T + t) or -1
-  const int32_t* cols;                  // free entities, grouped by type, in variable order
-  int32_t col_off[C_TYPES + 1];         // per type into cols
-  int32_t tile_off[C_TYPES + 1];        // CTA tiles per period, per type
+  const int32_t* items;                 // (type << 28 | entity) of every free entity, in
+                                        // network-locality order (key bus, type, entity)
+  int32_t n_items, tchunks;             // one warp per (item, 32-period chunk)
   const int32_t *lf, *lt, *l_therm;     // [L]
   const int8_t* fpos;                   // [5L] flow-row positions of (p, v_f, v_t, th_f, th_t) or -1
   const int8_t* apos;                   // [2L] angle-row positions of (th_f, th_t) or -1
@@ -33,7 +33,7 @@ struct OpfKktTab {
 struct OpfKkt {
   bool ready = false;
   OpfKktTab t{};
-  DBuf<int32_t> lent, cols, lf, lt, l_therm, lidx_to, lidx_from, gbus, ppos, qpos, g_ramp, ngp,
+  DBuf<int32_t> lent, items, lf, lt, l_therm, lidx_to, lidx_from, gbus, ppos, qpos, g_ramp, ngp,
       ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb;
   DBuf<int8_t> fpos, apos;
 };
