@@ -166,9 +166,9 @@ int gn_kkt_create(int32_t n, int32_t m, int64_t jac_nnz, const int32_t* jac_rows
 int gn_kkt_create_lifted(gn_ctx* ctx, gn_kkt** out, gn_error* err);
 int gn_kkt_destroy(gn_kkt* kkt);
 int gn_kkt_set_stream(gn_kkt* kkt, void* cuda_stream);
-/* dims = [dim, a_nnz, m_nnz, pair_count, jac_nnz, hess_nnz, n_rows, opf_ready]
- * (opf_ready = 1 when the OPF-specialised kernels verified against the generic
- * structure at creation and serve GN_IN_FULL inputs). */
+/* dims = [dim, a_nnz, m_nnz, pair_count, jac_nnz, hess_nnz, n_rows, opf_ready,
+ *         fused_ready] (opf_ready / fused_ready = 1 when the OPF-specialised /
+ * fused kernels verified against the generic structure at creation). */
 int gn_kkt_dims(gn_kkt* kkt, int64_t* dims);
 /* jacobian_csr() / pattern() (condensed.hpp:93-95). Any pointer may be NULL. */
 int gn_kkt_structure(gn_kkt* kkt, int32_t* rowptr, int32_t* colidx, int32_t* colptr,
@@ -182,6 +182,15 @@ int gn_kkt_set_jacobian(gn_kkt* kkt, const double* jac_vals, int mem);
  * summed per slot in the reference's order (bit-exact given equal inputs). */
 int gn_kkt_assemble(gn_kkt* kkt, const double* hess_vals, const double* sigma_x,
                     const double* sigma_s, double delta_w, double delta_c, int mem);
+/* Fused B200 path for lifted OPF KKTs (fused_ready): the same A and M as
+ *   set_jacobian(eval_jac(x))  and  assemble(eval_hess(x, w, ow), Sx, Ss, dw, dc)
+ * bit for bit, computed straight from x (and w, ow) without reading J or H.
+ * x is the FULL primal vector, row_weights/sigma_s have n_cons entries,
+ * sigma_x has n_free entries.  GN_ERR_UNSUPPORTED when the fused path is off. */
+int gn_kkt_set_jacobian_x(gn_kkt* kkt, const double* x, int mem);
+int gn_kkt_assemble_x(gn_kkt* kkt, const double* x, const double* row_weights,
+                      double obj_weight, const double* sigma_x, const double* sigma_s,
+                      double delta_w, double delta_c, int mem);
 /* jacobian_values() / values() (condensed.hpp:94-96). */
 int gn_kkt_values(gn_kkt* kkt, double* a_vals, double* m_vals, int mem);
 /* Selects the assembly algorithm: 0 = auto, 1 = generic contributor lists,

@@ -572,6 +572,7 @@ int gn_kkt_dims(gn_kkt* K, int64_t* dims) {
   dims[0] = K->n; dims[1] = K->annz; dims[2] = K->mnnz; dims[3] = K->npair;
   dims[4] = K->nj; dims[5] = K->nh; dims[6] = K->m;
   dims[7] = gnb::opf_kkt_ready(K) ? 1 : 0;
+  dims[8] = gnb::opf_fused_ready(K) ? 1 : 0;
   return GN_OK;
 }
 
@@ -634,6 +635,42 @@ int gn_kkt_assemble(gn_kkt* K, const double* hv, const double* sx, const double*
     dh = K->sh.p; dsx = K->ssx.p; dss = K->sss.p;
   }
   gnb::kkt_assemble(K, dh, dsx, dss, dw, dc, is_full(mem));
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_set_jacobian_x(gn_kkt* K, const double* x, int mem) {
+  if (!K || !x) return GN_ERR_INVALID;
+  if (!gnb::opf_fused_ready(K)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(K->device);
+  const double* dx = x;
+  if (!is_device(mem)) {
+    K->sj.upload(x, K->ctx->d.n, K->stream);
+    dx = K->sj.p;
+  }
+  gnb::opf_set_jacobian_fused(K, dx);
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_assemble_x(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
+                      const double* ss, double dw, double dc, int mem) {
+  if (!K || !x || !w || !sx || !ss) return GN_ERR_INVALID;
+  if (!gnb::opf_fused_ready(K)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(K->device);
+  const double *dx = x, *dwt = w, *dsx = sx, *dss = ss;
+  if (!is_device(mem)) {
+    K->sj.upload(x, K->ctx->d.n, K->stream);
+    K->sh.upload(w, K->m, K->stream);
+    K->ssx.upload(sx, K->n, K->stream);
+    K->sss.upload(ss, K->m, K->stream);
+    dx = K->sj.p; dwt = K->sh.p; dsx = K->ssx.p; dss = K->sss.p;
+  }
+  gnb::opf_assemble_fused(K, dx, dwt, ow, dsx, dss, dw, dc);
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
   return GN_OK;
   API_CATCH(nullptr)

@@ -13,6 +13,7 @@
 //   evaluate_jacobian    pattern_model.hpp:361-388
 //   evaluate_hessian     pattern_model.hpp:393-436 (w == 0 -> zeros, :409-412)
 #include "gn_eval.cuh"
+#include "gn_opf_math.cuh"
 
 namespace gnb {
 
@@ -46,10 +47,6 @@ __device__ __forceinline__ void const_out(double* __restrict__ out, int nb,
   for (int i = threadIdx.x; i < total; i += kBS) out[i] = c[i % K];
 }
 
-struct LineVals {
-  double vf, vt, Cs, Sn, vfvt, c, s;
-};
-
 // ---------------------------------------------------------------- lines
 // Patterns 1, 2 (balance-flow J/H), 7, 8 (flow definitions), 10 (angle).
 template <int MODE>
@@ -76,18 +73,12 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
     thf = x[d.th0 + (int64_t)f * d.T + t];
     tht = x[d.th0 + (int64_t)to * d.T + t];
   }
-  const double dth = thf - tht;
-  double sn, cs;
-  sincos(dth, &sn, &cs);
-  const double vfvt = vf * vt;
-  const double Cs = G * cs + B * sn;   // tape node 17 of flow_p
-  const double Sn = G * sn - B * cs;   // tape node 18 of flow_q
+  const LineState ls = line_state(G, B, vf, vt, thf, tht);
 
   if constexpr (MODE == EV_G) {
     if (valid) {
-      // opf.hpp:312-318 in tape order
-      const double gp = p - (G * (vf * vf) - vfvt * Cs);
-      const double gq = q - ((-B) * (vf * vf) - vfvt * Sn);
+      const double gp = g_flow_p(ls, G, p);
+      const double gq = g_flow_q(ls, B, q);
       const double ga = thf - tht;
       out[d.flow_p0 + r] = gp;
       out[d.flow_q0 + r] = gq;
@@ -102,12 +93,12 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
     const_out<2>(out + d.jac_off[K_BAL_P_FLOW] + 2 * r0, nb, pm);
     const_out<2>(out + d.jac_off[K_BAL_Q_FLOW] + 2 * r0, nb, pm);
     const_out<2>(out + d.jac_off[K_ANGLE] + 2 * r0, nb, pm);
-    // flow_p reverse sweep (tape order): xbar = [1, Cs*vt + (-2G)*vf, Cs*vf, a, -a]
-    const double a11 = (vfvt * B) * cs - (vfvt * G) * sn;
-    double jp[5] = {1.0, Cs * vt + ((-G) * 2.0) * vf, Cs * vf, a11, -a11};
-    // flow_q: xbar = [1, Sn*vt + (2B)*vf, Sn*vf, a, -a]
-    const double a12 = (vfvt * B) * sn + (vfvt * G) * cs;
-    double jq[5] = {1.0, Sn * vt + (B * 2.0) * vf, Sn * vf, a12, -a12};
+    double jp[5], jq[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+      jp[i] = j_flow_p(ls, G, B, i);
+      jq[i] = j_flow_q(ls, G, B, i);
+    }
     if (valid) {
       bool okp = true, okq = true;
 #pragma unroll
@@ -131,46 +122,11 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
       wp = w[d.flow_p0 + r];
       wq = w[d.flow_q0 + r];
     }
-    // Lower triangle, local order (0,0)(1,0)..(4,0)(1,1)..(4,1)(2,2)..(4,4);
-    // fields [flow, v_f, v_t, th_f, th_t].  Row/column 0 is identically 0.
     double hp[15], hq[15];
-    {
-      const double a = wp;
-      const double tS = vt * Sn, fS = vf * Sn, ffC = vfvt * Cs;
-      hp[0] = 0.0; hp[1] = 0.0; hp[2] = 0.0; hp[3] = 0.0; hp[4] = 0.0;
-      hp[5] = ((-2.0) * G) * a;   // (v_f, v_f)
-      hp[6] = Cs * a;             // (v_t, v_f)
-      hp[7] = -(tS * a);          // (th_f, v_f)
-      hp[8] = tS * a;             // (th_t, v_f)
-      hp[9] = 0.0;                // (v_t, v_t)
-      hp[10] = -(fS * a);         // (th_f, v_t)
-      hp[11] = fS * a;            // (th_t, v_t)
-      hp[12] = -(ffC * a);        // (th_f, th_f)
-      hp[13] = ffC * a;           // (th_t, th_f)
-      hp[14] = -(ffC * a);        // (th_t, th_t)
-      if (a == 0.0) {
 #pragma unroll
-        for (int i = 0; i < 15; ++i) hp[i] = 0.0;
-      }
-    }
-    {
-      const double a = wq;
-      const double tC = vt * Cs, fC = vf * Cs, ffS = vfvt * Sn;
-      hq[0] = 0.0; hq[1] = 0.0; hq[2] = 0.0; hq[3] = 0.0; hq[4] = 0.0;
-      hq[5] = (2.0 * B) * a;
-      hq[6] = Sn * a;
-      hq[7] = tC * a;
-      hq[8] = -(tC * a);
-      hq[9] = 0.0;
-      hq[10] = fC * a;
-      hq[11] = -(fC * a);
-      hq[12] = -(ffS * a);
-      hq[13] = ffS * a;
-      hq[14] = -(ffS * a);
-      if (a == 0.0) {
-#pragma unroll
-        for (int i = 0; i < 15; ++i) hq[i] = 0.0;
-      }
+    for (int i = 0; i < 15; ++i) {
+      hp[i] = h_flow_p(ls, G, wp, i);
+      hq[i] = h_flow_q(ls, B, wq, i);
     }
     if (valid) {
       bool okp = true, okq = true;
@@ -212,7 +168,7 @@ __global__ void __launch_bounds__(kBS) k_gen(OpfDims d, DevNet net, const double
     // ((c2*pg^2) + (c1*pg)) + c0, opf.hpp:245; partial sums in a fixed tree
     double v = 0.0;
     if (valid) {
-      v = (c2 * (pg * pg) + c1 * pg) + c0;
+      v = f_cost(c2, c1, c0, pg);
       if (!isfinite(v)) report(st, d.pid[K_COST], r);
     }
     red[threadIdx.x] = v;
@@ -224,7 +180,7 @@ __global__ void __launch_bounds__(kBS) k_gen(OpfDims d, DevNet net, const double
     if (threadIdx.x == 0) fpart[blockIdx.x] = red[0];
   } else if constexpr (MODE == EV_GRAD) {
     if (valid) {
-      const double gr = c1 + (c2 * 2.0) * pg;  // reverse sweep order
+      const double gr = grad_cost(c2, c1, pg);  // reverse sweep order
       out[d.pg0 + r] = gr;
       if (!isfinite(gr)) report(st, d.pid[K_COST], r);
     }
@@ -237,7 +193,7 @@ __global__ void __launch_bounds__(kBS) k_gen(OpfDims d, DevNet net, const double
     if (valid) {
       double h = 0.0;
       if (ow != 0.0) {
-        h = (ow * c2) * 2.0;
+        h = h_cost(ow, c2);
         if (!isfinite(h) || !isfinite(pg)) report(st, d.pid[K_COST], r);
       }
       out[d.hess_off[K_COST] + r] = h;
@@ -288,20 +244,20 @@ __global__ void __launch_bounds__(kBS) k_thermal(OpfDims d, DevNet net,
   }
   if constexpr (MODE == EV_G) {
     if (valid) {
-      const double v = p * p + q * q;
+      const double v = g_thermal(p, q);
       out[d.therm0 + r] = v;
       if (!isfinite(v)) report(st, d.pid[K_THERMAL], r);
     }
   } else if constexpr (MODE == EV_J) {
-    double j[2] = {2.0 * p, 2.0 * q};
+    double j[2] = {j_thermal(p), j_thermal(q)};
     if (valid && !(isfinite(j[0]) && isfinite(j[1]))) report(st, d.pid[K_THERMAL], r);
     stage_out<2>(sm, j, valid, out + d.jac_off[K_THERMAL] + 2 * r0, nb);
   } else {
     const double a = valid ? w[d.therm0 + r] : 0.0;
     double h[3] = {0.0, 0.0, 0.0};
     if (a != 0.0) {
-      h[0] = (a * 2.0);
-      h[2] = (a * 2.0);
+      h[0] = h_thermal_diag(a);
+      h[2] = h_thermal_diag(a);
       if (valid && !(isfinite(h[0]) && isfinite(p) && isfinite(q)))
         report(st, d.pid[K_THERMAL], r);
     }

@@ -32,59 +32,31 @@ struct In {
   double dw, dc;
 };
 
-// CSR row (rbase + rel) of an entity whose rows for consecutive periods are
-// consecutive and equally long: rowptr[rbase] is warp-uniform, the rest is arithmetic.
-// Returns (d_r * A[ka]) * A[kb] with d_r = sd / (1 + dc sd), sd = sigma_s + dw
-// (condensed.hpp:112-116, 126-129).
-__device__ __forceinline__ double pair_u(const OpfKktTab& t, const In& in, int32_t rbase,
-                                         int32_t rel, int ia, int ib) {
-  const int32_t rp0 = __ldg(t.rowptr + rbase);
-  const int32_t len = __ldg(t.rowptr + rbase + 1) - rp0;
-  const int32_t rp = rp0 + rel * len;
-  const double sd = in.ss[rbase + rel] + in.dw;
+__device__ __forceinline__ double pairval(const OpfKktTab& t, const In& in, int32_t r, int ia,
+                                          int ib) {
+  const int32_t rp = __ldg(t.rowptr + r);
+  const double sd = in.ss[r] + in.dw;  // condensed.hpp:112-116
   const double c = 1.0 / (1.0 + in.dc * sd);
   const double d = sd * c;
   const double va = d * in.A[rp + ia];
   return va * in.A[rp + ib];
 }
 
-// acc (+) f(i) for i = i0 .. i1-1 in that order; the terms of a batch of 8 are
-// loaded independently (memory-level parallelism), then added in order.
-template <class F>
-__device__ __forceinline__ double osum(double acc, int32_t i0, int32_t i1, F&& f) {
-  for (int32_t b = i0; b < i1; b += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = (b + u < i1) ? f(b + u) : 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (b + u < i1) acc += v[u];
-  }
-  return acc;
-}
-
 __device__ __forceinline__ int32_t lidx(const OpfKktTab& t, int32_t l, int32_t b) {
   return b == __ldg(t.lt + l) ? __ldg(t.lidx_to + l) : __ldg(t.lidx_from + l);
 }
 
-__device__ __forceinline__ int32_t type_off(const OpfKktTab& t, int type) {
-  switch (type) {
-    case C_PG: return 0;
-    case C_QG: return t.G;
-    case C_P: return 2 * t.G;
-    case C_Q: return 2 * t.G + t.L;
-    case C_V: return 2 * t.G + 2 * t.L;
-    default: return 2 * t.G + 2 * t.L + t.N;
-  }
-}
-
 __device__ __forceinline__ bool freev(const OpfKktTab& t, int type, int32_t e) {
-  return __ldg(t.lent + type_off(t, type) + e) >= 0;
-}
-
-__device__ __forceinline__ int32_t lv(const OpfKktTab& t, int type, int32_t e, int32_t tt) {
-  const int32_t k = __ldg(t.lent + type_off(t, type) + e);
-  return k < 0 ? -1 : k * t.T + tt;
+  int32_t off;
+  switch (type) {
+    case C_PG: off = 0; break;
+    case C_QG: off = t.G; break;
+    case C_P: off = 2 * t.G; break;
+    case C_Q: off = 2 * t.G + t.L; break;
+    case C_V: off = 2 * t.G + 2 * t.L; break;
+    default: off = 2 * t.G + 2 * t.L + t.N; break;
+  }
+  return __ldg(t.lent + off + e) >= 0;
 }
 
 // Writes (value or row index) of one slot.
@@ -100,14 +72,19 @@ struct Out {
   }
 };
 
-// other end of the incidence entry e (l << 1 | n-is-from)
-__device__ __forceinline__ int32_t other(const OpfKktTab& t, int32_t e) {
-  const int32_t l = e >> 1;
-  return (e & 1) ? __ldg(t.lt + l) : __ldg(t.lf + l);
+__device__ __forceinline__ int32_t lv(const OpfKktTab& t, int type, int32_t e, int32_t tt) {
+  int32_t off;
+  switch (type) {
+    case C_PG: off = 0; break;
+    case C_QG: off = t.G; break;
+    case C_P: off = 2 * t.G; break;
+    case C_Q: off = 2 * t.G + t.L; break;
+    case C_V: off = 2 * t.G + 2 * t.L; break;
+    default: off = 2 * t.G + 2 * t.L + t.N; break;
+  }
+  const int32_t k = __ldg(t.lent + off + e);
+  return k < 0 ? -1 : k * t.T + tt;
 }
-
-// H slot of a line record (pattern base ho, record stride k) at period tt
-#define HREC(ho, stride, l, slot) in.H[(ho) + (stride) * ((int64_t)(l) * T + tt) + (slot)]
 
 // ------------------------------------------------------------- M columns
 template <bool STRUCT>
@@ -115,61 +92,83 @@ __device__ void col_th(const OpfKktTab& t, const In& in, int32_t n, int32_t tt, 
   const int32_t T = t.T;
   const int32_t b0 = __ldg(t.bl_ptr + n), b1 = __ldg(t.bl_ptr + n + 1);
   const int32_t me = lv(t, C_TH, n, tt);
-  const int64_t h7 = t.ho[K_FLOW_P], h8 = t.ho[K_FLOW_Q], h10 = t.ho[K_ANGLE];
-  {  // diagonal: H flow_p, flow_q, angle; pairs flow_p, flow_q, angle rows; dw + sx
+  {  // diagonal
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      auto inc = [&](int32_t i) { return __ldg(t.bl + i); };
-      acc = osum(acc, b0, b1, [&](int32_t i) { const int32_t e = inc(i); return HREC(h7, 15, e >> 1, (e & 1) ? 12 : 14); });
-      acc = osum(acc, b0, b1, [&](int32_t i) { const int32_t e = inc(i); return HREC(h8, 15, e >> 1, (e & 1) ? 12 : 14); });
-      acc = osum(acc, b0, b1, [&](int32_t i) { const int32_t e = inc(i); return HREC(h10, 3, e >> 1, (e & 1) ? 0 : 2); });
-      acc = osum(acc, b0, b1, [&](int32_t i) {
-        const int32_t e = inc(i), l = e >> 1;
-        const int p = __ldg(t.fpos + 5 * l + ((e & 1) ? 3 : 4));
-        return pair_u(t, in, t.flow_p0 + l * T, tt, p, p);
-      });
-      acc = osum(acc, b0, b1, [&](int32_t i) {
-        const int32_t e = inc(i), l = e >> 1;
-        const int p = __ldg(t.fpos + 5 * l + ((e & 1) ? 3 : 4));
-        return pair_u(t, in, t.flow_q0 + l * T, tt, p, p);
-      });
-      acc = osum(acc, b0, b1, [&](int32_t i) {
-        const int32_t e = inc(i), l = e >> 1;
-        const int p = __ldg(t.apos + 2 * l + ((e & 1) ? 0 : 1));
-        return pair_u(t, in, t.ang0 + l * T, tt, p, p);
-      });
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        acc += in.H[t.ho[K_FLOW_P] + 15 * ((int64_t)l * T + tt) + (fr ? 12 : 14)];
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        acc += in.H[t.ho[K_FLOW_Q] + 15 * ((int64_t)l * T + tt) + (fr ? 12 : 14)];
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        acc += in.H[t.ho[K_ANGLE] + 3 * ((int64_t)l * T + tt) + (fr ? 0 : 2)];
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        const int p = __ldg(t.fpos + 5 * l + (fr ? 3 : 4));
+        acc += pairval(t, in, t.flow_p0 + l * T + tt, p, p);
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        const int p = __ldg(t.fpos + 5 * l + (fr ? 3 : 4));
+        acc += pairval(t, in, t.flow_q0 + l * T + tt, p, p);
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        const int p = __ldg(t.apos + 2 * l + (fr ? 0 : 1));
+        acc += pairval(t, in, t.ang0 + l * T + tt, p, p);
+      }
       acc += in.dw + in.sx[me];
     }
     o.put(acc, me);
   }
-  // th(n') for neighbours n' > n; each group = the lines between n and n' (ascending l)
+  // th(n') for neighbours n' > n, lines grouped by neighbour (ascending l)
   const int32_t q0 = __ldg(t.nb_ptr + n), q1 = __ldg(t.nb_ptr + n + 1);
-  for (int32_t i = q0; i < q1;) {
-    const int32_t nb = other(t, __ldg(t.nb + i));
+  int32_t i = q0;
+  while (i < q1) {
+    const int32_t e0 = __ldg(t.nb + i), l0 = e0 >> 1;
+    const int32_t nb = (e0 & 1) ? __ldg(t.lt + l0) : __ldg(t.lf + l0);
     int32_t k = i + 1;
-    while (k < q1 && other(t, __ldg(t.nb + k)) == nb) ++k;
+    while (k < q1) {
+      const int32_t ek = __ldg(t.nb + k), lk = ek >> 1;
+      const int32_t bk = (ek & 1) ? __ldg(t.lt + lk) : __ldg(t.lf + lk);
+      if (bk != nb) break;
+      ++k;
+    }
     if (nb > n && freev(t, C_TH, nb)) {
       double acc = 0.0;
       if constexpr (!STRUCT) {
-        auto ln = [&](int32_t u) { return __ldg(t.nb + u); };
-        acc = osum(acc, i, k, [&](int32_t u) { return HREC(h7, 15, ln(u) >> 1, 13); });
-        acc = osum(acc, i, k, [&](int32_t u) { return HREC(h8, 15, ln(u) >> 1, 13); });
-        acc = osum(acc, i, k, [&](int32_t u) { return HREC(h10, 3, ln(u) >> 1, 1); });
-        acc = osum(acc, i, k, [&](int32_t u) {
-          const int32_t e = ln(u), l = e >> 1, fr = e & 1;
-          return pair_u(t, in, t.flow_p0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 4 : 3)),
-                        __ldg(t.fpos + 5 * l + (fr ? 3 : 4)));
-        });
-        acc = osum(acc, i, k, [&](int32_t u) {
-          const int32_t e = ln(u), l = e >> 1, fr = e & 1;
-          return pair_u(t, in, t.flow_q0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 4 : 3)),
-                        __ldg(t.fpos + 5 * l + (fr ? 3 : 4)));
-        });
-        acc = osum(acc, i, k, [&](int32_t u) {
-          const int32_t e = ln(u), l = e >> 1, fr = e & 1;
-          return pair_u(t, in, t.ang0 + l * T, tt, __ldg(t.apos + 2 * l + (fr ? 1 : 0)),
-                        __ldg(t.apos + 2 * l + (fr ? 0 : 1)));
-        });
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t l = __ldg(t.nb + u) >> 1;
+          acc += in.H[t.ho[K_FLOW_P] + 15 * ((int64_t)l * T + tt) + 13];
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t l = __ldg(t.nb + u) >> 1;
+          acc += in.H[t.ho[K_FLOW_Q] + 15 * ((int64_t)l * T + tt) + 13];
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t l = __ldg(t.nb + u) >> 1;
+          acc += in.H[t.ho[K_ANGLE] + 3 * ((int64_t)l * T + tt) + 1];
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          const int pa = __ldg(t.fpos + 5 * l + (fr ? 4 : 3)), pb = __ldg(t.fpos + 5 * l + (fr ? 3 : 4));
+          acc += pairval(t, in, t.flow_p0 + l * T + tt, pa, pb);
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          const int pa = __ldg(t.fpos + 5 * l + (fr ? 4 : 3)), pb = __ldg(t.fpos + 5 * l + (fr ? 3 : 4));
+          acc += pairval(t, in, t.flow_q0 + l * T + tt, pa, pb);
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          const int pa = __ldg(t.apos + 2 * l + (fr ? 1 : 0)), pb = __ldg(t.apos + 2 * l + (fr ? 0 : 1));
+          acc += pairval(t, in, t.ang0 + l * T + tt, pa, pb);
+        }
       }
       o.put(acc, lv(t, C_TH, nb, tt));
     }
@@ -182,49 +181,63 @@ __device__ void col_v(const OpfKktTab& t, const In& in, int32_t n, int32_t tt, O
   const int32_t T = t.T;
   const int32_t b0 = __ldg(t.bl_ptr + n), b1 = __ldg(t.bl_ptr + n + 1);
   const int32_t me = lv(t, C_V, n, tt);
-  const int64_t h7 = t.ho[K_FLOW_P], h8 = t.ho[K_FLOW_Q];
-  auto inc = [&](int32_t i) { return __ldg(t.bl + i); };
-  {  // diagonal: slot (1,1) if n is from, (2,2) if n is to
+  {  // diagonal (v, v): flow_p slot (1,1) or (2,2), flow_q likewise, pairs, diag
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      acc = osum(acc, b0, b1, [&](int32_t i) { const int32_t e = inc(i); return HREC(h7, 15, e >> 1, (e & 1) ? 5 : 9); });
-      acc = osum(acc, b0, b1, [&](int32_t i) { const int32_t e = inc(i); return HREC(h8, 15, e >> 1, (e & 1) ? 5 : 9); });
-      acc = osum(acc, b0, b1, [&](int32_t i) {
-        const int32_t e = inc(i), l = e >> 1;
-        const int p = __ldg(t.fpos + 5 * l + ((e & 1) ? 1 : 2));
-        return pair_u(t, in, t.flow_p0 + l * T, tt, p, p);
-      });
-      acc = osum(acc, b0, b1, [&](int32_t i) {
-        const int32_t e = inc(i), l = e >> 1;
-        const int p = __ldg(t.fpos + 5 * l + ((e & 1) ? 1 : 2));
-        return pair_u(t, in, t.flow_q0 + l * T, tt, p, p);
-      });
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        acc += in.H[t.ho[K_FLOW_P] + 15 * ((int64_t)l * T + tt) + (fr ? 5 : 9)];
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        acc += in.H[t.ho[K_FLOW_Q] + 15 * ((int64_t)l * T + tt) + (fr ? 5 : 9)];
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        const int p = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+        acc += pairval(t, in, t.flow_p0 + l * T + tt, p, p);
+      }
+      for (int32_t i = b0; i < b1; ++i) {
+        const int32_t e = __ldg(t.bl + i), l = e >> 1, fr = e & 1;
+        const int p = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+        acc += pairval(t, in, t.flow_q0 + l * T + tt, p, p);
+      }
       acc += in.dw + in.sx[me];
     }
     o.put(acc, me);
   }
   const int32_t q0 = __ldg(t.nb_ptr + n), q1 = __ldg(t.nb_ptr + n + 1);
-  auto ln = [&](int32_t u) { return __ldg(t.nb + u); };
-  // v(n') for neighbours n' > n: slot (2,1)
+  // v(n') for neighbours n' > n
   for (int32_t i = q0; i < q1;) {
-    const int32_t nb = other(t, ln(i));
+    const int32_t e0 = __ldg(t.nb + i), l0 = e0 >> 1;
+    const int32_t nb = (e0 & 1) ? __ldg(t.lt + l0) : __ldg(t.lf + l0);
     int32_t k = i + 1;
-    while (k < q1 && other(t, ln(k)) == nb) ++k;
+    while (k < q1) {
+      const int32_t ek = __ldg(t.nb + k), lk = ek >> 1;
+      if (((ek & 1) ? __ldg(t.lt + lk) : __ldg(t.lf + lk)) != nb) break;
+      ++k;
+    }
     if (nb > n && freev(t, C_V, nb)) {
       double acc = 0.0;
       if constexpr (!STRUCT) {
-        acc = osum(acc, i, k, [&](int32_t u) { return HREC(h7, 15, ln(u) >> 1, 6); });
-        acc = osum(acc, i, k, [&](int32_t u) { return HREC(h8, 15, ln(u) >> 1, 6); });
-        acc = osum(acc, i, k, [&](int32_t u) {
-          const int32_t e = ln(u), l = e >> 1, fr = e & 1;
-          return pair_u(t, in, t.flow_p0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 2 : 1)),
-                        __ldg(t.fpos + 5 * l + (fr ? 1 : 2)));
-        });
-        acc = osum(acc, i, k, [&](int32_t u) {
-          const int32_t e = ln(u), l = e >> 1, fr = e & 1;
-          return pair_u(t, in, t.flow_q0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 2 : 1)),
-                        __ldg(t.fpos + 5 * l + (fr ? 1 : 2)));
-        });
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t l = __ldg(t.nb + u) >> 1;
+          acc += in.H[t.ho[K_FLOW_P] + 15 * ((int64_t)l * T + tt) + 6];
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t l = __ldg(t.nb + u) >> 1;
+          acc += in.H[t.ho[K_FLOW_Q] + 15 * ((int64_t)l * T + tt) + 6];
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          const int pa = __ldg(t.fpos + 5 * l + (fr ? 2 : 1)), pb = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+          acc += pairval(t, in, t.flow_p0 + l * T + tt, pa, pb);
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          const int pa = __ldg(t.fpos + 5 * l + (fr ? 2 : 1)), pb = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+          acc += pairval(t, in, t.flow_q0 + l * T + tt, pa, pb);
+        }
       }
       o.put(acc, lv(t, C_V, nb, tt));
     }
@@ -235,26 +248,37 @@ __device__ void col_v(const OpfKktTab& t, const In& in, int32_t n, int32_t tt, O
   for (int32_t i = q0; i <= q1;) {
     int32_t nb = 0x7fffffff, k = i + 1;
     if (i < q1) {
-      nb = other(t, ln(i));
-      while (k < q1 && other(t, ln(k)) == nb) ++k;
+      const int32_t e0 = __ldg(t.nb + i), l0 = e0 >> 1;
+      nb = (e0 & 1) ? __ldg(t.lt + l0) : __ldg(t.lf + l0);
+      while (k < q1) {
+        const int32_t ek = __ldg(t.nb + k), lk = ek >> 1;
+        if (((ek & 1) ? __ldg(t.lt + lk) : __ldg(t.lf + lk)) != nb) break;
+        ++k;
+      }
     }
-    if (!self_done && n < nb) {  // (th(n), v(n)): slot (3,1) if n is from, (4,2) if n is to
+    if (!self_done && n < nb) {  // the (th(n), v(n)) slot: every incident line
       self_done = true;
       if (freev(t, C_TH, n)) {
         double acc = 0.0;
         if constexpr (!STRUCT) {
-          acc = osum(acc, b0, b1, [&](int32_t u) { const int32_t e = inc(u); return HREC(h7, 15, e >> 1, (e & 1) ? 7 : 11); });
-          acc = osum(acc, b0, b1, [&](int32_t u) { const int32_t e = inc(u); return HREC(h8, 15, e >> 1, (e & 1) ? 7 : 11); });
-          acc = osum(acc, b0, b1, [&](int32_t u) {
-            const int32_t e = inc(u), l = e >> 1, fr = e & 1;
-            return pair_u(t, in, t.flow_p0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 3 : 4)),
-                          __ldg(t.fpos + 5 * l + (fr ? 1 : 2)));
-          });
-          acc = osum(acc, b0, b1, [&](int32_t u) {
-            const int32_t e = inc(u), l = e >> 1, fr = e & 1;
-            return pair_u(t, in, t.flow_q0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 3 : 4)),
-                          __ldg(t.fpos + 5 * l + (fr ? 1 : 2)));
-          });
+          for (int32_t u = b0; u < b1; ++u) {
+            const int32_t e = __ldg(t.bl + u), l = e >> 1, fr = e & 1;
+            acc += in.H[t.ho[K_FLOW_P] + 15 * ((int64_t)l * T + tt) + (fr ? 7 : 11)];
+          }
+          for (int32_t u = b0; u < b1; ++u) {
+            const int32_t e = __ldg(t.bl + u), l = e >> 1, fr = e & 1;
+            acc += in.H[t.ho[K_FLOW_Q] + 15 * ((int64_t)l * T + tt) + (fr ? 7 : 11)];
+          }
+          for (int32_t u = b0; u < b1; ++u) {
+            const int32_t e = __ldg(t.bl + u), l = e >> 1, fr = e & 1;
+            const int pa = __ldg(t.fpos + 5 * l + (fr ? 3 : 4)), pb = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+            acc += pairval(t, in, t.flow_p0 + l * T + tt, pa, pb);
+          }
+          for (int32_t u = b0; u < b1; ++u) {
+            const int32_t e = __ldg(t.bl + u), l = e >> 1, fr = e & 1;
+            const int pa = __ldg(t.fpos + 5 * l + (fr ? 3 : 4)), pb = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+            acc += pairval(t, in, t.flow_q0 + l * T + tt, pa, pb);
+          }
         }
         o.put(acc, lv(t, C_TH, n, tt));
       }
@@ -264,18 +288,24 @@ __device__ void col_v(const OpfKktTab& t, const In& in, int32_t n, int32_t tt, O
     if (freev(t, C_TH, nb)) {  // (th(n'), v(n)): slot (4,1) if n is from, (3,2) if n is to
       double acc = 0.0;
       if constexpr (!STRUCT) {
-        acc = osum(acc, i, k, [&](int32_t u) { const int32_t e = ln(u); return HREC(h7, 15, e >> 1, (e & 1) ? 8 : 10); });
-        acc = osum(acc, i, k, [&](int32_t u) { const int32_t e = ln(u); return HREC(h8, 15, e >> 1, (e & 1) ? 8 : 10); });
-        acc = osum(acc, i, k, [&](int32_t u) {
-          const int32_t e = ln(u), l = e >> 1, fr = e & 1;
-          return pair_u(t, in, t.flow_p0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 4 : 3)),
-                        __ldg(t.fpos + 5 * l + (fr ? 1 : 2)));
-        });
-        acc = osum(acc, i, k, [&](int32_t u) {
-          const int32_t e = ln(u), l = e >> 1, fr = e & 1;
-          return pair_u(t, in, t.flow_q0 + l * T, tt, __ldg(t.fpos + 5 * l + (fr ? 4 : 3)),
-                        __ldg(t.fpos + 5 * l + (fr ? 1 : 2)));
-        });
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          acc += in.H[t.ho[K_FLOW_P] + 15 * ((int64_t)l * T + tt) + (fr ? 8 : 10)];
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          acc += in.H[t.ho[K_FLOW_Q] + 15 * ((int64_t)l * T + tt) + (fr ? 8 : 10)];
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          const int pa = __ldg(t.fpos + 5 * l + (fr ? 4 : 3)), pb = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+          acc += pairval(t, in, t.flow_p0 + l * T + tt, pa, pb);
+        }
+        for (int32_t u = i; u < k; ++u) {
+          const int32_t e = __ldg(t.nb + u), l = e >> 1, fr = e & 1;
+          const int pa = __ldg(t.fpos + 5 * l + (fr ? 4 : 3)), pb = __ldg(t.fpos + 5 * l + (fr ? 1 : 2));
+          acc += pairval(t, in, t.flow_q0 + l * T + tt, pa, pb);
+        }
       }
       o.put(acc, lv(t, C_TH, nb, tt));
     }
@@ -295,29 +325,20 @@ __device__ void col_flow(const OpfKktTab& t, const In& in, int32_t l, int32_t tt
   const int32_t bal0 = Q ? t.bal_q0 : t.bal_p0, flow0 = Q ? t.flow_q0 : t.flow_p0;
   const int32_t* ng = Q ? t.ngq : t.ngp;
   const int32_t me = lv(t, Q ? C_Q : C_P, l, tt);
-  const int pl = __ldg(ng + blo) + lidx(t, l, blo), ph = __ldg(ng + bhi) + lidx(t, l, bhi);
   {
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      // independent terms first, then the ordered sum
-      const double h0 = in.H[t.ho[kb] + 2 * r];      // to-record (p,p)
-      const double h1 = in.H[t.ho[kb] + 2 * r + 1];  // from-record
-      const double h2 = in.H[t.ho[kf] + 15 * r];     // flow definition (0,0)
-      const double h3 = k >= 0 ? in.H[t.ho[K_THERMAL] + 3 * ((int64_t)k * T + tt) + (Q ? 2 : 0)] : 0.0;
-      const double p0 = pair_u(t, in, bal0 + blo * T, tt, pl, pl);
-      const double p1 = pair_u(t, in, bal0 + bhi * T, tt, ph, ph);
-      const double p2 = pair_u(t, in, flow0 + l * T, tt, 0, 0);
-      const double p3 = k >= 0 ? pair_u(t, in, t.therm0 + k * T, tt, Q ? 1 : 0, Q ? 1 : 0) : 0.0;
-      const double dg = in.dw + in.sx[me];
-      acc += h0;
-      acc += h1;
-      acc += h2;
-      if (k >= 0) acc += h3;
-      acc += p0;
-      acc += p1;
-      acc += p2;
-      if (k >= 0) acc += p3;
-      acc += dg;
+      acc += in.H[t.ho[kb] + 2 * r];      // to-record (p,p)
+      acc += in.H[t.ho[kb] + 2 * r + 1];  // from-record
+      acc += in.H[t.ho[kf] + 15 * r];     // flow definition (0,0)
+      if (k >= 0) acc += in.H[t.ho[K_THERMAL] + 3 * ((int64_t)k * T + tt) + (Q ? 2 : 0)];
+      const int pl = __ldg(ng + blo) + lidx(t, l, blo);
+      acc += pairval(t, in, bal0 + blo * T + tt, pl, pl);
+      const int ph = __ldg(ng + bhi) + lidx(t, l, bhi);
+      acc += pairval(t, in, bal0 + bhi * T + tt, ph, ph);
+      acc += pairval(t, in, flow0 + (int32_t)r, 0, 0);
+      if (k >= 0) acc += pairval(t, in, t.therm0 + k * T + tt, Q ? 1 : 0, Q ? 1 : 0);
+      acc += in.dw + in.sx[me];
     }
     o.put(acc, me);
   }
@@ -327,40 +348,39 @@ __device__ void col_flow(const OpfKktTab& t, const In& in, int32_t l, int32_t tt
     const int32_t e = __ldg(t.lnb + i), l2 = e >> 2, bits = e & 3;
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      double x0 = 0.0, x1 = 0.0;
-      if (bits & 1) x0 = pair_u(t, in, bal0 + blo * T, tt, __ldg(ng + blo) + lidx(t, l2, blo), pl);
-      if (bits & 2) x1 = pair_u(t, in, bal0 + bhi * T, tt, __ldg(ng + bhi) + lidx(t, l2, bhi), ph);
-      if (bits & 1) acc += x0;
-      if (bits & 2) acc += x1;
+      if (bits & 1) {
+        const int pa = __ldg(ng + blo) + lidx(t, l2, blo), pb = __ldg(ng + blo) + lidx(t, l, blo);
+        acc += pairval(t, in, bal0 + blo * T + tt, pa, pb);
+      }
+      if (bits & 2) {
+        const int pa = __ldg(ng + bhi) + lidx(t, l2, bhi), pb = __ldg(ng + bhi) + lidx(t, l, bhi);
+        acc += pairval(t, in, bal0 + bhi * T + tt, pa, pb);
+      }
     }
     o.put(acc, lv(t, Q ? C_Q : C_P, l2, tt));
   }
   if (!Q && k >= 0) {  // (q(l), p(l)) from the thermal row
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      const double h = in.H[t.ho[K_THERMAL] + 3 * ((int64_t)k * T + tt) + 1];
-      const double p = pair_u(t, in, t.therm0 + k * T, tt, 1, 0);
-      acc += h;
-      acc += p;
+      acc += in.H[t.ho[K_THERMAL] + 3 * ((int64_t)k * T + tt) + 1];
+      acc += pairval(t, in, t.therm0 + k * T + tt, 1, 0);
     }
     o.put(acc, lv(t, C_Q, l, tt));
   }
-  // v(b), then th(b), b ascending in {f, to}: H slot (field, 0) + flow-row pair
+  // v(b), then th(b), b ascending in {f, to}
 #pragma unroll
   for (int blk = 0; blk < 2; ++blk) {
 #pragma unroll
-    for (int sdx = 0; sdx < 2; ++sdx) {
-      const int32_t b = sdx == 0 ? blo : bhi;
+    for (int s = 0; s < 2; ++s) {
+      const int32_t b = s == 0 ? blo : bhi;
       const bool isf = (b == f);
       const int field = blk == 0 ? (isf ? 1 : 2) : (isf ? 3 : 4);
       const int pa = __ldg(t.fpos + 5 * l + field);
       if (pa < 0) continue;
       double acc = 0.0;
       if constexpr (!STRUCT) {
-        const double h = in.H[t.ho[kf] + 15 * r + field];
-        const double p = pair_u(t, in, flow0 + l * T, tt, pa, 0);
-        acc += h;
-        acc += p;
+        acc += in.H[t.ho[kf] + 15 * r + field];  // local slot (field, 0)
+        acc += pairval(t, in, flow0 + (int32_t)r, pa, 0);
       }
       o.put(acc, lv(t, blk == 0 ? C_V : C_TH, b, tt));
     }
@@ -375,42 +395,30 @@ __device__ void col_gen(const OpfKktTab& t, const In& in, int32_t g, int32_t tt,
   const int32_t* pos = Q ? t.qpos : t.ppos;
   const int32_t* ng = Q ? t.ngq : t.ngp;
   const int32_t bal0 = Q ? t.bal_q0 : t.bal_p0;
-  const int32_t rbb = bal0 + b * T;  // balance row of the bus at t = 0
+  const int32_t rb = bal0 + b * T + tt;
   const int my = __ldg(pos + g);
   const int32_t kr = Q ? -1 : __ldg(t.g_ramp + g);
-  const int32_t rr0 = t.ramp0 + (kr >= 0 ? kr : 0) * (T - 1);  // ramp row of step t = 1
   const int32_t me = lv(t, Q ? C_QG : C_PG, g, tt);
   const int64_t r = (int64_t)g * T + tt;
-  const bool lo_ok = kr >= 0 && tt >= 1, hi_ok = kr >= 0 && tt + 1 < T;
   {
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      const double h0 = Q ? 0.0 : in.H[t.ho[K_COST] + r];
-      const double h1 = in.H[t.ho[Q ? K_BAL_Q_INJ : K_BAL_P_INJ] + r];
-      const double h2 = lo_ok ? in.H[t.ho[K_RAMP] + 3 * ((int64_t)kr * (T - 1) + tt - 1)] : 0.0;
-      const double h3 = hi_ok ? in.H[t.ho[K_RAMP] + 3 * ((int64_t)kr * (T - 1) + tt) + 2] : 0.0;
-      const double p0 = pair_u(t, in, rbb, tt, my, my);
-      const double p1 = lo_ok ? pair_u(t, in, rr0, tt - 1, 1, 1) : 0.0;
-      const double p2 = hi_ok ? pair_u(t, in, rr0, tt, 0, 0) : 0.0;
-      const double dg = in.dw + in.sx[me];
-      if (!Q) acc += h0;
-      acc += h1;
-      if (lo_ok) acc += h2;
-      if (hi_ok) acc += h3;
-      acc += p0;
-      if (lo_ok) acc += p1;
-      if (hi_ok) acc += p2;
-      acc += dg;
+      if (!Q) acc += in.H[t.ho[K_COST] + r];
+      acc += in.H[t.ho[Q ? K_BAL_Q_INJ : K_BAL_P_INJ] + r];
+      if (kr >= 0 && tt >= 1) acc += in.H[t.ho[K_RAMP] + 3 * ((int64_t)kr * (T - 1) + tt - 1)];
+      if (kr >= 0 && tt + 1 < T) acc += in.H[t.ho[K_RAMP] + 3 * ((int64_t)kr * (T - 1) + tt) + 2];
+      acc += pairval(t, in, rb, my, my);
+      if (kr >= 0 && tt >= 1) acc += pairval(t, in, t.ramp0 + kr * (T - 1) + tt - 1, 1, 1);
+      if (kr >= 0 && tt + 1 < T) acc += pairval(t, in, t.ramp0 + kr * (T - 1) + tt, 0, 0);
+      acc += in.dw + in.sx[me];
     }
     o.put(acc, me);
   }
-  if (hi_ok) {  // (pg(g,t+1), pg(g,t))
+  if (kr >= 0 && tt + 1 < T) {  // (pg(g,t+1), pg(g,t))
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      const double h = in.H[t.ho[K_RAMP] + 3 * ((int64_t)kr * (T - 1) + tt) + 1];
-      const double p = pair_u(t, in, rr0, tt, 1, 0);
-      acc += h;
-      acc += p;
+      acc += in.H[t.ho[K_RAMP] + 3 * ((int64_t)kr * (T - 1) + tt) + 1];
+      acc += pairval(t, in, t.ramp0 + kr * (T - 1) + tt, 1, 0);
     }
     o.put(acc, me + 1);
   }
@@ -420,24 +428,17 @@ __device__ void col_gen(const OpfKktTab& t, const In& in, int32_t g, int32_t tt,
     const int32_t g2 = __ldg(t.bg + i);
     if (g2 <= g || !freev(t, Q ? C_QG : C_PG, g2)) continue;
     double acc = 0.0;
-    if constexpr (!STRUCT) acc += pair_u(t, in, rbb, tt, __ldg(pos + g2), my);
+    if constexpr (!STRUCT) acc += pairval(t, in, rb, __ldg(pos + g2), my);
     o.put(acc, lv(t, Q ? C_QG : C_PG, g2, tt));
   }
-  // incident flows (balance-row pairs), ascending l
+  // incident flows
   const int32_t b0 = __ldg(t.bl_ptr + b), b1 = __ldg(t.bl_ptr + b + 1);
   const int nfree = __ldg(ng + b);
-  for (int32_t i0 = b0; i0 < b1; i0 += 8) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if constexpr (!STRUCT) v[u] = (i0 + u < b1) ? pair_u(t, in, rbb, tt, nfree + (i0 + u - b0), my) : 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (i0 + u < b1) {
-        double acc = 0.0;
-        if constexpr (!STRUCT) acc += v[u];
-        o.put(acc, lv(t, Q ? C_Q : C_P, __ldg(t.bl + i0 + u) >> 1, tt));
-      }
+  for (int32_t i = b0; i < b1; ++i) {
+    const int32_t l = __ldg(t.bl + i) >> 1;
+    double acc = 0.0;
+    if constexpr (!STRUCT) acc += pairval(t, in, rb, nfree + (i - b0), my);
+    o.put(acc, lv(t, Q ? C_Q : C_P, l, tt));
   }
 }
 
@@ -446,7 +447,7 @@ __device__ void col_gen(const OpfKktTab& t, const In& in, int32_t g, int32_t tt,
 // contiguous.  Work items are ordered by network locality (key bus) so that all
 // consumers of a line's H records / A rows run close together and hit in L2.
 template <bool STRUCT>
-__global__ void __launch_bounds__(kMB, 8) k_opf_assemble(OpfKktTab t, In in, double* __restrict__ M,
+__global__ void __launch_bounds__(kMB) k_opf_assemble(OpfKktTab t, In in, double* __restrict__ M,
                                                       int32_t* __restrict__ rows,
                                                       int32_t* __restrict__ bad) {
   const int64_t w = ((int64_t)blockIdx.x * kMB + threadIdx.x) >> 5;
@@ -619,17 +620,25 @@ bool opf_kkt_prepare(gn_kkt* K) {
   std::vector<int32_t> l_therm(L, -1);
   for (int32_t k = 0; k < d.LT; ++k) l_therm[c->thermal_lines[k]] = k;
   // neighbour-grouped incidence (other bus, l)
-  std::vector<int32_t> nb_ptr(N + 1, 0), nb;
+  std::vector<int32_t> nb_ptr(N + 1, 0), nb, nb_inc;
+  int32_t maxdeg = 0;
   for (int32_t n = 0; n < N; ++n) {
-    std::vector<std::pair<int32_t, int32_t>> v;
-    for (int32_t e : inc[n]) {
-      const int32_t l = e >> 1;
-      v.push_back({(e & 1) ? c->line_to[l] : c->line_from[l], e});
+    std::vector<std::pair<std::pair<int32_t, int32_t>, int32_t>> v;
+    for (size_t i = 0; i < inc[n].size(); ++i) {
+      const int32_t e = inc[n][i], l = e >> 1;
+      v.push_back({{(e & 1) ? c->line_to[l] : c->line_from[l], e}, static_cast<int32_t>(i)});
     }
     std::sort(v.begin(), v.end());
-    for (auto& pr : v) nb.push_back(pr.second);
+    for (auto& pr : v) {
+      nb.push_back(pr.first.second);
+      nb_inc.push_back(pr.second);
+    }
     nb_ptr[n + 1] = static_cast<int32_t>(nb.size());
+    maxdeg = std::max(maxdeg, static_cast<int32_t>(inc[n].size()));
   }
+  t.maxdeg = maxdeg;
+  t.pg0 = d.pg0; t.qg0 = d.qg0; t.p0 = d.p0; t.q0 = d.q0; t.v0 = d.v0; t.th0 = d.th0;
+  t.lg = c->lg.p; t.lb = c->lb.p; t.c2 = c->c2.p;
   // flow-row / angle-row positions
   std::vector<int8_t> fpos(5 * static_cast<size_t>(L)), apos(2 * static_cast<size_t>(L));
   for (int32_t l = 0; l < L; ++l) {
@@ -675,13 +684,13 @@ bool opf_kkt_prepare(gn_kkt* K) {
   up(X->fpos, fpos, s); up(X->apos, apos, s); up(X->lidx_to, lidx_to, s); up(X->lidx_from, lidx_from, s);
   up(X->gbus, c->gen_bus, s); up(X->ppos, ppos, s); up(X->qpos, qpos, s); up(X->g_ramp, g_ramp, s);
   up(X->ngp, ngp, s); up(X->ngq, ngq, s); up(X->bl_ptr, bl_ptr, s); up(X->bl, bl, s);
-  up(X->bg_ptr, bg_ptr, s); up(X->bg, bg, s); up(X->nb_ptr, nb_ptr, s); up(X->nb, nb, s);
+  up(X->bg_ptr, bg_ptr, s); up(X->bg, bg, s); up(X->nb_ptr, nb_ptr, s); up(X->nb, nb, s); up(X->nb_inc, nb_inc, s);
   up(X->lnb_ptr, lnb_ptr, s); up(X->lnb, lnb, s);
   t.lent = X->lent.p; t.items = X->items.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
   t.fpos = X->fpos.p; t.apos = X->apos.p; t.lidx_to = X->lidx_to.p; t.lidx_from = X->lidx_from.p;
   t.gbus = X->gbus.p; t.ppos = X->ppos.p; t.qpos = X->qpos.p; t.g_ramp = X->g_ramp.p;
   t.ngp = X->ngp.p; t.ngq = X->ngq.p; t.bl_ptr = X->bl_ptr.p; t.bl = X->bl.p;
-  t.bg_ptr = X->bg_ptr.p; t.bg = X->bg.p; t.nb_ptr = X->nb_ptr.p; t.nb = X->nb.p;
+  t.bg_ptr = X->bg_ptr.p; t.bg = X->bg.p; t.nb_ptr = X->nb_ptr.p; t.nb = X->nb.p; t.nb_inc = X->nb_inc.p;
   t.lnb_ptr = X->lnb_ptr.p; t.lnb = X->lnb.p;
   t.rowptr = K->A.ptr.p; t.colptr = K->M.ptr.p;
   GN_CK(cudaStreamSynchronize(s));
@@ -713,6 +722,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
     }
   }
   X->ready = ok;
+  X->fused_ready = ok && opf_fused_verify(K);
   return ok;
 }
 

@@ -28,14 +28,22 @@ struct OpfKktTab {
   const int32_t *nb_ptr, *nb;           // [N+1] incident lines sorted by (other bus, l): l<<1|is_from
   const int32_t *lnb_ptr, *lnb;         // [L+1] lines l' > l sharing a bus: (l' , shared-bus bits)
   const int32_t *rowptr, *colptr;       // CSR(A) / CSC(M) from the generic build
+  // fused (recompute-from-x) path
+  int32_t pg0, qg0, p0, q0, v0, th0;    // variable block offsets (full x)
+  const double *lg, *lb, *c2;           // line G, B; generator c2
+  const int32_t* nb_inc;                // [nb] index of the nb entry in the bus's bl list
+  int32_t maxdeg;                       // max incident lines of a bus
 };
 
 struct OpfKkt {
   bool ready = false;
   OpfKktTab t{};
   DBuf<int32_t> lent, items, lf, lt, l_therm, lidx_to, lidx_from, gbus, ppos, qpos, g_ramp, ngp,
-      ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb;
+      ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb, nb_inc;
   DBuf<int8_t> fpos, apos;
+  bool fused_ready = false;
 };
+
+void count_diff(const int32_t* a, const int32_t* b, int64_t n, int32_t* diff, cudaStream_t s);
 
 }  // namespace gnb

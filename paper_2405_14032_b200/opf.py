@@ -254,10 +254,10 @@ class CondensedKkt:
                                         _i32(hc), device, C.byref(h), C.byref(err))
         _check(rc, err, "gn_kkt_create")
         self.h = h
-        d = (C.c_int64 * 8)()
+        d = (C.c_int64 * 9)()
         self.lib.gn_kkt_dims(h, d)
         self.dim, self.a_nnz, self.m_nnz, self.pair_count, self.jac_nnz, self.hess_nnz, \
-            self.n_rows, self.opf_ready = list(d)
+            self.n_rows, self.opf_ready, self.fused_ready = list(d)
 
     def close(self):
         if getattr(self, "h", None):
@@ -298,6 +298,17 @@ class CondensedKkt:
                  mem: int = GN_MEM_HOST):
         _check(self.lib.gn_kkt_assemble(self.h, _f64(hvals), _f64(sigma_x), _f64(sigma_s),
                                         float(delta_w), float(delta_c), mem))
+
+    def set_jacobian_x(self, x, mem: int = GN_MEM_HOST):
+        """A = set_jacobian(eval_jac(x)) computed from x (fused path)."""
+        _check(self.lib.gn_kkt_set_jacobian_x(self.h, _f64(x), mem))
+
+    def assemble_x(self, x, row_weights, obj_weight, sigma_x, sigma_s, delta_w, delta_c,
+                   mem: int = GN_MEM_HOST):
+        """M = assemble(eval_hess(x, w, ow), ...) computed from x (fused path)."""
+        _check(self.lib.gn_kkt_assemble_x(self.h, _f64(x), _f64(row_weights), float(obj_weight),
+                                          _f64(sigma_x), _f64(sigma_s), float(delta_w),
+                                          float(delta_c), mem))
 
     def values(self, a=None, m=None):
         a = np.empty(self.a_nnz) if a is None else a

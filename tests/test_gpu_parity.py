@@ -268,3 +268,49 @@ def test_specialised_kkt_equals_generic_and_oracle(gpu, T):
             OK.assemble(hv[lo["hess_pick"]], sx, ss, dw, dc)
             for a, b, nm in zip(K.values(), OK.values(), ("A", "M")):
                 assert_bitexact(a, b, f"{nm} algo={algo} dw={dw}")
+
+
+def _fused_check(nlp, K, x, w, ow, sx, ss):
+    """Fused A/M (from x) == set_jacobian(eval_jac(x)) / assemble(eval_hess(x, w, ow))."""
+    assert K.fused_ready == 1, "fused enumeration did not verify"
+    ok, jv = nlp.eval_jac(x)
+    ok2, hv = nlp.eval_hess(x, w, ow)
+    assert ok and ok2
+    K.set_jacobian(jv, mem=GN_IN_FULL)
+    for dw, dc in DELTAS:
+        K.assemble(hv, sx, ss, dw, dc, mem=GN_IN_FULL)
+        a_ref, m_ref = K.values()
+        K.set_jacobian_x(x)
+        K.assemble_x(x, w, ow, sx, ss, dw, dc)
+        a, m = K.values()
+        assert_bitexact(a, a_ref, f"fused A dw={dw}")
+        assert_bitexact(m, m_ref, f"fused M dw={dw}")
+        K.set_jacobian(jv, mem=GN_IN_FULL)  # restore the contract A for the next delta
+
+
+@pytest.mark.parametrize("fx", FIXTURES)
+def test_fused_kkt_equals_contract_path_fixtures(gpu, fx):
+    nlp, z, meta, net = _nlp(fx)
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    _fused_check(nlp, K, z["x"], z["w"], float(z["ow"]), z["sx"], z["ss"])
+    # and against the reference's own M (value tolerance: H/J differ by sin/cos ulps)
+    K.set_jacobian_x(z["x"])
+    K.assemble_x(z["x"], z["w"], float(z["ow"]), z["sx"], z["ss"], *DELTAS[1])
+    assert_close(K.values()[1], z["mvals1"], what="fused M vs reference")
+
+
+@pytest.mark.parametrize("T", [1, 2, 7, 40])
+def test_fused_kkt_equals_contract_path_edge_network(gpu, T):
+    from paper_2405_14032_b200.opf import load_profile
+    net = _edge_network(seed=30 + T)
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale)
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, T)
+    w = row_weights(nlp.sizes.n_cons, T + 1, zero_every=9)
+    sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, T + 2)
+    _fused_check(nlp, K, x, w, 0.7, sx, ss)
+    _fused_check(nlp, K, x, w, 0.0, sx, ss)  # restoration-style obj_weight 0
