@@ -113,10 +113,17 @@ def alg_bytes(s, kkt):
     return 8 * (2 * n + 2 * m + 1 + J + H) + 8 * (Jl + Hl + nl + m + M)
 
 
-def stage_bytes(s, kkt, net, periods):
+def stage_bytes(s, kkt, net, periods, fused=False):
     """Algorithmic bytes per call (contract inputs read once + outputs written once)."""
     n, m, J, H = s.n_vars, s.n_cons, s.jac_nnz, s.hess_nnz
     GT = net.n_gen * periods
+    if fused:  # A, M from x: x (+ w, sigma) read once, A / M written once
+        return {
+            "f": 8 * (GT + 1), "grad": 8 * (n + GT), "g": 8 * (n + m), "jac": 8 * (n + J),
+            "hess": 8 * (n + m + H),
+            "set_jacobian": 8 * (n + kkt.a_nnz),
+            "assemble": 8 * (n + 2 * m + s.n_free + kkt.m_nnz),
+        }
     return {
         "f": 8 * (GT + 1),
         "grad": 8 * (n + GT),
@@ -164,6 +171,9 @@ def run_ours(args, rank, world, local_rank, dist):
     A = GN_MEM_DEVICE_ASYNC
     L = abi.lib()
     stages = ["f", "grad", "g", "jac", "hess", "set_jacobian", "assemble"]
+    fused = args.pipeline == "fused"
+    if fused and not kkt.fused_ready:
+        raise SystemExit("fused KKT path unavailable (verification failed)")
 
     def step(ev=None):
         def mark(i):
@@ -180,9 +190,14 @@ def run_ours(args, rank, world, local_rank, dist):
         mark(4)
         nlp.eval_device("hess", dx, H, w=dwt, ow=1.0, sync=False)
         mark(5)
-        kkt.set_jacobian(J, mem=A | GN_IN_FULL)
-        mark(6)
-        kkt.assemble(H, dsx, dss, dw_reg, dc_reg, mem=A | GN_IN_FULL)
+        if fused:  # A and M straight from x: bit-identical to the contract path
+            kkt.set_jacobian_x(dx, mem=A)
+            mark(6)
+            kkt.assemble_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)
+        else:      # contract path: A from J, M from H (GN_IN_FULL: lifted gather fused)
+            kkt.set_jacobian(J, mem=A | GN_IN_FULL)
+            mark(6)
+            kkt.assemble(H, dsx, dss, dw_reg, dc_reg, mem=A | GN_IN_FULL)
         mark(7)
 
     for _ in range(args.warmup):
@@ -219,7 +234,7 @@ def run_ours(args, rank, world, local_rank, dist):
 
     # roofline: dominant call (one kernel: the KKT assembly / else the largest stage)
     peak, peak_kind = peaks()
-    sb = stage_bytes(s, kkt, net, args.periods)
+    sb = stage_bytes(s, kkt, net, args.periods, fused)
     dom = max(per_stage, key=per_stage.get)
     achieved = sb[dom] / (per_stage[dom] * 1e-3) / 1e9
     unit_bytes = alg_bytes(s, kkt)
@@ -293,6 +308,9 @@ def run_ours(args, rank, world, local_rank, dist):
                      "alg_bytes_per_launch": sb[dom], "traffic": None},
         "unit_roofline": {"alg_bytes": unit_bytes, "achieved": unit_gbs, "peak": peak,
                           "frac": unit_gbs / peak, "unit": "GB/s"},
+        "pipeline": ("fused: set_jacobian/assemble recompute J/H terms from x "
+                     "(bit-identical to the contract path, tested)") if fused else
+                    "contract: set_jacobian(J) + assemble(H) read the callback outputs",
         "stages_ms": per_stage,
         "setup_s": setup_s,
         "clocks": clk,
@@ -412,6 +430,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-periods", type=int, default=2)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
     args = ap.parse_args()
 
