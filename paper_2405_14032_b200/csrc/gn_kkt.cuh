@@ -34,7 +34,7 @@ struct gn_kkt {
   gnb::Csc M;                    // M lower CSC: ptr = colptr, idx = rowidx, slot = [hess|pair|diag]
   gnb::DBuf<int32_t> pka, pkb;   // per pair: CSR positions ka, kb
   gnb::DBuf<int32_t> arow;       // per CSR(A) entry: its row
-  gnb::DBuf<double> avals, mvals;
+  gnb::DBuf<double> avals, mvals, dvals;
   gnb::DBuf<double> sj, sh, ssx, sss;  // host-mode staging
   gnb::OpfKkt* opf = nullptr;    // OPF-specialised tables (gn_kkt_create_lifted)
 };

@@ -21,7 +21,6 @@
 
 namespace gnb {
 
-constexpr int kFW = 4;  // warps per CTA
 
 struct FIn {
   const double* __restrict__ x;
@@ -53,26 +52,25 @@ struct Ctx {
   const FIn& in;
   int32_t n, tt, T;
   int32_t b0, deg;
-  double* S;  // per-warp state: [deg][4][32] = Cs, Sn, cs, sn
+  double* S;  // per-warp state: [deg][6][32] = vf, vt, Cs, Sn, cs, sn
   int lane;
+  const double* dv;  // d_r per row (k_fz_dvec)
   int32_t off_pg, off_qg, off_p, off_q, off_v, off_th;
 
   __device__ int32_t inc(int i) const { return __ldg(t.bl + b0 + i); }
   __device__ LineState st(int i) const {
-    const int32_t e = inc(i), l = e >> 1;
-    const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
+    const double* q = S + (i * 6) * 32 + lane;
     LineState s;
-    s.vf = in.x[t.v0 + (int64_t)f * T + tt];
-    s.vt = in.x[t.v0 + (int64_t)to * T + tt];
+    s.vf = q[0];
+    s.vt = q[32];
     s.vfvt = s.vf * s.vt;
-    const double* q = S + (i * 4) * 32 + lane;
-    s.Cs = q[0];
-    s.Sn = q[32];
-    s.cs = q[64];
-    s.sn = q[96];
+    s.Cs = q[64];
+    s.Sn = q[96];
+    s.cs = q[128];
+    s.sn = q[160];
     return s;
   }
-  __device__ double d(int32_t row) const { return dvec(in.ss[row], in.dw, in.dc); }
+  __device__ double d(int32_t row) const { return dv[row]; }
   __device__ double wt(int32_t row) const { return in.w[row]; }
   __device__ int32_t col(int32_t off, int32_t e) const {
     const int32_t k = f_lent(t, off, e);
@@ -317,17 +315,28 @@ __device__ void fused_bus(const Ctx& c, double* M, int32_t* rows, int32_t* bad) 
     check(o, ct);
   }
 
-  // ------------------------------------------------- p(l), q(l) for lines keyed at n
-  for (int i = 0; i < deg; ++i) {
-    const int32_t e = c.inc(i), l = e >> 1, fr = e & 1;
+}
+
+// p(l) and q(l) columns of line l at period c.tt (thread per (l, t)).
+template <bool STRUCT>
+__device__ void fz_line_cols(const Ctx& c, int32_t l, double* M, int32_t* rows, int32_t* bad) {
+  const OpfKktTab& t = c.t;
+  const FIn& in = c.in;
+  const int32_t T = c.T, tt = c.tt;
+  auto check = [&](const FOut<STRUCT>& o, int32_t cc) {
+    if (STRUCT && o.base + o.j != __ldg(t.colptr + cc + 1)) atomicOr(bad, 1);
+  };
+  {
     const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
-    const int32_t ob = fr ? to : f;
-    if (ob < n) continue;  // keyed at the smaller terminal
-    const int32_t blo = n, bhi = ob;
+    const int32_t blo = min(f, to), bhi = max(f, to);
     const int32_t k = __ldg(t.l_therm + l);
     const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
     const int64_t r = (int64_t)l * T + tt;
     const double sgn_lo = (blo == to) ? 1.0 : -1.0, sgn_hi = (bhi == to) ? 1.0 : -1.0;
+    LineState s{};
+    if constexpr (!STRUCT)
+      s = line_state(G, B, in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
+                     in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
 #pragma unroll
     for (int Q = 0; Q < 2; ++Q) {
       const int32_t cc = c.col(Q ? c.off_q : c.off_p, l);
@@ -369,8 +378,6 @@ __device__ void fused_bus(const Ctx& c, double* M, int32_t* rows, int32_t* bad) 
         }
         o.put(acc, c.col(c.off_q, l));
       }
-      LineState s;
-      if constexpr (!STRUCT) s = c.st(i);
 #pragma unroll
       for (int blk = 0; blk < 2; ++blk)
 #pragma unroll
@@ -389,11 +396,22 @@ __device__ void fused_bus(const Ctx& c, double* M, int32_t* rows, int32_t* bad) 
       check(o, cc);
     }
   }
+}
 
-  // ------------------------------------------------------- pg(g), qg(g) at n
+// pg(g) and qg(g) columns of generator g at period c.tt (thread per (g, t)).
+template <bool STRUCT>
+__device__ void fz_gen_cols(const Ctx& c, int32_t gsel, double* M, int32_t* rows, int32_t* bad) {
+  const OpfKktTab& t = c.t;
+  const FIn& in = c.in;
+  const int32_t T = c.T, tt = c.tt;
+  const int32_t n = __ldg(t.gbus + gsel);
+  const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
+  auto check = [&](const FOut<STRUCT>& o, int32_t cc) {
+    if (STRUCT && o.base + o.j != __ldg(t.colptr + cc + 1)) atomicOr(bad, 1);
+  };
   const int32_t g0 = __ldg(t.bg_ptr + n), g1 = __ldg(t.bg_ptr + n + 1);
-  for (int32_t gi = g0; gi < g1; ++gi) {
-    const int32_t g = __ldg(t.bg + gi);
+  {
+    const int32_t g = gsel;
 #pragma unroll
     for (int Q = 0; Q < 2; ++Q) {
       const int32_t cc = c.col(Q ? c.off_qg : c.off_pg, g);
@@ -429,7 +447,7 @@ __device__ void fused_bus(const Ctx& c, double* M, int32_t* rows, int32_t* bad) 
         o.put(acc, c2c);
       }
       for (int i = 0; i < deg; ++i) {
-        const int32_t e = c.inc(i), l = e >> 1;
+        const int32_t e = __ldg(t.bl + b0 + i), l = e >> 1;
         double acc = 0.0;
         if constexpr (!STRUCT) acc += pair_term(c.d(rb), (e & 1) ? -1.0 : 1.0, 1.0);
         o.put(acc, c.col(Q ? c.off_q : c.off_p, l));
@@ -439,13 +457,23 @@ __device__ void fused_bus(const Ctx& c, double* M, int32_t* rows, int32_t* bad) 
   }
 }
 
+// d_r for every row (condensed.hpp:111-117), once per assemble call.
+__global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __restrict__ ss, double dw,
+                                                 double dc, double* __restrict__ dv) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < m) dv[r] = dvec(ss[r], dw, dc);
+}
+
+constexpr int kBW = 2;  // warps per CTA of the bus kernel
+
 template <bool STRUCT>
-__global__ void __launch_bounds__(kFW * 32) k_opf_fused(OpfKktTab t, FIn in, double* __restrict__ M,
-                                                        int32_t* __restrict__ rows,
-                                                        int32_t* __restrict__ bad) {
+__global__ void __launch_bounds__(kBW * 32) k_fz_bus(OpfKktTab t, FIn in, const double* __restrict__ dv,
+                                                     double* __restrict__ M,
+                                                     int32_t* __restrict__ rows,
+                                                     int32_t* __restrict__ bad) {
   extern __shared__ double fsm[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kFW + warp;
+  const int64_t w = (int64_t)blockIdx.x * kBW + warp;
   const int64_t n64 = w / t.tchunks;
   if (n64 >= t.N) return;
   const int32_t n = (int32_t)n64;
@@ -453,24 +481,50 @@ __global__ void __launch_bounds__(kFW * 32) k_opf_fused(OpfKktTab t, FIn in, dou
   if (tt >= t.T) return;
   const int32_t T = t.T;
   const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
-  double* S = fsm + (size_t)warp * t.maxdeg * 4 * 32;
-  Ctx c{t, in, n, tt, T, b0, deg, S, lane,
+  double* S = fsm + (size_t)warp * t.maxdeg * 6 * 32;
+  Ctx c{t, in, n, tt, T, b0, deg, S, lane, dv,
         0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
   if constexpr (!STRUCT) {
-    for (int i = 0; i < deg; ++i) {  // trigonometric state of every incident line
+    for (int i = 0; i < deg; ++i) {  // state of every incident line, once per lane
       const int32_t l = __ldg(t.bl + b0 + i) >> 1;
       const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
       const LineState s = line_state(__ldg(t.lg + l), __ldg(t.lb + l),
                                      in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
                                      in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
-      double* q = S + (i * 4) * 32 + lane;
-      q[0] = s.Cs;
-      q[32] = s.Sn;
-      q[64] = s.cs;
-      q[96] = s.sn;
+      double* q = S + (i * 6) * 32 + lane;
+      q[0] = s.vf;
+      q[32] = s.vt;
+      q[64] = s.Cs;
+      q[96] = s.Sn;
+      q[128] = s.cs;
+      q[160] = s.sn;
     }
   }
   fused_bus<STRUCT>(c, M, rows, bad);
+}
+
+template <bool STRUCT>
+__global__ void __launch_bounds__(256) k_fz_line(OpfKktTab t, FIn in, const double* __restrict__ dv,
+                                                 double* __restrict__ M, int32_t* __restrict__ rows,
+                                                 int32_t* __restrict__ bad) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (int64_t)t.L * t.T) return;
+  const int32_t l = (int32_t)(r / t.T), tt = (int32_t)(r - (int64_t)l * t.T);
+  Ctx c{t, in, 0, tt, t.T, 0, 0, nullptr, 0, dv,
+        0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
+  fz_line_cols<STRUCT>(c, l, M, rows, bad);
+}
+
+template <bool STRUCT>
+__global__ void __launch_bounds__(256) k_fz_gen(OpfKktTab t, FIn in, const double* __restrict__ dv,
+                                                double* __restrict__ M, int32_t* __restrict__ rows,
+                                                int32_t* __restrict__ bad) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= (int64_t)t.G * t.T) return;
+  const int32_t g = (int32_t)(r / t.T), tt = (int32_t)(r - (int64_t)g * t.T);
+  Ctx c{t, in, 0, tt, t.T, 0, 0, nullptr, 0, dv,
+        0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
+  fz_gen_cols<STRUCT>(c, g, M, rows, bad);
 }
 
 // ------------------------------------------------------ A straight from x
@@ -534,25 +588,45 @@ __global__ void k_opf_set_jac_thermal(OpfKktTab t, const double* __restrict__ x,
 
 // ------------------------------------------------------------------ host
 static size_t fused_smem(const OpfKktTab& t) {
-  return (size_t)kFW * (size_t)(t.maxdeg > 0 ? t.maxdeg : 1) * 4 * 32 * sizeof(double);
+  return (size_t)kBW * (size_t)(t.maxdeg > 0 ? t.maxdeg : 1) * 6 * 32 * sizeof(double);
 }
 
 static int64_t fused_blocks(const OpfKktTab& t) {
-  return ((int64_t)t.N * t.tchunks + kFW - 1) / kFW;
+  return ((int64_t)t.N * t.tchunks + kBW - 1) / kBW;
+}
+
+template <bool STRUCT>
+static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, int32_t* rows,
+                         int32_t* bad) {
+  const OpfKktTab& t = K->opf->t;
+  cudaStream_t s = K->stream;
+  const int64_t bb = fused_blocks(t);
+  if (bb > 0) {
+    k_fz_bus<STRUCT><<<(unsigned)bb, kBW * 32, fused_smem(t), s>>>(t, in, dv, M, rows, bad);
+    count_launch();
+  }
+  const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
+  if (nl > 0) {
+    k_fz_line<STRUCT><<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
+    count_launch();
+  }
+  if (ng > 0) {
+    k_fz_gen<STRUCT><<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
+    count_launch();
+  }
+  GN_CK(cudaGetLastError());
 }
 
 bool opf_fused_ready(const gn_kkt* K) { return K->opf && K->opf->fused_ready; }
 
 void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
                         const double* ss, double dw, double dc) {
-  const OpfKktTab& t = K->opf->t;
-  const int64_t blocks = fused_blocks(t);
-  if (blocks <= 0) return;
   FIn in{x, w, ow, sx, ss, dw, dc};
-  k_opf_fused<false><<<(unsigned)blocks, kFW * 32, fused_smem(t), K->stream>>>(t, in, K->mvals.p,
-                                                                                nullptr, nullptr);
-  count_launch();
-  GN_CK(cudaGetLastError());
+  if (K->m > 0) {
+    k_fz_dvec<<<(unsigned)((K->m + 255) / 256), 256, 0, K->stream>>>(K->m, ss, dw, dc, K->dvals.p);
+    count_launch();
+  }
+  launch_fused<false>(K, in, K->dvals.p, K->mvals.p, nullptr, nullptr);
 }
 
 void opf_set_jacobian_fused(gn_kkt* K, const double* x) {
@@ -573,12 +647,11 @@ bool opf_fused_verify(gn_kkt* K) {
   const OpfKktTab& t = K->opf->t;
   const size_t smem = fused_smem(t);
   if (smem > 200 * 1024) return false;
-  GN_CK(cudaFuncSetAttribute(k_opf_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  GN_CK(cudaFuncSetAttribute(k_fz_bus<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem));
-  GN_CK(cudaFuncSetAttribute(k_opf_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  GN_CK(cudaFuncSetAttribute(k_fz_bus<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem));
-  const int64_t blocks = fused_blocks(t);
-  if (blocks <= 0) return false;
+  K->dvals.alloc(static_cast<size_t>(K->m) + 1);
   cudaStream_t s = K->stream;
   DBuf<int32_t> rows, bad, diff;
   rows.alloc(static_cast<size_t>(K->mnnz) + 1);
@@ -588,9 +661,7 @@ bool opf_fused_verify(gn_kkt* K) {
   GN_CK(cudaMemsetAsync(diff.p, 0, 4, s));
   GN_CK(cudaMemsetAsync(rows.p, 0xff, sizeof(int32_t) * K->mnnz, s));
   FIn in{};
-  k_opf_fused<true><<<(unsigned)blocks, kFW * 32, smem, s>>>(t, in, nullptr, rows.p, bad.p);
-  count_launch();
-  GN_CK(cudaGetLastError());
+  launch_fused<true>(K, in, nullptr, nullptr, rows.p, bad.p);
   count_diff(rows.p, K->M.idx.p, K->mnnz, diff.p, s);
   int32_t hb[2] = {0, 0};
   GN_CK(cudaMemcpyAsync(&hb[0], bad.p, 4, cudaMemcpyDeviceToHost, s));
