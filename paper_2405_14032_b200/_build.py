@@ -75,7 +75,7 @@ def build_oracle(with_reference: bool | None = None) -> None:
     if with_reference is None:
         with_reference = Path("/root/reference/proj/include").exists()
     if with_reference:
-        r = subprocess.run(["make", "-C", str(oracle), "ref"], capture_output=True, text=True)
+        r = subprocess.run(["make", "-C", str(oracle), "ref", "dropin"], capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"oracle/_ref build failed:\n{r.stdout}\n{r.stderr}")
 
