@@ -22,15 +22,6 @@
 namespace gnb {
 
 
-struct FIn {
-  const double* __restrict__ x;
-  const double* __restrict__ w;
-  double ow;
-  const double* __restrict__ sx;
-  const double* __restrict__ ss;
-  double dw, dc;
-};
-
 template <bool STRUCT>
 struct FOut {
   double* M;
@@ -52,7 +43,7 @@ struct Ctx {
   const FIn& in;
   int32_t n, tt, T;
   int32_t b0, deg;
-  double* S;  // per-warp state: [deg][6][32] = vf, vt, Cs, Sn, cs, sn
+  double* S;  // unused by the line/generator kernels
   int lane;
   const double* dv;  // d_r per row (k_fz_dvec)
   int32_t off_pg, off_qg, off_p, off_q, off_v, off_th;
@@ -77,245 +68,6 @@ struct Ctx {
     return k < 0 ? -1 : k * T + tt;
   }
 };
-
-// ----------------------------------------------------------------- columns
-template <bool STRUCT>
-__device__ void fused_bus(const Ctx& c, double* M, int32_t* rows, int32_t* bad) {
-  const OpfKktTab& t = c.t;
-  const FIn& in = c.in;
-  const int32_t T = c.T, tt = c.tt, n = c.n;
-  const int32_t deg = c.deg;
-  const int32_t q0 = __ldg(t.nb_ptr + n), q1 = __ldg(t.nb_ptr + n + 1);
-  auto fr_of = [&](int i) { return c.inc(i) & 1; };
-  auto line_of = [&](int i) { return c.inc(i) >> 1; };
-  auto other_nb = [&](int32_t u) {
-    const int32_t e = __ldg(t.nb + u), l = e >> 1;
-    return (e & 1) ? __ldg(t.lt + l) : __ldg(t.lf + l);
-  };
-  auto check = [&](const FOut<STRUCT>& o, int32_t cc) {
-    if (STRUCT && o.base + o.j != __ldg(t.colptr + cc + 1)) atomicOr(bad, 1);
-  };
-
-  // ------------------------------------------------------------ v(n)
-  const int32_t cv = c.col(c.off_v, n);
-  if (cv >= 0) {
-    FOut<STRUCT> o{M, rows, __ldg(t.colptr + cv), 0};
-    {  // diagonal
-      double acc = 0.0;
-      if constexpr (!STRUCT) {
-        for (int i = 0; i < deg; ++i)
-          if (fr_of(i)) {
-            const int32_t l = line_of(i);
-            acc += h_flow_p(c.st(i), __ldg(t.lg + l), c.wt(t.flow_p0 + l * T + tt), 5);
-          }
-        for (int i = 0; i < deg; ++i)
-          if (fr_of(i)) {
-            const int32_t l = line_of(i);
-            acc += h_flow_q(c.st(i), __ldg(t.lb + l), c.wt(t.flow_q0 + l * T + tt), 5);
-          }
-        for (int i = 0; i < deg; ++i) {
-          const int32_t l = line_of(i);
-          const double j = j_flow_p(c.st(i), __ldg(t.lg + l), __ldg(t.lb + l), fr_of(i) ? 1 : 2);
-          acc += pair_term(c.d(t.flow_p0 + l * T + tt), j, j);
-        }
-        for (int i = 0; i < deg; ++i) {
-          const int32_t l = line_of(i);
-          const double j = j_flow_q(c.st(i), __ldg(t.lg + l), __ldg(t.lb + l), fr_of(i) ? 1 : 2);
-          acc += pair_term(c.d(t.flow_q0 + l * T + tt), j, j);
-        }
-        acc += in.dw + in.sx[cv];
-      }
-      o.put(acc, cv);
-    }
-    // v(n') for neighbours n' > n
-    for (int32_t u0 = q0; u0 < q1;) {
-      const int32_t nb = other_nb(u0);
-      int32_t u1 = u0 + 1;
-      while (u1 < q1 && other_nb(u1) == nb) ++u1;
-      const int32_t cr = c.col(c.off_v, nb);
-      if (nb > n && cr >= 0) {
-        double acc = 0.0;
-        if constexpr (!STRUCT) {
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i);
-            acc += h_flow_p(c.st(i), __ldg(t.lg + l), c.wt(t.flow_p0 + l * T + tt), 6);
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i);
-            acc += h_flow_q(c.st(i), __ldg(t.lb + l), c.wt(t.flow_q0 + l * T + tt), 6);
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i), fr = fr_of(i);
-            const LineState s = c.st(i);
-            const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-            acc += pair_term(c.d(t.flow_p0 + l * T + tt), j_flow_p(s, G, B, fr ? 2 : 1),
-                             j_flow_p(s, G, B, fr ? 1 : 2));
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i), fr = fr_of(i);
-            const LineState s = c.st(i);
-            const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-            acc += pair_term(c.d(t.flow_q0 + l * T + tt), j_flow_q(s, G, B, fr ? 2 : 1),
-                             j_flow_q(s, G, B, fr ? 1 : 2));
-          }
-        }
-        o.put(acc, cr);
-      }
-      u0 = u1;
-    }
-    // th(x), x in {n} U neighbours ascending
-    bool self_done = false;
-    for (int32_t u0 = q0; u0 <= q1;) {
-      int32_t nb = 0x7fffffff, u1 = u0 + 1;
-      if (u0 < q1) {
-        nb = other_nb(u0);
-        while (u1 < q1 && other_nb(u1) == nb) ++u1;
-      }
-      if (!self_done && n < nb) {
-        self_done = true;
-        const int32_t cr = c.col(c.off_th, n);
-        if (cr >= 0) {
-          double acc = 0.0;
-          if constexpr (!STRUCT) {
-            for (int i = 0; i < deg; ++i) {
-              const int32_t l = line_of(i);
-              acc += h_flow_p(c.st(i), __ldg(t.lg + l), c.wt(t.flow_p0 + l * T + tt), fr_of(i) ? 7 : 11);
-            }
-            for (int i = 0; i < deg; ++i) {
-              const int32_t l = line_of(i);
-              acc += h_flow_q(c.st(i), __ldg(t.lb + l), c.wt(t.flow_q0 + l * T + tt), fr_of(i) ? 7 : 11);
-            }
-            for (int i = 0; i < deg; ++i) {
-              const int32_t l = line_of(i), fr = fr_of(i);
-              const LineState s = c.st(i);
-              const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-              acc += pair_term(c.d(t.flow_p0 + l * T + tt), j_flow_p(s, G, B, fr ? 3 : 4),
-                               j_flow_p(s, G, B, fr ? 1 : 2));
-            }
-            for (int i = 0; i < deg; ++i) {
-              const int32_t l = line_of(i), fr = fr_of(i);
-              const LineState s = c.st(i);
-              const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-              acc += pair_term(c.d(t.flow_q0 + l * T + tt), j_flow_q(s, G, B, fr ? 3 : 4),
-                               j_flow_q(s, G, B, fr ? 1 : 2));
-            }
-          }
-          o.put(acc, cr);
-        }
-        continue;
-      }
-      if (u0 >= q1) break;
-      const int32_t cr = c.col(c.off_th, nb);
-      if (cr >= 0) {
-        double acc = 0.0;
-        if constexpr (!STRUCT) {
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i);
-            acc += h_flow_p(c.st(i), __ldg(t.lg + l), c.wt(t.flow_p0 + l * T + tt), fr_of(i) ? 8 : 10);
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i);
-            acc += h_flow_q(c.st(i), __ldg(t.lb + l), c.wt(t.flow_q0 + l * T + tt), fr_of(i) ? 8 : 10);
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i), fr = fr_of(i);
-            const LineState s = c.st(i);
-            const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-            acc += pair_term(c.d(t.flow_p0 + l * T + tt), j_flow_p(s, G, B, fr ? 4 : 3),
-                             j_flow_p(s, G, B, fr ? 1 : 2));
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i), fr = fr_of(i);
-            const LineState s = c.st(i);
-            const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-            acc += pair_term(c.d(t.flow_q0 + l * T + tt), j_flow_q(s, G, B, fr ? 4 : 3),
-                             j_flow_q(s, G, B, fr ? 1 : 2));
-          }
-        }
-        o.put(acc, cr);
-      }
-      u0 = u1;
-    }
-    check(o, cv);
-  }
-
-  // ------------------------------------------------------------ th(n)
-  const int32_t ct = c.col(c.off_th, n);
-  if (ct >= 0) {
-    FOut<STRUCT> o{M, rows, __ldg(t.colptr + ct), 0};
-    {
-      double acc = 0.0;
-      if constexpr (!STRUCT) {
-        for (int i = 0; i < deg; ++i) {
-          const int32_t l = line_of(i);
-          acc += h_flow_p(c.st(i), __ldg(t.lg + l), c.wt(t.flow_p0 + l * T + tt), fr_of(i) ? 12 : 14);
-        }
-        for (int i = 0; i < deg; ++i) {
-          const int32_t l = line_of(i);
-          acc += h_flow_q(c.st(i), __ldg(t.lb + l), c.wt(t.flow_q0 + l * T + tt), fr_of(i) ? 12 : 14);
-        }
-        for (int i = 0; i < deg; ++i) {
-          const int32_t l = line_of(i), fr = fr_of(i);
-          const double j = j_flow_p(c.st(i), __ldg(t.lg + l), __ldg(t.lb + l), fr ? 3 : 4);
-          acc += pair_term(c.d(t.flow_p0 + l * T + tt), j, j);
-        }
-        for (int i = 0; i < deg; ++i) {
-          const int32_t l = line_of(i), fr = fr_of(i);
-          const double j = j_flow_q(c.st(i), __ldg(t.lg + l), __ldg(t.lb + l), fr ? 3 : 4);
-          acc += pair_term(c.d(t.flow_q0 + l * T + tt), j, j);
-        }
-        for (int i = 0; i < deg; ++i) {
-          const int32_t l = line_of(i);
-          const double a = fr_of(i) ? 1.0 : -1.0;  // angle J: (th_f, th_t) = (1, -1)
-          acc += pair_term(c.d(t.ang0 + l * T + tt), a, a);
-        }
-        acc += in.dw + in.sx[ct];
-      }
-      o.put(acc, ct);
-    }
-    for (int32_t u0 = q0; u0 < q1;) {
-      const int32_t nb = other_nb(u0);
-      int32_t u1 = u0 + 1;
-      while (u1 < q1 && other_nb(u1) == nb) ++u1;
-      const int32_t cr = c.col(c.off_th, nb);
-      if (nb > n && cr >= 0) {
-        double acc = 0.0;
-        if constexpr (!STRUCT) {
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i);
-            acc += h_flow_p(c.st(i), __ldg(t.lg + l), c.wt(t.flow_p0 + l * T + tt), 13);
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i);
-            acc += h_flow_q(c.st(i), __ldg(t.lb + l), c.wt(t.flow_q0 + l * T + tt), 13);
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i), fr = fr_of(i);
-            const LineState s = c.st(i);
-            const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-            acc += pair_term(c.d(t.flow_p0 + l * T + tt), j_flow_p(s, G, B, fr ? 4 : 3),
-                             j_flow_p(s, G, B, fr ? 3 : 4));
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i), fr = fr_of(i);
-            const LineState s = c.st(i);
-            const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-            acc += pair_term(c.d(t.flow_q0 + l * T + tt), j_flow_q(s, G, B, fr ? 4 : 3),
-                             j_flow_q(s, G, B, fr ? 3 : 4));
-          }
-          for (int32_t u = u0; u < u1; ++u) {
-            const int i = __ldg(t.nb_inc + u), l = line_of(i), fr = fr_of(i);
-            acc += pair_term(c.d(t.ang0 + l * T + tt), fr ? -1.0 : 1.0, fr ? 1.0 : -1.0);
-          }
-        }
-        o.put(acc, cr);
-      }
-      u0 = u1;
-    }
-    check(o, ct);
-  }
-
-}
 
 // p(l) and q(l) columns of line l at period c.tt (thread per (l, t)).
 template <bool STRUCT>
@@ -464,45 +216,6 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
   if (r < m) dv[r] = dvec(ss[r], dw, dc);
 }
 
-constexpr int kBW = 2;  // warps per CTA of the bus kernel
-
-template <bool STRUCT>
-__global__ void __launch_bounds__(kBW * 32) k_fz_bus(OpfKktTab t, FIn in, const double* __restrict__ dv,
-                                                     double* __restrict__ M,
-                                                     int32_t* __restrict__ rows,
-                                                     int32_t* __restrict__ bad) {
-  extern __shared__ double fsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kBW + warp;
-  const int64_t n64 = w / t.tchunks;
-  if (n64 >= t.N) return;
-  const int32_t n = (int32_t)n64;
-  const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
-  if (tt >= t.T) return;
-  const int32_t T = t.T;
-  const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
-  double* S = fsm + (size_t)warp * t.maxdeg * 6 * 32;
-  Ctx c{t, in, n, tt, T, b0, deg, S, lane, dv,
-        0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
-  if constexpr (!STRUCT) {
-    for (int i = 0; i < deg; ++i) {  // state of every incident line, once per lane
-      const int32_t l = __ldg(t.bl + b0 + i) >> 1;
-      const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
-      const LineState s = line_state(__ldg(t.lg + l), __ldg(t.lb + l),
-                                     in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
-                                     in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
-      double* q = S + (i * 6) * 32 + lane;
-      q[0] = s.vf;
-      q[32] = s.vt;
-      q[64] = s.Cs;
-      q[96] = s.Sn;
-      q[128] = s.cs;
-      q[160] = s.sn;
-    }
-  }
-  fused_bus<STRUCT>(c, M, rows, bad);
-}
-
 template <bool STRUCT>
 __global__ void __launch_bounds__(256) k_fz_line(OpfKktTab t, FIn in, const double* __restrict__ dv,
                                                  double* __restrict__ M, int32_t* __restrict__ rows,
@@ -587,24 +300,13 @@ __global__ void k_opf_set_jac_thermal(OpfKktTab t, const double* __restrict__ x,
 }
 
 // ------------------------------------------------------------------ host
-static size_t fused_smem(const OpfKktTab& t) {
-  return (size_t)kBW * (size_t)(t.maxdeg > 0 ? t.maxdeg : 1) * 6 * 32 * sizeof(double);
-}
-
-static int64_t fused_blocks(const OpfKktTab& t) {
-  return ((int64_t)t.N * t.tchunks + kBW - 1) / kBW;
-}
-
 template <bool STRUCT>
 static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, int32_t* rows,
                          int32_t* bad) {
   const OpfKktTab& t = K->opf->t;
   cudaStream_t s = K->stream;
-  const int64_t bb = fused_blocks(t);
-  if (bb > 0) {
-    k_fz_bus<STRUCT><<<(unsigned)bb, kBW * 32, fused_smem(t), s>>>(t, in, dv, M, rows, bad);
-    count_launch();
-  }
+  if (K->opf->n_bus_items > 0)
+    launch_fz_bus(t, K->opf->bus_items.p, K->opf->n_bus_items, in, dv, M, rows, bad, s);
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
     k_fz_line<STRUCT><<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
@@ -645,13 +347,23 @@ void opf_set_jacobian_fused(gn_kkt* K, const double* x) {
 // Structure check of the fused enumeration (row index of every slot, column lengths).
 bool opf_fused_verify(gn_kkt* K) {
   const OpfKktTab& t = K->opf->t;
-  const size_t smem = fused_smem(t);
-  if (smem > 200 * 1024) return false;
-  GN_CK(cudaFuncSetAttribute(k_fz_bus<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem));
-  GN_CK(cudaFuncSetAttribute(k_fz_bus<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem));
+  if (t.maxdeg > 32) return false;  // bus-column kernel holds one line per lane
   K->dvals.alloc(static_cast<size_t>(K->m) + 1);
+  {  // work list of the bus-column kernel: (bus, first period) per warp
+    std::vector<int32_t> bp(t.N + 1);
+    GN_CK(cudaMemcpyAsync(bp.data(), t.bl_ptr, sizeof(int32_t) * (t.N + 1), cudaMemcpyDeviceToHost,
+                          K->stream));
+    GN_CK(cudaStreamSynchronize(K->stream));
+    std::vector<int2> items;
+    for (int32_t n = 0; n < t.N; ++n) {
+      int P = 1;
+      while (P < bp[n + 1] - bp[n]) P <<= 1;
+      const int per = 32 / P;
+      for (int32_t t0 = 0; t0 < t.T; t0 += per) items.push_back(make_int2(n, t0));
+    }
+    K->opf->bus_items.upload(items.data(), items.size(), K->stream);
+    K->opf->n_bus_items = static_cast<int64_t>(items.size());
+  }
   cudaStream_t s = K->stream;
   DBuf<int32_t> rows, bad, diff;
   rows.alloc(static_cast<size_t>(K->mnnz) + 1);

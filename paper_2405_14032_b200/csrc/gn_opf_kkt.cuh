@@ -35,6 +35,21 @@ struct OpfKktTab {
   int32_t maxdeg;                       // max incident lines of a bus
 };
 
+// Inputs of the fused (recompute-from-x) assembly.
+struct FIn {
+  const double* __restrict__ x;
+  const double* __restrict__ w;
+  double ow;
+  const double* __restrict__ sx;
+  const double* __restrict__ ss;
+  double dw, dc;
+};
+
+// Bus-column kernel (v(n), th(n) columns): one warp per (bus, period chunk);
+// lanes = (32/P periods) x (P incident-line slots), P = next pow2 >= degree.
+void launch_fz_bus(const OpfKktTab& t, const int2* items, int64_t n_items, const FIn& in,
+                   const double* dv, double* M, int32_t* rows, int32_t* bad, cudaStream_t s);
+
 struct OpfKkt {
   bool ready = false;
   OpfKktTab t{};
@@ -42,6 +57,8 @@ struct OpfKkt {
       ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb, nb_inc;
   DBuf<int8_t> fpos, apos;
   bool fused_ready = false;
+  DBuf<int2> bus_items;  // (bus, first period) per warp of the bus-column kernel
+  int64_t n_bus_items = 0;
 };
 
 void count_diff(const int32_t* a, const int32_t* b, int64_t n, int32_t* diff, cudaStream_t s);

@@ -1,0 +1,94 @@
+"""Summarise ncu outputs into the small text files committed under profiles/.
+
+  python profiles/summarize.py launches <launches.csv> <out.md>
+      per-kernel launch count, total / mean device time and share of the
+      timed steps (from `ncu --metrics gpu__time_duration.sum --csv`)
+  python profiles/summarize.py full <report.ncu-rep> <out.md> [traffic.json]
+      key metrics of every profiled kernel of an `ncu --set full` capture
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+import subprocess
+import sys
+from collections import OrderedDict
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "DRAM % of peak"),
+    ("lts__t_sector_hit_rate.pct", "L2 hit %"),
+    ("l1tex__t_sector_hit_rate.pct", "L1 hit %"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__inst_executed.sum", "instructions"),
+    ("launch__registers_per_thread", "registers"),
+    ("smsp__average_warp_latency_per_inst_issued.ratio", "cycles/inst"),
+]
+
+
+def short(name: str) -> str:
+    return name.split("(")[0].replace("void ", "").strip()
+
+
+def launches(path: str, out: str):
+    text = open(path).read().splitlines()
+    start = next(i for i, l in enumerate(text) if l.startswith('"ID"'))
+    rows = [r for r in csv.DictReader(text[start:]) if r.get("Metric Name") == "gpu__time_duration.sum"]
+    agg: "OrderedDict[str, list]" = OrderedDict()
+    for r in rows:
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "ns")
+        us = v / 1000.0 if unit == "nsecond" or unit == "ns" else (v * 1000.0 if unit in ("msecond", "ms") else v)
+        agg.setdefault(short(r["Kernel Name"]), []).append(us)
+    total = sum(sum(v) for v in agg.values())
+    lines = ["| kernel | launches | total us | mean us | share |", "|---|---:|---:|---:|---:|"]
+    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.2f} | {sum(v)/total:.1%} |")
+    lines.append(f"\n{len(rows)} launches, {total/1000:.3f} ms total device time (cold-cache, serialised).")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+
+
+def full(rep: str, out: str, traffic_json: str | None = None):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    head, units = rows[0], rows[1]
+    lines = ["| kernel | " + " | ".join(lbl for _, lbl in KEYS) + " |",
+             "|---|" + "---:|" * len(KEYS)]
+    traffic = {}
+    for r in rows[2:]:
+        name = short(r[head.index("Kernel Name")])
+        cells = []
+        for key, _ in KEYS:
+            try:
+                i = head.index(key)
+                cells.append(f"{r[i]} {units[i]}".strip())
+            except ValueError:
+                cells.append("-")
+        lines.append(f"| `{name}` | " + " | ".join(cells) + " |")
+        try:
+            rd = float(r[head.index("dram__bytes_read.sum")]) * _scale(units[head.index("dram__bytes_read.sum")])
+            wr = float(r[head.index("dram__bytes_write.sum")]) * _scale(units[head.index("dram__bytes_write.sum")])
+            traffic[name] = rd + wr
+        except (ValueError, IndexError):
+            pass
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines))
+    if traffic_json:
+        json.dump(traffic, open(traffic_json, "w"), indent=1)
+
+
+def _scale(unit: str) -> float:
+    return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1.0)
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "launches":
+        launches(sys.argv[2], sys.argv[3])
+    else:
+        full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)
