@@ -107,125 +107,54 @@ __global__ void __launch_bounds__(kBW2 * 32) k_fz_bus2(OpfKktTab t, const int2* 
       b.py10 = pair_term(d10, ao, an);
     }
   }
-  // ordered sums over all lines / over the lines of a neighbour group
-#define SUM_ALL(acc, fld) for (int k = 0; k < deg; ++k) acc += shfl(b.fld, base + k)
-#define SUM_GRP(acc, fld)                                 \
-  for (int32_t u = u0; u < u1; ++u) acc += shfl(b.fld, base + __ldg(t.nb_inc + u))
-
-  const int32_t q0 = __ldg(t.nb_ptr + n), q1 = __ldg(t.nb_ptr + n + 1);
-  auto other_nb = [&](int32_t u) {
-    const int32_t e = __ldg(t.nb + u), l = e >> 1;
-    return (e & 1) ? __ldg(t.lt + l) : __ldg(t.lf + l);
-  };
+  // Per-bus slot program (built on the host, opf_kkt_prepare): each slot is
+  // (lane mask of its lines, type, row entity); types 0-3 belong to v(n),
+  // 4-5 to th(n).  Mask bits ascend with l, so the shuffle order is the
+  // reference's record order.
+  const int32_t p0 = __ldg(t.bprog_ptr + n), p1 = __ldg(t.bprog_ptr + n + 1);
   auto col = [&](int32_t off, int32_t e) {
     const int32_t k = __ldg(t.lent + off + e);
     return k < 0 ? -1 : k * T + tc;
   };
-  auto put = [&](int64_t base_pos, int& j, double v, int32_t row) {
+  const int32_t cv = col(off_v, n), ct = col(off_th, n);
+  const int64_t posv = cv >= 0 ? (int64_t)__ldg(t.colptr + cv) : 0;
+  const int64_t post = ct >= 0 ? (int64_t)__ldg(t.colptr + ct) : 0;
+  int jv = 0, jt = 0;
+#define MSUM(fld)                                                     \
+  for (uint32_t mm = mask; mm; mm &= mm - 1) acc += shfl(b.fld, base + __ffs(mm) - 1)
+  for (int32_t q = p0; q < p1; ++q) {
+    const unsigned long long code = __ldg(t.bprog + q);
+    const uint32_t mask = (uint32_t)code;
+    const int type = (int)((code >> 32) & 7);
+    const int32_t rent = (int32_t)(code >> 35);
+    double acc = 0.0;
+    switch (type) {
+      case 0: MSUM(hv7); MSUM(hv8); MSUM(pv7); MSUM(pv8); break;
+      case 1: MSUM(ho7); MSUM(ho8); MSUM(po7); MSUM(po8); break;
+      case 2: MSUM(hs7); MSUM(hs8); MSUM(ps7); MSUM(ps8); break;
+      case 3: MSUM(hx7); MSUM(hx8); MSUM(px7); MSUM(px8); break;
+      case 4: MSUM(ht7); MSUM(ht8); MSUM(pt7); MSUM(pt8); MSUM(pt10); break;
+      default: MSUM(hy7); MSUM(hy8); MSUM(py7); MSUM(py8); MSUM(py10); break;
+    }
+    const bool in_v = type < 4;
     if (writer) {
-      if constexpr (STRUCT) rows[base_pos + j] = row; else M[base_pos + j] = v;
+      const int32_t cc = in_v ? cv : ct;
+      if (type == 0 || type == 4) acc += in.dw + in.sx[cc];  // diagonal
+      const int64_t at = in_v ? posv + jv : post + jt;
+      if constexpr (STRUCT) {
+        const int32_t row = col((type == 1 || type == 0) ? off_v : off_th, rent);
+        rows[at] = row;
+      } else {
+        M[at] = acc;
+      }
     }
-    ++j;
-  };
-  auto check = [&](int64_t base_pos, int j, int32_t cc) {
-    if (STRUCT && writer && base_pos + j != __ldg(t.colptr + cc + 1)) atomicOr(bad, 1);
-  };
-
-  // ------------------------------------------------------------------ v(n)
-  const int32_t cv = col(off_v, n);
-  if (cv >= 0) {
-    const int64_t pos = __ldg(t.colptr + cv);
-    int j = 0;
-    double acc = 0.0;
-    SUM_ALL(acc, hv7);
-    SUM_ALL(acc, hv8);
-    SUM_ALL(acc, pv7);
-    SUM_ALL(acc, pv8);
-    if (!STRUCT && writer) acc += in.dw + in.sx[cv];
-    put(pos, j, acc, cv);
-    for (int32_t u0 = q0; u0 < q1;) {  // v(n') for n' > n
-      const int32_t nb = other_nb(u0);
-      int32_t u1 = u0 + 1;
-      while (u1 < q1 && other_nb(u1) == nb) ++u1;
-      const int32_t cr = col(off_v, nb);
-      if (nb > n && cr >= 0) {
-        double a = 0.0;
-        SUM_GRP(a, ho7);
-        SUM_GRP(a, ho8);
-        SUM_GRP(a, po7);
-        SUM_GRP(a, po8);
-        put(pos, j, a, cr);
-      }
-      u0 = u1;
-    }
-    bool self_done = false;  // th(x), x in {n} U neighbours ascending
-    for (int32_t u0 = q0; u0 <= q1;) {
-      int32_t nb = 0x7fffffff, u1 = u0 + 1;
-      if (u0 < q1) {
-        nb = other_nb(u0);
-        while (u1 < q1 && other_nb(u1) == nb) ++u1;
-      }
-      if (!self_done && n < nb) {
-        self_done = true;
-        const int32_t cr = col(off_th, n);
-        if (cr >= 0) {
-          double a = 0.0;
-          SUM_ALL(a, hs7);
-          SUM_ALL(a, hs8);
-          SUM_ALL(a, ps7);
-          SUM_ALL(a, ps8);
-          put(pos, j, a, cr);
-        }
-        continue;
-      }
-      if (u0 >= q1) break;
-      const int32_t cr = col(off_th, nb);
-      if (cr >= 0) {
-        double a = 0.0;
-        SUM_GRP(a, hx7);
-        SUM_GRP(a, hx8);
-        SUM_GRP(a, px7);
-        SUM_GRP(a, px8);
-        put(pos, j, a, cr);
-      }
-      u0 = u1;
-    }
-    check(pos, j, cv);
+    if (in_v) ++jv; else ++jt;
   }
-
-  // ----------------------------------------------------------------- th(n)
-  const int32_t ct = col(off_th, n);
-  if (ct >= 0) {
-    const int64_t pos = __ldg(t.colptr + ct);
-    int j = 0;
-    double acc = 0.0;
-    SUM_ALL(acc, ht7);
-    SUM_ALL(acc, ht8);
-    SUM_ALL(acc, pt7);
-    SUM_ALL(acc, pt8);
-    SUM_ALL(acc, pt10);
-    if (!STRUCT && writer) acc += in.dw + in.sx[ct];
-    put(pos, j, acc, ct);
-    for (int32_t u0 = q0; u0 < q1;) {
-      const int32_t nb = other_nb(u0);
-      int32_t u1 = u0 + 1;
-      while (u1 < q1 && other_nb(u1) == nb) ++u1;
-      const int32_t cr = col(off_th, nb);
-      if (nb > n && cr >= 0) {
-        double a = 0.0;
-        SUM_GRP(a, hy7);
-        SUM_GRP(a, hy8);
-        SUM_GRP(a, py7);
-        SUM_GRP(a, py8);
-        SUM_GRP(a, py10);
-        put(pos, j, a, cr);
-      }
-      u0 = u1;
-    }
-    check(pos, j, ct);
+#undef MSUM
+  if (STRUCT && writer) {
+    if (cv >= 0 && posv + jv != __ldg(t.colptr + cv + 1)) atomicOr(bad, 1);
+    if (ct >= 0 && post + jt != __ldg(t.colptr + ct + 1)) atomicOr(bad, 1);
   }
-#undef SUM_ALL
-#undef SUM_GRP
 }
 
 void launch_fz_bus(const OpfKktTab& t, const int2* items, int64_t n_items, const FIn& in,

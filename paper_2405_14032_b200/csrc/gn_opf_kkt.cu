@@ -637,6 +637,49 @@ bool opf_kkt_prepare(gn_kkt* K) {
     maxdeg = std::max(maxdeg, static_cast<int32_t>(inc[n].size()));
   }
   t.maxdeg = maxdeg;
+  // slot programs of the fused bus-column kernel (gn_opf_fused_bus.cu): rows of
+  // v(n) then th(n) in CSC order, each with the lane mask of its lines
+  std::vector<int32_t> bprog_ptr(N + 1, 0);
+  std::vector<unsigned long long> bprog;
+  if (maxdeg <= 32) {
+    auto slot = [&](uint32_t mask, int type, int32_t ent) {
+      bprog.push_back((static_cast<unsigned long long>(ent) << 35) |
+                      (static_cast<unsigned long long>(type) << 32) | mask);
+    };
+    for (int32_t n = 0; n < N; ++n) {
+      const int32_t deg = static_cast<int32_t>(inc[n].size());
+      const uint32_t all = deg >= 32 ? 0xffffffffu : ((1u << deg) - 1u);
+      // neighbour groups (ascending other bus): lane mask of the group's lines
+      std::vector<std::pair<int32_t, uint32_t>> groups;
+      for (int32_t u = nb_ptr[n]; u < nb_ptr[n + 1]; ++u) {
+        const int32_t e = nb[u], l = e >> 1;
+        const int32_t ob = (e & 1) ? c->line_to[l] : c->line_from[l];
+        if (groups.empty() || groups.back().first != ob) groups.push_back({ob, 0u});
+        groups.back().second |= 1u << nb_inc[u];
+      }
+      const bool vfree_n = !fixed[offs[C_V] + n], tfree_n = !fixed[offs[C_TH] + n];
+      if (vfree_n) {
+        slot(all, 0, n);
+        for (auto& gp : groups)
+          if (gp.first > n && !fixed[offs[C_V] + gp.first]) slot(gp.second, 1, gp.first);
+        bool self = false;
+        for (size_t k = 0; k <= groups.size(); ++k) {
+          const int32_t ob = k < groups.size() ? groups[k].first : 0x7fffffff;
+          if (!self && n < ob) {
+            self = true;
+            if (tfree_n) slot(all, 2, n);
+          }
+          if (k < groups.size() && !fixed[offs[C_TH] + ob]) slot(groups[k].second, 3, ob);
+        }
+      }
+      if (tfree_n) {
+        slot(all, 4, n);
+        for (auto& gp : groups)
+          if (gp.first > n && !fixed[offs[C_TH] + gp.first]) slot(gp.second, 5, gp.first);
+      }
+      bprog_ptr[n + 1] = static_cast<int32_t>(bprog.size());
+    }
+  }
   t.pg0 = d.pg0; t.qg0 = d.qg0; t.p0 = d.p0; t.q0 = d.q0; t.v0 = d.v0; t.th0 = d.th0;
   t.lg = c->lg.p; t.lb = c->lb.p; t.c2 = c->c2.p;
   // flow-row / angle-row positions
@@ -686,12 +729,14 @@ bool opf_kkt_prepare(gn_kkt* K) {
   up(X->ngp, ngp, s); up(X->ngq, ngq, s); up(X->bl_ptr, bl_ptr, s); up(X->bl, bl, s);
   up(X->bg_ptr, bg_ptr, s); up(X->bg, bg, s); up(X->nb_ptr, nb_ptr, s); up(X->nb, nb, s); up(X->nb_inc, nb_inc, s);
   up(X->lnb_ptr, lnb_ptr, s); up(X->lnb, lnb, s);
+  up(X->bprog_ptr, bprog_ptr, s); up(X->bprog, bprog, s);
   t.lent = X->lent.p; t.items = X->items.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
   t.fpos = X->fpos.p; t.apos = X->apos.p; t.lidx_to = X->lidx_to.p; t.lidx_from = X->lidx_from.p;
   t.gbus = X->gbus.p; t.ppos = X->ppos.p; t.qpos = X->qpos.p; t.g_ramp = X->g_ramp.p;
   t.ngp = X->ngp.p; t.ngq = X->ngq.p; t.bl_ptr = X->bl_ptr.p; t.bl = X->bl.p;
   t.bg_ptr = X->bg_ptr.p; t.bg = X->bg.p; t.nb_ptr = X->nb_ptr.p; t.nb = X->nb.p; t.nb_inc = X->nb_inc.p;
   t.lnb_ptr = X->lnb_ptr.p; t.lnb = X->lnb.p;
+  t.bprog_ptr = X->bprog_ptr.p; t.bprog = X->bprog.p;
   t.rowptr = K->A.ptr.p; t.colptr = K->M.ptr.p;
   GN_CK(cudaStreamSynchronize(s));
 

@@ -33,6 +33,8 @@ struct OpfKktTab {
   const double *lg, *lb, *c2;           // line G, B; generator c2
   const int32_t* nb_inc;                // [nb] index of the nb entry in the bus's bl list
   int32_t maxdeg;                       // max incident lines of a bus
+  const int32_t* bprog_ptr;             // [N+1] per-bus slot programs of the v(n)/th(n) columns
+  const unsigned long long* bprog;      // (row entity << 35 | type << 32 | lane mask)
 };
 
 // Inputs of the fused (recompute-from-x) assembly.
@@ -57,6 +59,8 @@ struct OpfKkt {
       ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb, nb_inc;
   DBuf<int8_t> fpos, apos;
   bool fused_ready = false;
+  DBuf<int32_t> bprog_ptr;
+  DBuf<unsigned long long> bprog;
   DBuf<int2> bus_items;  // (bus, first period) per warp of the bus-column kernel
   int64_t n_bus_items = 0;
 };
