@@ -23,147 +23,174 @@
 
 namespace gnb {
 
-constexpr int kBW2 = 4;  // warps per CTA
+constexpr int kBW3 = 4;  // warps per CTA
 
-// terms of one (line, bus side, period)
-struct BusTerms {
-  double hv7, hv8, pv7, pv8;           // (v_n, v_n)
-  double hs7, hs8, ps7, ps8;           // (th_n, v_n)
-  double ht7, ht8, pt7, pt8, pt10;     // (th_n, th_n)
-  double ho7, ho8, po7, po8;           // (v_o, v_n), o > n
-  double hx7, hx8, px7, px8;           // (th_o, v_n)
-  double hy7, hy8, py7, py8, py10;     // (th_o, th_n), o > n
-};
-
-__device__ __forceinline__ double shfl(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
-
+// One warp per (bus n, 32 consecutive periods), lane = period.  The
+// trigonometric state (Cs, Sn, cs, sn) of each incident line is computed once
+// per lane into shared memory; the bus's slot program (host-built: lane mask of
+// the lines of each slot + slot type) then drives the ordered sums.
 template <bool STRUCT>
-__global__ void __launch_bounds__(kBW2 * 32) k_fz_bus2(OpfKktTab t, const int2* __restrict__ items,
-                                                       int64_t n_items, FIn in,
+__global__ void __launch_bounds__(kBW3 * 32) k_fz_bus3(OpfKktTab t, FIn in,
                                                        const double* __restrict__ dv,
                                                        double* __restrict__ M,
                                                        int32_t* __restrict__ rows,
                                                        int32_t* __restrict__ bad) {
-  const int64_t w = ((int64_t)blockIdx.x * kBW2 * 32 + threadIdx.x) >> 5;
-  if (w >= n_items) return;  // warp-uniform
-  const int lane = threadIdx.x & 31;
-  const int2 it = items[w];
-  const int32_t n = it.x, T = t.T;
+  extern __shared__ double bsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * kBW3 + warp;
+  const int64_t n64 = w / t.tchunks;
+  if (n64 >= t.N) return;
+  const int32_t n = (int32_t)n64, T = t.T;
+  const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
+  if (tt >= T) return;  // no warp collectives below
   const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
-  int P = 1;
-  while (P < deg) P <<= 1;
-  const int g = lane / P, i = lane - g * P;
-  const int base = g * P;  // lane of line slot 0 of this period group
-  const int32_t tt = it.y + g;
-  const bool tvalid = (g < 32 / P) && tt < T;
-  const bool writer = tvalid && i == 0;
-  const int32_t tc = tvalid ? tt : 0;  // safe period for idle lanes
+  double* S = bsm + (size_t)warp * t.maxdeg * 4 * 32 + lane;
   const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
 
-  // ---------------------------------------------------------------- terms
-  BusTerms b{};
   if constexpr (!STRUCT) {
-    if (i < deg) {
-      const int32_t e = __ldg(t.bl + b0 + i), l = e >> 1, fr = e & 1;
+    for (int i = 0; i < deg; ++i) {
+      const int32_t l = __ldg(t.bl + b0 + i) >> 1;
       const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
-      const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-      const int64_t lt_ = (int64_t)l * T + tc;
-      const LineState s =
-          line_state(G, B, in.x[t.v0 + (int64_t)f * T + tc], in.x[t.v0 + (int64_t)to * T + tc],
-                     in.x[t.th0 + (int64_t)f * T + tc], in.x[t.th0 + (int64_t)to * T + tc]);
-      const double w7 = in.w[t.flow_p0 + lt_], w8 = in.w[t.flow_q0 + lt_];
-      const double d7 = dv[t.flow_p0 + lt_], d8 = dv[t.flow_q0 + lt_], d10 = dv[t.ang0 + lt_];
-      const int vn = fr ? 1 : 2, vo = fr ? 2 : 1, tn = fr ? 3 : 4, to4 = fr ? 4 : 3;
-      const double p_vn = j_flow_p(s, G, B, vn), p_vo = j_flow_p(s, G, B, vo);
-      const double p_tn = j_flow_p(s, G, B, tn), p_to = j_flow_p(s, G, B, to4);
-      const double q_vn = j_flow_q(s, G, B, vn), q_vo = j_flow_q(s, G, B, vo);
-      const double q_tn = j_flow_q(s, G, B, tn), q_to = j_flow_q(s, G, B, to4);
-      const double an = fr ? 1.0 : -1.0, ao = -an;
-      b.hv7 = h_flow_p(s, G, w7, fr ? 5 : 9);
-      b.hv8 = h_flow_q(s, B, w8, fr ? 5 : 9);
-      b.pv7 = pair_term(d7, p_vn, p_vn);
-      b.pv8 = pair_term(d8, q_vn, q_vn);
-      b.hs7 = h_flow_p(s, G, w7, fr ? 7 : 11);
-      b.hs8 = h_flow_q(s, B, w8, fr ? 7 : 11);
-      b.ps7 = pair_term(d7, p_tn, p_vn);
-      b.ps8 = pair_term(d8, q_tn, q_vn);
-      b.ht7 = h_flow_p(s, G, w7, fr ? 12 : 14);
-      b.ht8 = h_flow_q(s, B, w8, fr ? 12 : 14);
-      b.pt7 = pair_term(d7, p_tn, p_tn);
-      b.pt8 = pair_term(d8, q_tn, q_tn);
-      b.pt10 = pair_term(d10, an, an);
-      b.ho7 = h_flow_p(s, G, w7, 6);
-      b.ho8 = h_flow_q(s, B, w8, 6);
-      b.po7 = pair_term(d7, p_vo, p_vn);
-      b.po8 = pair_term(d8, q_vo, q_vn);
-      b.hx7 = h_flow_p(s, G, w7, fr ? 8 : 10);
-      b.hx8 = h_flow_q(s, B, w8, fr ? 8 : 10);
-      b.px7 = pair_term(d7, p_to, p_vn);
-      b.px8 = pair_term(d8, q_to, q_vn);
-      b.hy7 = h_flow_p(s, G, w7, 13);
-      b.hy8 = h_flow_q(s, B, w8, 13);
-      b.py7 = pair_term(d7, p_to, p_tn);
-      b.py8 = pair_term(d8, q_to, q_tn);
-      b.py10 = pair_term(d10, ao, an);
+      const LineState s = line_state(__ldg(t.lg + l), __ldg(t.lb + l),
+                                     in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
+                                     in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
+      S[(i * 4 + 0) * 32] = s.Cs;
+      S[(i * 4 + 1) * 32] = s.Sn;
+      S[(i * 4 + 2) * 32] = s.cs;
+      S[(i * 4 + 3) * 32] = s.sn;
     }
   }
-  // Per-bus slot program (built on the host, opf_kkt_prepare): each slot is
-  // (lane mask of its lines, type, row entity); types 0-3 belong to v(n),
-  // 4-5 to th(n).  Mask bits ascend with l, so the shuffle order is the
-  // reference's record order.
-  const int32_t p0 = __ldg(t.bprog_ptr + n), p1 = __ldg(t.bprog_ptr + n + 1);
+  // line k of the bus: state + the per-row inputs of this period
+  struct LV {
+    LineState s;
+    double G, B;
+    int32_t l, fr;
+  };
+  auto lv = [&](int k) {
+    LV r;
+    const int32_t e = __ldg(t.bl + b0 + k);
+    r.l = e >> 1;
+    r.fr = e & 1;
+    r.G = __ldg(t.lg + r.l);
+    r.B = __ldg(t.lb + r.l);
+    const int32_t f = __ldg(t.lf + r.l), to = __ldg(t.lt + r.l);
+    r.s.vf = in.x[t.v0 + (int64_t)f * T + tt];
+    r.s.vt = in.x[t.v0 + (int64_t)to * T + tt];
+    r.s.vfvt = r.s.vf * r.s.vt;
+    r.s.Cs = S[(k * 4 + 0) * 32];
+    r.s.Sn = S[(k * 4 + 1) * 32];
+    r.s.cs = S[(k * 4 + 2) * 32];
+    r.s.sn = S[(k * 4 + 3) * 32];
+    return r;
+  };
+  auto rowp = [&](int32_t base0, int32_t l) { return base0 + (int64_t)l * T + tt; };
+  auto w7 = [&](const LV& r) { return in.w[rowp(t.flow_p0, r.l)]; };
+  auto w8 = [&](const LV& r) { return in.w[rowp(t.flow_q0, r.l)]; };
+  auto d7 = [&](const LV& r) { return dv[rowp(t.flow_p0, r.l)]; };
+  auto d8 = [&](const LV& r) { return dv[rowp(t.flow_q0, r.l)]; };
+  auto d10 = [&](const LV& r) { return dv[rowp(t.ang0, r.l)]; };
+  // fields of this bus's side (n = from -> v_f / th_f)
+  auto JP = [&](const LV& r, bool other, bool theta) {
+    const int f = theta ? ((r.fr ^ other) ? 3 : 4) : ((r.fr ^ other) ? 1 : 2);
+    return j_flow_p(r.s, r.G, r.B, f);
+  };
+  auto JQ = [&](const LV& r, bool other, bool theta) {
+    const int f = theta ? ((r.fr ^ other) ? 3 : 4) : ((r.fr ^ other) ? 1 : 2);
+    return j_flow_q(r.s, r.G, r.B, f);
+  };
+
   auto col = [&](int32_t off, int32_t e) {
     const int32_t k = __ldg(t.lent + off + e);
-    return k < 0 ? -1 : k * T + tc;
+    return k < 0 ? -1 : k * T + tt;
   };
   const int32_t cv = col(off_v, n), ct = col(off_th, n);
   const int64_t posv = cv >= 0 ? (int64_t)__ldg(t.colptr + cv) : 0;
   const int64_t post = ct >= 0 ? (int64_t)__ldg(t.colptr + ct) : 0;
   int jv = 0, jt = 0;
-#define MSUM(fld)                                                     \
-  for (uint32_t mm = mask; mm; mm &= mm - 1) acc += shfl(b.fld, base + __ffs(mm) - 1)
+  const int32_t p0 = __ldg(t.bprog_ptr + n), p1 = __ldg(t.bprog_ptr + n + 1);
+#define PASS(expr)                                 \
+  for (uint32_t mm = mask; mm; mm &= mm - 1) {     \
+    const LV r = lv(__ffs(mm) - 1);                \
+    acc += (expr);                                 \
+  }
   for (int32_t q = p0; q < p1; ++q) {
     const unsigned long long code = __ldg(t.bprog + q);
     const uint32_t mask = (uint32_t)code;
     const int type = (int)((code >> 32) & 7);
     const int32_t rent = (int32_t)(code >> 35);
     double acc = 0.0;
-    switch (type) {
-      case 0: MSUM(hv7); MSUM(hv8); MSUM(pv7); MSUM(pv8); break;
-      case 1: MSUM(ho7); MSUM(ho8); MSUM(po7); MSUM(po8); break;
-      case 2: MSUM(hs7); MSUM(hs8); MSUM(ps7); MSUM(ps8); break;
-      case 3: MSUM(hx7); MSUM(hx8); MSUM(px7); MSUM(px8); break;
-      case 4: MSUM(ht7); MSUM(ht8); MSUM(pt7); MSUM(pt8); MSUM(pt10); break;
-      default: MSUM(hy7); MSUM(hy8); MSUM(py7); MSUM(py8); MSUM(py10); break;
-    }
-    const bool in_v = type < 4;
-    if (writer) {
-      const int32_t cc = in_v ? cv : ct;
-      if (type == 0 || type == 4) acc += in.dw + in.sx[cc];  // diagonal
-      const int64_t at = in_v ? posv + jv : post + jt;
-      if constexpr (STRUCT) {
-        const int32_t row = col((type == 1 || type == 0) ? off_v : off_th, rent);
-        rows[at] = row;
-      } else {
-        M[at] = acc;
+    if constexpr (!STRUCT) {
+      switch (type) {
+        case 0:  // (v_n, v_n)
+          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 5 : 9));
+          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 5 : 9));
+          PASS(pair_term(d7(r), JP(r, false, false), JP(r, false, false)));
+          PASS(pair_term(d8(r), JQ(r, false, false), JQ(r, false, false)));
+          acc += in.dw + in.sx[cv];
+          break;
+        case 1:  // (v_o, v_n), o > n
+          PASS(h_flow_p(r.s, r.G, w7(r), 6));
+          PASS(h_flow_q(r.s, r.B, w8(r), 6));
+          PASS(pair_term(d7(r), JP(r, true, false), JP(r, false, false)));
+          PASS(pair_term(d8(r), JQ(r, true, false), JQ(r, false, false)));
+          break;
+        case 2:  // (th_n, v_n)
+          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 7 : 11));
+          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 7 : 11));
+          PASS(pair_term(d7(r), JP(r, false, true), JP(r, false, false)));
+          PASS(pair_term(d8(r), JQ(r, false, true), JQ(r, false, false)));
+          break;
+        case 3:  // (th_o, v_n)
+          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 8 : 10));
+          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 8 : 10));
+          PASS(pair_term(d7(r), JP(r, true, true), JP(r, false, false)));
+          PASS(pair_term(d8(r), JQ(r, true, true), JQ(r, false, false)));
+          break;
+        case 4:  // (th_n, th_n)
+          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 12 : 14));
+          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 12 : 14));
+          PASS(pair_term(d7(r), JP(r, false, true), JP(r, false, true)));
+          PASS(pair_term(d8(r), JQ(r, false, true), JQ(r, false, true)));
+          PASS(pair_term(d10(r), r.fr ? 1.0 : -1.0, r.fr ? 1.0 : -1.0));
+          acc += in.dw + in.sx[ct];
+          break;
+        default:  // (th_o, th_n), o > n
+          PASS(h_flow_p(r.s, r.G, w7(r), 13));
+          PASS(h_flow_q(r.s, r.B, w8(r), 13));
+          PASS(pair_term(d7(r), JP(r, true, true), JP(r, false, true)));
+          PASS(pair_term(d8(r), JQ(r, true, true), JQ(r, false, true)));
+          PASS(pair_term(d10(r), r.fr ? -1.0 : 1.0, r.fr ? 1.0 : -1.0));
+          break;
       }
     }
+    const bool in_v = type < 4;
+    const int64_t at = in_v ? posv + jv : post + jt;
+    if constexpr (STRUCT) rows[at] = col((type == 0 || type == 1) ? off_v : off_th, rent);
+    else M[at] = acc;
     if (in_v) ++jv; else ++jt;
   }
-#undef MSUM
-  if (STRUCT && writer) {
+#undef PASS
+  if (STRUCT) {
     if (cv >= 0 && posv + jv != __ldg(t.colptr + cv + 1)) atomicOr(bad, 1);
     if (ct >= 0 && post + jt != __ldg(t.colptr + ct + 1)) atomicOr(bad, 1);
   }
 }
 
-void launch_fz_bus(const OpfKktTab& t, const int2* items, int64_t n_items, const FIn& in,
-                   const double* dv, double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((n_items + kBW2 - 1) / kBW2);
+void launch_fz_bus(const OpfKktTab& t, const int2*, int64_t, const FIn& in, const double* dv,
+                   double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
+  const int64_t warps = (int64_t)t.N * t.tchunks;
+  const unsigned blocks = (unsigned)((warps + kBW3 - 1) / kBW3);
+  const size_t smem = (size_t)kBW3 * (t.maxdeg > 0 ? t.maxdeg : 1) * 4 * 32 * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    GN_CK(cudaFuncSetAttribute(k_fz_bus3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
   if (rows)
-    k_fz_bus2<true><<<blocks, kBW2 * 32, 0, s>>>(t, items, n_items, in, dv, M, rows, bad);
+    k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, in, dv, M, rows, bad);
   else
-    k_fz_bus2<false><<<blocks, kBW2 * 32, 0, s>>>(t, items, n_items, in, dv, M, rows, bad);
+    k_fz_bus3<false><<<blocks, kBW3 * 32, smem, s>>>(t, in, dv, M, rows, bad);
   count_launch();
 }
 
