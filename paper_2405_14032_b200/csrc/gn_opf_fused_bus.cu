@@ -30,7 +30,7 @@ constexpr int kBW3 = 4;  // warps per CTA
 // per lane into shared memory; the bus's slot program (host-built: lane mask of
 // the lines of each slot + slot type) then drives the ordered sums.
 template <bool STRUCT>
-__global__ void __launch_bounds__(kBW3 * 32) k_fz_bus3(OpfKktTab t, FIn in,
+__global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, FIn in,
                                                        const double* __restrict__ dv,
                                                        double* __restrict__ M,
                                                        int32_t* __restrict__ rows,
@@ -44,20 +44,38 @@ __global__ void __launch_bounds__(kBW3 * 32) k_fz_bus3(OpfKktTab t, FIn in,
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
   if (tt >= T) return;  // no warp collectives below
   const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
-  double* S = bsm + (size_t)warp * t.maxdeg * 4 * 32 + lane;
+  double* S = bsm + (size_t)warp * t.maxdeg * 6 * 32 + lane;
+  // per-line warp-uniform data, filled by lanes 0..deg-1 in parallel
+  struct LU {
+    double G, B;
+    int32_t l, fr;
+  };
+  LU* U = reinterpret_cast<LU*>(bsm + (size_t)kBW3 * t.maxdeg * 6 * 32) + warp * t.maxdeg;
+  if (lane < deg) {
+    const int32_t e = __ldg(t.bl + b0 + lane);
+    LU u;
+    u.l = e >> 1;
+    u.fr = e & 1;
+    u.G = __ldg(t.lg + u.l);
+    u.B = __ldg(t.lb + u.l);
+    U[lane] = u;
+  }
+  __syncwarp();
   const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
 
   if constexpr (!STRUCT) {
     for (int i = 0; i < deg; ++i) {
-      const int32_t l = __ldg(t.bl + b0 + i) >> 1;
-      const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
-      const LineState s = line_state(__ldg(t.lg + l), __ldg(t.lb + l),
+      const LU u = U[i];
+      const int32_t f = __ldg(t.lf + u.l), to = __ldg(t.lt + u.l);
+      const LineState s = line_state(u.G, u.B,
                                      in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
                                      in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
-      S[(i * 4 + 0) * 32] = s.Cs;
-      S[(i * 4 + 1) * 32] = s.Sn;
-      S[(i * 4 + 2) * 32] = s.cs;
-      S[(i * 4 + 3) * 32] = s.sn;
+      S[(i * 6 + 0) * 32] = s.Cs;
+      S[(i * 6 + 1) * 32] = s.Sn;
+      S[(i * 6 + 2) * 32] = s.cs;
+      S[(i * 6 + 3) * 32] = s.sn;
+      S[(i * 6 + 4) * 32] = s.vf;
+      S[(i * 6 + 5) * 32] = s.vt;
     }
   }
   // line k of the bus: state + the per-row inputs of this period
@@ -68,19 +86,18 @@ __global__ void __launch_bounds__(kBW3 * 32) k_fz_bus3(OpfKktTab t, FIn in,
   };
   auto lv = [&](int k) {
     LV r;
-    const int32_t e = __ldg(t.bl + b0 + k);
-    r.l = e >> 1;
-    r.fr = e & 1;
-    r.G = __ldg(t.lg + r.l);
-    r.B = __ldg(t.lb + r.l);
-    const int32_t f = __ldg(t.lf + r.l), to = __ldg(t.lt + r.l);
-    r.s.vf = in.x[t.v0 + (int64_t)f * T + tt];
-    r.s.vt = in.x[t.v0 + (int64_t)to * T + tt];
+    const LU u = U[k];
+    r.l = u.l;
+    r.fr = u.fr;
+    r.G = u.G;
+    r.B = u.B;
+    r.s.Cs = S[(k * 6 + 0) * 32];
+    r.s.Sn = S[(k * 6 + 1) * 32];
+    r.s.cs = S[(k * 6 + 2) * 32];
+    r.s.sn = S[(k * 6 + 3) * 32];
+    r.s.vf = S[(k * 6 + 4) * 32];
+    r.s.vt = S[(k * 6 + 5) * 32];
     r.s.vfvt = r.s.vf * r.s.vt;
-    r.s.Cs = S[(k * 4 + 0) * 32];
-    r.s.Sn = S[(k * 4 + 1) * 32];
-    r.s.cs = S[(k * 4 + 2) * 32];
-    r.s.sn = S[(k * 4 + 3) * 32];
     return r;
   };
   auto rowp = [&](int32_t base0, int32_t l) { return base0 + (int64_t)l * T + tt; };
@@ -180,7 +197,8 @@ void launch_fz_bus(const OpfKktTab& t, const int2*, int64_t, const FIn& in, cons
                    double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
   const int64_t warps = (int64_t)t.N * t.tchunks;
   const unsigned blocks = (unsigned)((warps + kBW3 - 1) / kBW3);
-  const size_t smem = (size_t)kBW3 * (t.maxdeg > 0 ? t.maxdeg : 1) * 4 * 32 * sizeof(double);
+  const int md = t.maxdeg > 0 ? t.maxdeg : 1;
+  const size_t smem = (size_t)kBW3 * md * (6 * 32 * sizeof(double) + 24);
   static bool attr = false;
   if (!attr) {
     GN_CK(cudaFuncSetAttribute(k_fz_bus3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
