@@ -305,8 +305,8 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
                          int32_t* bad) {
   const OpfKktTab& t = K->opf->t;
   cudaStream_t s = K->stream;
-  if (K->opf->n_bus_items > 0)
-    launch_fz_bus(t, K->opf->bus_items.p, K->opf->n_bus_items, in, dv, M, rows, bad, s);
+  launch_fz_bus(t, K->opf->bus_small.p, K->opf->n_bus_small, kSmallDeg, in, dv, M, rows, bad, s);
+  launch_fz_bus(t, K->opf->bus_large.p, K->opf->n_bus_large, t.maxdeg, in, dv, M, rows, bad, s);
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
     k_fz_line<STRUCT><<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
@@ -349,20 +349,19 @@ bool opf_fused_verify(gn_kkt* K) {
   const OpfKktTab& t = K->opf->t;
   if (t.maxdeg > 32) return false;  // bus-column kernel holds one line per lane
   K->dvals.alloc(static_cast<size_t>(K->m) + 1);
-  {  // work list of the bus-column kernel: (bus, first period) per warp
+  {  // bus lists of the bus-column kernel, by degree class (shared-memory footprint)
     std::vector<int32_t> bp(t.N + 1);
     GN_CK(cudaMemcpyAsync(bp.data(), t.bl_ptr, sizeof(int32_t) * (t.N + 1), cudaMemcpyDeviceToHost,
                           K->stream));
     GN_CK(cudaStreamSynchronize(K->stream));
-    std::vector<int2> items;
-    for (int32_t n = 0; n < t.N; ++n) {
-      int P = 1;
-      while (P < bp[n + 1] - bp[n]) P <<= 1;
-      const int per = 32 / P;
-      for (int32_t t0 = 0; t0 < t.T; t0 += per) items.push_back(make_int2(n, t0));
-    }
-    K->opf->bus_items.upload(items.data(), items.size(), K->stream);
-    K->opf->n_bus_items = static_cast<int64_t>(items.size());
+    std::vector<int32_t> small, large;
+    for (int32_t n = 0; n < t.N; ++n) (bp[n + 1] - bp[n] <= kSmallDeg ? small : large).push_back(n);
+    K->opf->bus_small.upload(small.data(), small.size(), K->stream);
+    K->opf->bus_large.upload(large.data(), large.size(), K->stream);
+    if (small.empty()) K->opf->bus_small.alloc(1);
+    if (large.empty()) K->opf->bus_large.alloc(1);
+    K->opf->n_bus_small = static_cast<int32_t>(small.size());
+    K->opf->n_bus_large = static_cast<int32_t>(large.size());
   }
   cudaStream_t s = K->stream;
   DBuf<int32_t> rows, bad, diff;

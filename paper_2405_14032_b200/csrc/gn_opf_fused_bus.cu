@@ -30,7 +30,8 @@ constexpr int kBW3 = 4;  // warps per CTA
 // per lane into shared memory; the bus's slot program (host-built: lane mask of
 // the lines of each slot + slot type) then drives the ordered sums.
 template <bool STRUCT>
-__global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, FIn in,
+__global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int32_t* __restrict__ buses,
+                                                       int32_t n_buses, int32_t maxdeg, FIn in,
                                                        const double* __restrict__ dv,
                                                        double* __restrict__ M,
                                                        int32_t* __restrict__ rows,
@@ -39,18 +40,17 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, FIn in,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = (int64_t)blockIdx.x * kBW3 + warp;
   const int64_t n64 = w / t.tchunks;
-  if (n64 >= t.N) return;
-  const int32_t n = (int32_t)n64, T = t.T;
+  if (n64 >= n_buses) return;  // warp-uniform
+  const int32_t n = __ldg(buses + n64), T = t.T;
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
-  if (tt >= T) return;  // no warp collectives below
   const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
-  double* S = bsm + (size_t)warp * t.maxdeg * 6 * 32 + lane;
+  double* S = bsm + (size_t)warp * maxdeg * 6 * 32 + lane;
   // per-line warp-uniform data, filled by lanes 0..deg-1 in parallel
   struct LU {
     double G, B;
     int32_t l, fr;
   };
-  LU* U = reinterpret_cast<LU*>(bsm + (size_t)kBW3 * t.maxdeg * 6 * 32) + warp * t.maxdeg;
+  LU* U = reinterpret_cast<LU*>(bsm + (size_t)kBW3 * maxdeg * 6 * 32) + warp * maxdeg;
   if (lane < deg) {
     const int32_t e = __ldg(t.bl + b0 + lane);
     LU u;
@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, FIn in,
     U[lane] = u;
   }
   __syncwarp();
+  if (tt >= T) return;  // no warp collectives below
   const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
 
   if constexpr (!STRUCT) {
@@ -193,11 +194,13 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, FIn in,
   }
 }
 
-void launch_fz_bus(const OpfKktTab& t, const int2*, int64_t, const FIn& in, const double* dv,
-                   double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
-  const int64_t warps = (int64_t)t.N * t.tchunks;
+void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
+                   const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
+                   cudaStream_t s) {
+  if (n_buses <= 0) return;
+  const int64_t warps = (int64_t)n_buses * t.tchunks;
   const unsigned blocks = (unsigned)((warps + kBW3 - 1) / kBW3);
-  const int md = t.maxdeg > 0 ? t.maxdeg : 1;
+  const int md = maxdeg > 0 ? maxdeg : 1;
   const size_t smem = (size_t)kBW3 * md * (6 * 32 * sizeof(double) + 24);
   static bool attr = false;
   if (!attr) {
@@ -206,9 +209,9 @@ void launch_fz_bus(const OpfKktTab& t, const int2*, int64_t, const FIn& in, cons
     attr = true;
   }
   if (rows)
-    k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, in, dv, M, rows, bad);
+    k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else
-    k_fz_bus3<false><<<blocks, kBW3 * 32, smem, s>>>(t, in, dv, M, rows, bad);
+    k_fz_bus3<false><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   count_launch();
 }
 
