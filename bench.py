@@ -19,6 +19,7 @@ drop-in.  `--impl reference` times the reference's own CPU implementation
 from __future__ import annotations
 
 import argparse
+import ctypes as C
 import json
 import os
 import subprocess
@@ -56,44 +57,54 @@ def inputs(nlp_bounds, m, n_free, seed_shift=0):
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clocks and throttle reasons sampled every ~2 ms during the timed region
+    (NVML; B200_PROFILING.md clocks line)."""
+
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index: int):
-        self.proc = None
+        import threading
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[index]) if vis and vis.split(",")[index].isdigit() else index
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
         except Exception:
-            self.proc = None
+            self.nv = None
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, attr in self.REASONS.items():
+                    if r & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def stop(self):
-        if not self.proc:
+        if self.nv is None:
             return None
-        self.proc.terminate()
-        out, _ = self.proc.communicate(timeout=10)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
-            f = [c.strip() for c in line.split(",")]
-            if len(f) < 7:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx.append(float(f[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[3:7]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
+        self._stop.set()
+        self.t.join(timeout=5)
+        if not self.samples:
             return None
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)),
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
 # ------------------------------------------------------------------ workload
@@ -133,6 +144,70 @@ def stage_bytes(s, kkt, net, periods, fused=False):
         "set_jacobian": 8 * (s.jac_nnz_lifted + kkt.a_nnz),
         "assemble": 8 * (s.hess_nnz_lifted + kkt.a_nnz + s.n_free + m + kkt.m_nnz),
     }
+
+
+def kernel_bytes(s, kkt, nlp, net, T):
+    """Algorithmic bytes per launch of each library kernel: the contract outputs
+    it writes once plus the inputs it needs read once (index maps excluded)."""
+    N, L, G, D = net.n_bus, net.n_line, net.n_gen, net.n_load
+    LTh, GR = s.n_thermal, s.n_ramp_gens
+    R = max(T - 1, 0)
+    m, annz = s.n_cons, kkt.a_nnz
+    # M slots per column block, from the lifted structure
+    _, _, colptr, _ = kkt.structure()
+    lens = np.diff(colptr.astype(np.int64))
+    f2f = nlp.lifted_structure()["free_to_full"]
+    bounds = np.cumsum([0, G * T, G * T, L * T, L * T, N * T, N * T])
+    blk = np.searchsorted(bounds, f2f, side="right") - 1  # 0 pg 1 qg 2 p 3 q 4 v 5 th
+    deg = np.bincount(np.concatenate([net.line_from, net.line_to]), minlength=N)
+    small = deg <= 4
+    ent = np.where(blk >= 4, (f2f - bounds[np.minimum(blk, 5)]) // T, -1)
+    vth = blk >= 4
+    m_small = int(lens[vth & small[np.maximum(ent, 0)]].sum())
+    m_large = int(lens[vth & ~small[np.maximum(ent, 0)]].sum())
+    m_pq = int(lens[(blk == 2) | (blk == 3)].sum())
+    m_g = int(lens[blk <= 1].sum())
+    fs = float(deg[small].sum()) / max(2 * L, 1)
+    nsm, nlg = int(small.sum()) * T, int((~small).sum()) * T
+    b = {
+        "k_gen<F>": G * T, "k_gen<GRAD>": 2 * G * T,
+        "k_bus<G>": 2 * N * T + 2 * L * T + 2 * G * T + 2 * D * T,
+        "k_line<G>": 5 * L * T + 2 * N * T, "k_thermal<G>": 3 * LTh * T,
+        "k_ramp<G>": GR * R + G * T,
+        "k_line<J>": 16 * L * T + 2 * N * T, "k_gen<J>": 2 * G * T,
+        "k_thermal<J>": 4 * LTh * T, "k_ramp<J>": 2 * GR * R,
+        "k_line<H>": 39 * L * T + 2 * N * T, "k_gen<H>": 4 * G * T,
+        "k_thermal<H>": 6 * LTh * T, "k_ramp<H>": 3 * GR * R,
+        "k_opf_set_jac_fused": annz - 2 * LTh * T + 2 * N * T,
+        "k_opf_set_jac_thermal": 4 * LTh * T,
+        "k_fz_dvec": 2 * m,
+        "k_fz_bus3<small>": m_small + 4 * nsm + fs * 5 * L * T,
+        "k_fz_bus3<large>": m_large + 4 * nlg + (1 - fs) * 5 * L * T,
+        "k_fz_line": m_pq + 2 * L * T + 2 * N * T + 2 * N * T + 2 * L * T + 2 * LTh * T + 2 * L * T,
+        "k_fz_gen": m_g + 2 * G * T + GR * R + 2 * G * T,
+        "k_opf_set_jac": 2 * annz, "k_set_jac_generic": 2 * annz,
+        "k_opf_assemble": s.hess_nnz_lifted + annz + s.n_free + m + kkt.m_nnz,
+        "k_assemble_generic": s.hess_nnz_lifted + annz + s.n_free + m + kkt.m_nnz,
+    }
+    return {k: 8.0 * v for k, v in b.items()}
+
+
+def profile_kernels(L, step, steps, stream):
+    """Per-kernel CUDA-event times (library KTimer) over `steps` extra steps."""
+    import torch
+    L.gn_profile_reset()
+    L.gn_profile_enable(1)
+    for _ in range(steps):
+        step()
+    torch.cuda.synchronize()
+    L.gn_profile_enable(0)
+    out = {}
+    for i in range(L.gn_profile_count()):
+        ms, n = C.c_double(), C.c_int64()
+        name = L.gn_profile_get(i, C.byref(ms), C.byref(n)).decode()
+        out[name] = (ms.value / max(n.value, 1), n.value)
+    L.gn_profile_reset()
+    return out
 
 
 def run_ours(args, rank, world, local_rank, dist):
@@ -232,11 +307,17 @@ def run_ours(args, rank, world, local_rank, dist):
     nnz_step = s.jac_nnz + s.hess_nnz + kkt.m_nnz
     value = nnz_step * world / (ms * 1e-3)
 
-    # roofline: dominant call (one kernel: the KKT assembly / else the largest stage)
+    # roofline of the dominant kernel: per-kernel CUDA events on the launch stream
+    # (library KTimer), measured over extra steps after the timed region
     peak, peak_kind = peaks()
-    sb = stage_bytes(s, kkt, net, args.periods, fused)
-    dom = max(per_stage, key=per_stage.get)
-    achieved = sb[dom] / (per_stage[dom] * 1e-3) / 1e9
+    kprof = profile_kernels(L, step, max(3, min(args.steps, 10)), stream)
+    kb = kernel_bytes(s, kkt, nlp, net, args.periods)
+    dom = max(kprof, key=lambda k: kprof[k][0] * kprof[k][1])
+    dom_ms = kprof[dom][0]
+    achieved = kb.get(dom, 0.0) / (dom_ms * 1e-3) / 1e9
+    kernels = {k: {"ms": v[0], "launches_per_step": v[1] / max(3, min(args.steps, 10)),
+                   "gbs": kb.get(k, 0.0) / (v[0] * 1e-3) / 1e9 if k in kb else None}
+               for k, v in sorted(kprof.items(), key=lambda kv: -kv[1][0] * kv[1][1])}
     unit_bytes = alg_bytes(s, kkt)
     unit_gbs = unit_bytes / (ms * 1e-3) / 1e9
 
@@ -305,7 +386,9 @@ def run_ours(args, rank, world, local_rank, dist):
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "peak_source": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                     "alg_bytes_per_launch": sb[dom], "traffic": None},
+                     "alg_bytes_per_launch": kb.get(dom), "ms_per_launch": dom_ms,
+                     "traffic": None},
+        "kernels": kernels,
         "unit_roofline": {"alg_bytes": unit_bytes, "achieved": unit_gbs, "peak": peak,
                           "frac": unit_gbs / peak, "unit": "GB/s"},
         "pipeline": ("fused: set_jacobian/assemble recompute J/H terms from x "
@@ -319,7 +402,8 @@ def run_ours(args, rank, world, local_rank, dist):
     }
     if args.traffic_json and Path(args.traffic_json).exists():
         tr = json.loads(Path(args.traffic_json).read_text())
-        line["roofline"]["traffic"] = tr.get(dom)
+        key = dom.split("<")[0] if dom not in tr else dom
+        line["roofline"]["traffic"] = tr.get(dom, tr.get(key))
     if rank == 0:
         print(json.dumps(line), flush=True)
 

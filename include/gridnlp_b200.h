@@ -86,6 +86,13 @@ typedef struct gn_kkt gn_kkt;
 int gn_abi_version(void);
 /* Number of CUDA kernels this library has launched (process-wide counter). */
 int64_t gn_launch_count(void);
+/* Per-kernel CUDA-event timing of this library's launches (bench.py roofline):
+ * enable, run, then gn_profile_count() synchronises and returns the number of
+ * kernels; gn_profile_get(i) returns its name, total ms and launch count. */
+void gn_profile_enable(int on);
+void gn_profile_reset(void);
+int gn_profile_count(void);
+const char* gn_profile_get(int i, double* total_ms, int64_t* launches);
 /* Reports whether a usable CUDA device is present (count into *n_devices). */
 int gn_device_count(int32_t* n_devices);
 
@@ -105,6 +112,23 @@ int gn_load_profile(int32_t n_load, int32_t periods, double resolution_minutes,
  * network.hpp:166-171).  Lines with from == to are rejected (GN_ERR_UNSUPPORTED). */
 int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale,
                   int32_t device, gn_ctx** out, gn_error* err);
+/* One period shard of a periods_total-period horizon: the
+ * periods [first_period, first_period + periods), scale = that slice of the
+ * demand table.  Layout = the reference layout over the shard's periods, plus
+ * ghost generator set-points after the regular blocks: pg(first_period - 1)
+ * (fixed; the caller writes the previous rank's values into x) and
+ * pg(first_period + periods) (free; the rows using it are owned by the next
+ * rank, whose sigma_s values the caller writes into the ghost rows).  The
+ * ramp row of step t belongs to the rank owning period t.  With the halo
+ * filled, every owned row, record and lifted M column equals the global
+ * problem's, bit for bit (tests/test_shard.py). */
+int gn_ctx_create_shard(const gn_network* net, int32_t periods_total, int32_t first_period,
+                        int32_t periods, const double* scale, int32_t device, gn_ctx** out,
+                        gn_error* err);
+/* info = [t0, T_total, prev, next, n_ramp_gens, n_base, ghost_prev0, ghost_next0,
+ *         ramp_row0, ramp_rows_per_gen, first_step, owned_lifted_columns (-1 before
+ *         gn_lifted_create)]; ramp_gens[n_ramp_gens] (may be NULL). */
+int gn_ctx_shard_info(gn_ctx* ctx, int64_t* info, int32_t* ramp_gens);
 int gn_ctx_destroy(gn_ctx* ctx);
 /* Use a caller-owned cudaStream_t (as void*) for every launch of this context. */
 int gn_ctx_set_stream(gn_ctx* ctx, void* cuda_stream);

@@ -54,10 +54,17 @@ _SIGS = {
     "gn_abi_version": (C.c_int, []),
     "gn_launch_count": (C.c_int64, []),
     "gn_device_count": (C.c_int, [i32p]),
+    "gn_profile_enable": (None, [C.c_int]),
+    "gn_profile_reset": (None, []),
+    "gn_profile_count": (C.c_int, []),
+    "gn_profile_get": (C.c_char_p, [C.c_int, f64p, i64p]),
     "gn_load_profile": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_uint64, C.c_double,
                                   C.c_double, f64p, C.POINTER(GnError)]),
     "gn_ctx_create": (C.c_int, [C.POINTER(GnNetwork), C.c_int32, f64p, C.c_int32,
                                 C.POINTER(vp), C.POINTER(GnError)]),
+    "gn_ctx_create_shard": (C.c_int, [C.POINTER(GnNetwork), C.c_int32, C.c_int32, C.c_int32, f64p,
+                                      C.c_int32, C.POINTER(vp), C.POINTER(GnError)]),
+    "gn_ctx_shard_info": (C.c_int, [vp, i64p, i32p]),
     "gn_ctx_destroy": (C.c_int, [vp]),
     "gn_ctx_set_stream": (C.c_int, [vp, vp]),
     "gn_ctx_get_stream": (C.c_int, [vp, C.POINTER(vp)]),

@@ -85,6 +85,13 @@ void copy_i32(int32_t* dst, const int32_t* src, int64_t n, int mem, cudaStream_t
 extern "C" {
 
 int gn_abi_version(void) { return GN_ABI_VERSION; }
+
+void gn_profile_enable(int on) { gnb::profile_enable(on != 0); }
+void gn_profile_reset(void) { gnb::profile_reset(); }
+int gn_profile_count(void) { return gnb::profile_count(); }
+const char* gn_profile_get(int i, double* total_ms, int64_t* launches) {
+  return gnb::profile_get(i, total_ms, launches);
+}
 int64_t gn_launch_count(void) { return gnb::launch_count(); }
 
 int gn_device_count(int32_t* n_devices) {
@@ -124,14 +131,17 @@ int gn_load_profile(int32_t n_load, int32_t periods, double resolution_minutes, 
 }
 
 // ----------------------------------------------------------------- context
-int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale, int32_t device,
-                  gn_ctx** out, gn_error* err) {
+static int ctx_create(const gn_network* net, int32_t periods_total, int32_t first_period,
+                      int32_t periods, const double* scale, int32_t device, gn_ctx** out,
+                      gn_error* err) {
   if (!net || !out) return fail(err, GN_ERR_INVALID, "null argument");
   *out = nullptr;
   gn_ctx* c = nullptr;
   API_TRY
   const int32_t N = net->n_bus, L = net->n_line, G = net->n_gen, D = net->n_load;
   const int32_t T = periods;
+  if (first_period < 0 || periods < 1 || first_period + periods > periods_total)
+    throw Error(GN_ERR_INVALID, "shard: periods outside the horizon");
   if (N < 0 || L < 0 || G < 0 || D < 0) throw Error(GN_ERR_INVALID, "negative element count");
   if (net->reference_bus < 0 || net->reference_bus >= N)
     throw Error(GN_ERR_INVALID, "opf: network has no reference bus");
@@ -187,7 +197,7 @@ int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale, i
   const double inf = std::numeric_limits<double>::infinity();
   for (int32_t l = 0; l < L; ++l)
     if (c->line_smax[l] < inf) c->thermal_lines.push_back(l);
-  if (T >= 2)
+  if (periods_total >= 2)  // ramp rows exist when the whole horizon has >= 2 periods
     for (int32_t g = 0; g < G; ++g)
       if (c->gen_ramp[g] < inf) {
         if (-c->gen_ramp[g] > c->gen_ramp[g])
@@ -196,7 +206,7 @@ int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale, i
       }
   const int32_t LT = static_cast<int32_t>(c->thermal_lines.size());
   const int32_t GR = static_cast<int32_t>(c->ramp_gens.size());
-  c->d = gnb::make_dims(T, N, L, G, D, LT, GR, net->reference_bus);
+  c->d = gnb::make_dims(T, N, L, G, D, LT, GR, net->reference_bus, first_period, periods_total);
 
   GN_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
@@ -267,6 +277,28 @@ int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale, i
     delete c;
     return fail(err, GN_ERR_INVALID, e.what());
   }
+}
+
+int gn_ctx_create(const gn_network* net, int32_t periods, const double* scale, int32_t device,
+                  gn_ctx** out, gn_error* err) {
+  return ctx_create(net, periods, 0, periods, scale, device, out, err);
+}
+
+int gn_ctx_create_shard(const gn_network* net, int32_t periods_total, int32_t first_period,
+                        int32_t periods, const double* scale, int32_t device, gn_ctx** out,
+                        gn_error* err) {
+  return ctx_create(net, periods_total, first_period, periods, scale, device, out, err);
+}
+
+int gn_ctx_shard_info(gn_ctx* c, int64_t* info, int32_t* ramp_gens) {
+  if (!c || !info) return GN_ERR_INVALID;
+  const auto& d = c->d;
+  const int64_t v[12] = {d.t0, d.T_total, d.prev, d.next, d.GR, d.n_base, d.gh_prev, d.gh_next,
+                         d.ramp0, d.R, d.s_lo, c->lifted ? (int64_t)c->n_free - (d.next ? d.GR : 0) : -1};
+  for (int i = 0; i < 12; ++i) info[i] = v[i];
+  if (ramp_gens)
+    for (int32_t k = 0; k < d.GR; ++k) ramp_gens[k] = c->ramp_gens[k];
+  return GN_OK;
 }
 
 int gn_ctx_destroy(gn_ctx* c) {

@@ -18,10 +18,77 @@ static int64_t g_launches = 0;
 void count_launch(int n) { g_launches += n; }
 int64_t launch_count() { return g_launches; }
 
+// ---- per-kernel event timing (gn_profile_*)
+struct ProfRec {
+  std::string name;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+  double ms = 0.0;
+  int64_t launches = 0;
+};
+static bool g_prof = false;
+static std::vector<ProfRec> g_recs;
+
+KTimer::KTimer(const char* name, cudaStream_t stream) {
+  if (!g_prof) return;
+  for (size_t i = 0; i < g_recs.size(); ++i)
+    if (g_recs[i].name == name) idx = static_cast<int>(i);
+  if (idx < 0) {
+    g_recs.push_back(ProfRec{name});
+    idx = static_cast<int>(g_recs.size()) - 1;
+  }
+  s = stream;
+  cudaEventCreate(&a);
+  cudaEventRecord(a, s);
+}
+KTimer::~KTimer() {
+  if (idx < 0) return;
+  cudaEvent_t b;
+  cudaEventCreate(&b);
+  cudaEventRecord(b, s);
+  g_recs[idx].pending.push_back({a, b});
+}
+
+void profile_enable(bool on) { g_prof = on; }
+void profile_reset() {
+  for (auto& r : g_recs)
+    for (auto& e : r.pending) {
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+  g_recs.clear();
+}
+int profile_count() {
+  for (auto& r : g_recs) {
+    for (auto& e : r.pending) {
+      float ms = 0.f;
+      cudaEventSynchronize(e.second);
+      cudaEventElapsedTime(&ms, e.first, e.second);
+      r.ms += ms;
+      r.launches += 1;
+      cudaEventDestroy(e.first);
+      cudaEventDestroy(e.second);
+    }
+    r.pending.clear();
+  }
+  return static_cast<int>(g_recs.size());
+}
+const char* profile_get(int i, double* ms, int64_t* launches) {
+  if (i < 0 || i >= static_cast<int>(g_recs.size())) return nullptr;
+  *ms = g_recs[i].ms;
+  *launches = g_recs[i].launches;
+  return g_recs[i].name.c_str();
+}
+
 OpfDims make_dims(int32_t T, int32_t N, int32_t L, int32_t G, int32_t D, int32_t LT,
-                  int32_t GR, int32_t ref) {
+                  int32_t GR, int32_t ref, int32_t t0, int32_t T_total) {
   OpfDims d{};
   d.T = T; d.N = N; d.L = L; d.G = G; d.D = D; d.LT = LT; d.GR = GR; d.ref = ref;
+  d.t0 = t0;
+  d.T_total = T_total < 0 ? T : T_total;
+  d.prev = t0 > 0 ? 1 : 0;
+  d.next = t0 + T < d.T_total ? 1 : 0;
+  d.s_lo = d.prev ? 0 : 1;
+  d.R = T - 1 + d.prev + d.next;
   const int64_t T64 = T;
   auto chk = [](int64_t v, const char* what) {
     if (v > std::numeric_limits<int32_t>::max())
@@ -35,7 +102,10 @@ OpfDims make_dims(int32_t T, int32_t N, int32_t L, int32_t G, int32_t D, int32_t
   d.q0 = chk(d.p0 + L * T64, "n");
   d.v0 = chk(d.q0 + L * T64, "n");
   d.th0 = chk(d.v0 + N * T64, "n");
-  d.n = chk(d.th0 + N * T64, "n");
+  d.n_base = chk(d.th0 + N * T64, "n");
+  d.gh_prev = d.n_base;
+  d.gh_next = chk(d.gh_prev + (int64_t)(d.prev ? GR : 0), "n");
+  d.n = chk(d.gh_next + (int64_t)(d.next ? GR : 0), "n");
   // rows (opf.hpp:186-230)
   d.bal_p0 = 0;
   d.bal_q0 = chk(N * T64, "m");
@@ -44,7 +114,7 @@ OpfDims make_dims(int32_t T, int32_t N, int32_t L, int32_t G, int32_t D, int32_t
   d.therm0 = chk(d.flow_q0 + L * T64, "m");
   d.ang0 = chk(d.therm0 + LT * T64, "m");
   d.ramp0 = chk(d.ang0 + L * T64, "m");
-  const int64_t ramp_rows = GR * std::max<int64_t>(T64 - 1, 0);
+  const int64_t ramp_rows = GR * std::max<int64_t>(d.R, 0);
   d.m = chk(d.ramp0 + ramp_rows, "m");
   // patterns: records and fields
   const int64_t nrec[K_COUNT] = {G * T64, 2 * L * T64, 2 * L * T64, G * T64, G * T64,
@@ -164,11 +234,11 @@ __global__ void k_struct_thermal(OpfDims d, DevNet net, int32_t* jr, int32_t* jc
 __global__ void k_struct_ramp(OpfDims d, DevNet net, int32_t* jr, int32_t* jc, int32_t* hr,
                               int32_t* hc) {
   const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int32_t Tm = d.T - 1;
-  if (Tm <= 0 || r >= (int64_t)d.GR * Tm) return;
-  const int32_t k = (int32_t)(r / Tm), st = (int32_t)(r - (int64_t)k * Tm);
+  const int32_t Rk = d.R;
+  if (Rk <= 0 || r >= (int64_t)d.GR * Rk) return;
+  const int32_t k = (int32_t)(r / Rk), st = (int32_t)(r - (int64_t)k * Rk);
   const int32_t g = net.ramp_gen[k];
-  const int32_t a = d.pg0 + g * d.T + st + 1, b = a - 1;
+  const int32_t a = ramp_var(d, g, k, d.s_lo + st, true), b = ramp_var(d, g, k, d.s_lo + st, false);
   const int64_t s = d.jac_off[K_RAMP] + 2 * r;
   jr[s] = d.ramp0 + (int32_t)r; jc[s] = a;
   jr[s + 1] = d.ramp0 + (int32_t)r; jc[s + 1] = b;
@@ -195,7 +265,7 @@ void build_structure(gn_ctx* c, int32_t* jr, int32_t* jc, int32_t* hr, int32_t* 
     count_launch();
   }
   if (d.pid[K_RAMP] >= 0) {
-    k_struct_ramp<<<blocks_for((int64_t)d.GR * (d.T - 1), bs), bs, 0, c->stream>>>(d, net, jr, jc, hr, hc);
+    k_struct_ramp<<<blocks_for((int64_t)d.GR * d.R, bs), bs, 0, c->stream>>>(d, net, jr, jc, hr, hc);
     count_launch();
   }
   GN_CK(cudaGetLastError());
@@ -203,9 +273,14 @@ void build_structure(gn_ctx* c, int32_t* jr, int32_t* jc, int32_t* hr, int32_t* 
 
 // ------------------------------------------------------------------ lifted
 // var i belongs to entity i / T in block order [pg G][qg G][p L][q L][v N][th N].
-__global__ void k_free_flags(int32_t n, int32_t T, const uint8_t* fixed_ent, int32_t* flag) {
+__global__ void k_free_flags(int32_t n, int32_t T, int32_t n_base, int32_t gh_next,
+                             const uint8_t* fixed_ent, int32_t* flag) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if (i >= n_base) {  // ghost set-points: prev ghosts are fixed (halo values), next free
+    flag[i] = i >= gh_next ? 1 : 0;
+    return;
+  }
   flag[i] = fixed_ent[i / T] ? 0 : 1;
 }
 __global__ void k_free_scatter(int32_t n, const int32_t* flag, const int32_t* pos,
@@ -272,7 +347,8 @@ void build_lifted(gn_ctx* c) {
   DBuf<int32_t> flag, pos;
   flag.alloc(static_cast<size_t>(d.n) + 1);
   pos.alloc(static_cast<size_t>(d.n) + 1);
-  k_free_flags<<<blocks_for(d.n, bs), bs, 0, s>>>(d.n, d.T, c->var_fixed.p, flag.p);
+  k_free_flags<<<blocks_for(d.n, bs), bs, 0, s>>>(d.n, d.T, d.n_base, d.gh_next, c->var_fixed.p,
+                                                  flag.p);
   count_launch();
   c->n_free = exclusive_scan(flag.p, pos.p, d.n, s);
   c->free_of_full.alloc(static_cast<size_t>(d.n) + 1);
@@ -351,6 +427,14 @@ void host_bounds(const gn_ctx* c, double* xl, double* xu, double* xs, double* rl
   spread(xl, d.th0, d.N, [&](int32_t n) { return n == d.ref ? 0.0 : -inf; });
   spread(xu, d.th0, d.N, [&](int32_t n) { return n == d.ref ? 0.0 : inf; });
   spread(xs, d.th0, d.N, [&](int32_t n) { return n == d.ref ? 0.0 : c->va_start[n]; });
+  // ghost set-points of a period shard: prev ghosts are fixed (their x entries
+  // carry the halo values), next ghosts are free
+  for (int32_t i = d.n_base; i < d.n; ++i) {
+    const bool fixed = i < d.gh_next;
+    if (xl) xl[i] = fixed ? 0.0 : -inf;
+    if (xu) xu[i] = fixed ? 0.0 : inf;
+    if (xs) xs[i] = 0.0;
+  }
   if (rl || ru) {
     for (int32_t i = 0; i < d.therm0; ++i) {
       if (rl) rl[i] = 0.0;
@@ -370,9 +454,9 @@ void host_bounds(const gn_ctx* c, double* xl, double* xu, double* xs, double* rl
       }
     for (int32_t k = 0; k < d.GR; ++k) {
       const double r = c->gen_ramp[c->ramp_gens[k]];
-      for (int64_t s = 0; s < T - 1; ++s) {
-        if (rl) rl[d.ramp0 + k * (T - 1) + s] = -r;
-        if (ru) ru[d.ramp0 + k * (T - 1) + s] = r;
+      for (int64_t s = 0; s < d.R; ++s) {
+        if (rl) rl[d.ramp0 + (int64_t)k * d.R + s] = -r;
+        if (ru) ru[d.ramp0 + (int64_t)k * d.R + s] = r;
       }
     }
   }

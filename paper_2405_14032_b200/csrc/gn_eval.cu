@@ -272,17 +272,16 @@ __global__ void __launch_bounds__(kBS) k_ramp(OpfDims d, DevNet net,
                                               const double* __restrict__ x,
                                               double* __restrict__ out,
                                               unsigned long long* st) {
-  const int32_t Tm = d.T - 1;
-  const int64_t nrec = (int64_t)d.GR * Tm;
+  const int32_t Tm = d.R;
+  const int64_t nrec = (int64_t)d.GR * (Tm > 0 ? Tm : 0);
   const int64_t r0 = (int64_t)blockIdx.x * kBS;
   const int64_t r = r0 + threadIdx.x;
   const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
   if constexpr (MODE == EV_G) {
     if (r < nrec) {
-      const int32_t k = (int32_t)(r / Tm), s = (int32_t)(r - (int64_t)k * Tm);
+      const int32_t k = (int32_t)(r / Tm), s = d.s_lo + (int32_t)(r - (int64_t)k * Tm);
       const int32_t g = __ldg(net.ramp_gen + k);
-      const int64_t i = d.pg0 + (int64_t)g * d.T + s + 1;
-      const double v = x[i] - x[i - 1];
+      const double v = x[ramp_var(d, g, k, s, true)] - x[ramp_var(d, g, k, s, false)];
       out[d.ramp0 + r] = v;
       if (!isfinite(v)) report(st, d.pid[K_RAMP], r);
     }
@@ -346,15 +345,15 @@ void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
                  const double* w, double ow, double* out, double* fpart,
                  unsigned long long* st, cudaStream_t s) {
   const int64_t nl = (int64_t)d.L * d.T, ng = (int64_t)d.G * d.T, nt = (int64_t)d.LT * d.T,
-                nr = d.pid[K_RAMP] >= 0 ? (int64_t)d.GR * (d.T - 1) : 0,
+                nr = d.pid[K_RAMP] >= 0 ? (int64_t)d.GR * d.R : 0,
                 nb = (int64_t)d.N * d.T;
   switch (mode) {
     case EV_F: {
       const unsigned blocks = nblk(ng);
       if (blocks) {
-        k_gen<EV_F><<<blocks, kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
+        { KTimer kt("k_gen<F>", s); k_gen<EV_F><<<blocks, kBS, 0, s>>>(d, net, x, ow, out, fpart, st); }
         count_launch();
-        k_sum_partials<<<1, kBS, 0, s>>>(fpart, (int)blocks, out);
+        { KTimer kt("k_sum_partials", s); k_sum_partials<<<1, kBS, 0, s>>>(fpart, (int)blocks, out); }
         count_launch();
       } else {
         GN_CK(cudaMemsetAsync(out, 0, sizeof(double), s));
@@ -364,32 +363,36 @@ void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
     case EV_GRAD:
       // zero the non-generator blocks, then the cost gradient over pg
       if (d.n > d.qg0) GN_CK(cudaMemsetAsync(out + d.qg0, 0, sizeof(double) * (d.n - d.qg0), s));
-      if (ng) { k_gen<EV_GRAD><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st); count_launch(); }
+      if (ng) { KTimer kt("k_gen<GRAD>", s); k_gen<EV_GRAD><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st); count_launch(); }
       break;
     case EV_G:
-      if (nb) { k_bus<<<nblk(nb), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
-      if (nl) { k_line<EV_G><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
-      if (nt) { k_thermal<EV_G><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
-      if (nr) { k_ramp<EV_G><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
+      if (nb) { KTimer kt("k_bus<G>", s); k_bus<<<nblk(nb), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
+      if (nl) { KTimer kt("k_line<G>", s); k_line<EV_G><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
+      if (nt) { KTimer kt("k_thermal<G>", s); k_thermal<EV_G><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
+      if (nr) { KTimer kt("k_ramp<G>", s); k_ramp<EV_G><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
       break;
     case EV_J:
     case EV_H:
       if (nl) {
+        KTimer kt(mode == EV_J ? "k_line<J>" : "k_line<H>", s);
         if (mode == EV_J) k_line<EV_J><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st);
         else k_line<EV_H><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st);
         count_launch();
       }
       if (ng) {
+        KTimer kt(mode == EV_J ? "k_gen<J>" : "k_gen<H>", s);
         if (mode == EV_J) k_gen<EV_J><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
         else k_gen<EV_H><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
         count_launch();
       }
       if (nt) {
+        KTimer kt(mode == EV_J ? "k_thermal<J>" : "k_thermal<H>", s);
         if (mode == EV_J) k_thermal<EV_J><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st);
         else k_thermal<EV_H><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st);
         count_launch();
       }
       if (nr) {
+        KTimer kt(mode == EV_J ? "k_ramp<J>" : "k_ramp<H>", s);
         if (mode == EV_J) k_ramp<EV_J><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st);
         else k_ramp<EV_H><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st);
         count_launch();

@@ -17,5 +17,9 @@ void host_bounds(const gn_ctx* c, double* xl, double* xu, double* xs, double* rl
                  double* ru);
 int32_t exclusive_scan(const int32_t* flag, int32_t* pos, int64_t n, cudaStream_t s);
 int64_t launch_count();
+void profile_enable(bool on);
+void profile_reset();
+int profile_count();
+const char* profile_get(int i, double* ms, int64_t* launches);
 
 }  // namespace gnb

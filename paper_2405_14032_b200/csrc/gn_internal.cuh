@@ -29,6 +29,15 @@ struct Error : std::runtime_error {
 
 void count_launch(int n = 1);
 
+// Optional per-kernel CUDA-event timing (gn_profile_*): RAII around a launch.
+struct KTimer {
+  int idx = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t a = nullptr;
+  KTimer(const char* name, cudaStream_t stream);
+  ~KTimer();
+};
+
 // Owning device buffer (cudaMalloc / cudaFree on the current device).
 template <class T>
 struct DBuf {
@@ -75,6 +84,12 @@ enum Kind {
 // pattern_model.hpp:158-207).
 struct OpfDims {
   int32_t T, N, L, G, D, LT, GR, ref;
+  // period shard [t0, t0 + T) of a T_total-period horizon; a full
+  // problem is t0 = 0, T_total = T.  Ramp steps s = s_lo .. s_hi (R per ramp
+  // generator) may reference ghost set-points pg(-1) (prev, fixed, halo from
+  // rank r-1) and pg(T) (next, free; its rows are owned by rank r+1), stored
+  // after the regular blocks: [n_base, gh_prev + GR) and [gh_next, gh_next + GR).
+  int32_t t0, T_total, prev, next, s_lo, R, n_base, gh_prev, gh_next;
   int32_t pg0, qg0, p0, q0, v0, th0, n;
   int32_t bal_p0, bal_q0, flow_p0, flow_q0, therm0, ang0, ramp0, m;
   int64_t jac_off[K_COUNT], hess_off[K_COUNT], nrec[K_COUNT];
@@ -83,7 +98,18 @@ struct OpfDims {
 };
 
 OpfDims make_dims(int32_t T, int32_t N, int32_t L, int32_t G, int32_t D, int32_t LT,
-                  int32_t GR, int32_t ref);
+                  int32_t GR, int32_t ref, int32_t t0 = 0, int32_t T_total = -1);
+
+// variable of ramp step s (s = 0..T): pg(s) (a = true) or pg(s-1) (a = false)
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int32_t ramp_var(const OpfDims& d, int32_t g, int32_t k, int32_t s, bool a) {
+  const int32_t p = a ? s : s - 1;
+  if (p < 0) return d.gh_prev + k;
+  if (p >= d.T) return d.gh_next + k;
+  return d.pg0 + g * d.T + p;
+}
 
 // Device pointers to the SoA network tables consumed by the kernels.
 struct DevNet {

@@ -280,6 +280,7 @@ void kkt_set_jacobian(gn_kkt* K, const double* J, bool full) {
   if (!K->annz) return;
   if (full && K->algo != 1 && opf_kkt_ready(K)) return opf_set_jacobian(K, J);
   const int32_t* pick = full ? K->ctx->jpick.p : nullptr;
+  KTimer kt("k_set_jac_generic", K->stream);
   k_set_jac_generic<<<nblk(K->annz), 256, 0, K->stream>>>(K->annz, K->A.seg.p, K->A.src.p, pick,
                                                           J, K->avals.p);
   count_launch();
@@ -291,6 +292,7 @@ void kkt_assemble(gn_kkt* K, const double* H, const double* sx, const double* ss
   if (!K->mnnz) return;
   if (full && K->algo != 1 && opf_kkt_ready(K)) return opf_assemble(K, H, sx, ss, dw, dc);
   const int32_t* hpick = full ? K->ctx->hpick.p : nullptr;
+  KTimer kt("k_assemble_generic", K->stream);
   k_assemble_generic<<<nblk(K->mnnz), 256, 0, K->stream>>>(
       K->mnnz, K->nh, K->npair, K->M.seg.p, K->M.src.p, hpick, H, K->pka.p, K->pkb.p,
       K->arow.p, K->avals.p, sx, ss, dw, dc, K->mvals.p);

@@ -171,22 +171,25 @@ __device__ void fz_gen_cols(const Ctx& c, int32_t gsel, double* M, int32_t* rows
       FOut<STRUCT> o{M, rows, __ldg(t.colptr + cc), 0};
       const int32_t rb = (Q ? t.bal_q0 : t.bal_p0) + n * T + tt;
       const int32_t kr = Q ? -1 : __ldg(t.g_ramp + g);
-      const bool lo_ok = kr >= 0 && tt >= 1, hi_ok = kr >= 0 && tt + 1 < T;
-      const int32_t rr = t.ramp0 + (kr >= 0 ? kr : 0) * (T - 1);  // ramp row of step t=1
+      // ramp row of step s = s_lo .. s_lo + R - 1: row (k, s) couples pg(s-1), pg(s)
+      const bool lo_ok = kr >= 0 && tt >= t.s_lo;              // row (k, tt) exists
+      const bool hi_ok = kr >= 0 && tt + 1 <= t.s_lo + t.R - 1;  // row (k, tt+1) exists
+      const bool ghost = hi_ok && tt + 1 == T;  // its pg(tt+1) is the next rank's (ghost)
+      const int32_t rr = t.ramp0 + (kr >= 0 ? kr : 0) * t.R - t.s_lo;  // + s = row of step s
       {
         double acc = 0.0;
         if constexpr (!STRUCT) {
           if (!Q) acc += h_cost(in.ow, __ldg(t.c2 + g));
           acc += pair_term(c.d(rb), 1.0, 1.0);
-          if (lo_ok) acc += pair_term(c.d(rr + tt - 1), 1.0, 1.0);
-          if (hi_ok) acc += pair_term(c.d(rr + tt), -1.0, -1.0);
+          if (lo_ok) acc += pair_term(c.d(rr + tt), 1.0, 1.0);
+          if (hi_ok) acc += pair_term(c.d(rr + tt + 1), -1.0, -1.0);
           acc += in.dw + in.sx[cc];
         }
         o.put(acc, cc);
       }
-      if (hi_ok) {
+      if (hi_ok && !ghost) {  // (pg(g,t+1), pg(g,t))
         double acc = 0.0;
-        if constexpr (!STRUCT) acc += pair_term(c.d(rr + tt), 1.0, -1.0);
+        if constexpr (!STRUCT) acc += pair_term(c.d(rr + tt + 1), 1.0, -1.0);
         o.put(acc, cc + 1);
       }
       for (int32_t gj = g0; gj < g1; ++gj) {
@@ -203,6 +206,11 @@ __device__ void fz_gen_cols(const Ctx& c, int32_t gsel, double* M, int32_t* rows
         double acc = 0.0;
         if constexpr (!STRUCT) acc += pair_term(c.d(rb), (e & 1) ? -1.0 : 1.0, 1.0);
         o.put(acc, c.col(Q ? c.off_q : c.off_p, l));
+      }
+      if (ghost) {  // (pg_next ghost, pg(g, T-1)): the ghost's lifted index is after every owned column
+        double acc = 0.0;
+        if constexpr (!STRUCT) acc += pair_term(c.d(rr + tt + 1), 1.0, -1.0);
+        o.put(acc, t.n_owned + kr);
       }
       check(o, cc);
     }
@@ -281,6 +289,8 @@ __global__ void __launch_bounds__(256) k_opf_set_jac_fused(OpfKktTab t, int32_t 
     if (len == 2) {
       A[rp] = 0.0 + (-1.0);
       A[rp + 1] = 0.0 + 1.0;
+    } else if (len == 1) {  // shard boundary row: its pg(s-1) is a fixed ghost
+      A[rp] = 0.0 + 1.0;
     }
   }
 }
@@ -309,10 +319,12 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   launch_fz_bus(t, K->opf->bus_large.p, K->opf->n_bus_large, t.maxdeg, in, dv, M, rows, bad, s);
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
+    KTimer kt("k_fz_line", s);
     k_fz_line<STRUCT><<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
     count_launch();
   }
   if (ng > 0) {
+    KTimer kt("k_fz_gen", s);
     k_fz_gen<STRUCT><<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
     count_launch();
   }
@@ -325,6 +337,7 @@ void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, 
                         const double* ss, double dw, double dc) {
   FIn in{x, w, ow, sx, ss, dw, dc};
   if (K->m > 0) {
+    KTimer kt("k_fz_dvec", K->stream);
     k_fz_dvec<<<(unsigned)((K->m + 255) / 256), 256, 0, K->stream>>>(K->m, ss, dw, dc, K->dvals.p);
     count_launch();
   }
@@ -334,10 +347,14 @@ void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, 
 void opf_set_jacobian_fused(gn_kkt* K, const double* x) {
   const OpfKktTab& t = K->opf->t;
   if (K->m <= 0) return;
-  k_opf_set_jac_fused<<<(unsigned)((K->m + 255) / 256), 256, 0, K->stream>>>(t, K->m, x, K->avals.p);
+  {
+    KTimer kt("k_opf_set_jac_fused", K->stream);
+    k_opf_set_jac_fused<<<(unsigned)((K->m + 255) / 256), 256, 0, K->stream>>>(t, K->m, x, K->avals.p);
+  }
   count_launch();
   const int64_t nl = (int64_t)t.L * t.T;
   if (nl > 0 && t.therm0 < t.ang0) {
+    KTimer kt("k_opf_set_jac_thermal", K->stream);
     k_opf_set_jac_thermal<<<(unsigned)((nl + 255) / 256), 256, 0, K->stream>>>(t, x, K->avals.p);
     count_launch();
   }
@@ -373,7 +390,10 @@ bool opf_fused_verify(gn_kkt* K) {
   GN_CK(cudaMemsetAsync(rows.p, 0xff, sizeof(int32_t) * K->mnnz, s));
   FIn in{};
   launch_fused<true>(K, in, nullptr, nullptr, rows.p, bad.p);
-  count_diff(rows.p, K->M.idx.p, K->mnnz, diff.p, s);
+  int32_t owned_nnz = 0;  // slots of the owned columns (next-ghost columns are not assembled)
+  GN_CK(cudaMemcpyAsync(&owned_nnz, K->M.ptr.p + t.n_owned, 4, cudaMemcpyDeviceToHost, s));
+  GN_CK(cudaStreamSynchronize(s));
+  count_diff(rows.p, K->M.idx.p, owned_nnz, diff.p, s);
   int32_t hb[2] = {0, 0};
   GN_CK(cudaMemcpyAsync(&hb[0], bad.p, 4, cudaMemcpyDeviceToHost, s));
   GN_CK(cudaMemcpyAsync(&hb[1], diff.p, 4, cudaMemcpyDeviceToHost, s));

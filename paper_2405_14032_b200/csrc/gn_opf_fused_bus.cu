@@ -208,6 +208,7 @@ void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, in
     GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
+  KTimer kt(maxdeg > kSmallDeg ? "k_fz_bus3<large>" : "k_fz_bus3<small>", s);
   if (rows)
     k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else

@@ -681,6 +681,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
     }
   }
   t.pg0 = d.pg0; t.qg0 = d.qg0; t.p0 = d.p0; t.q0 = d.q0; t.v0 = d.v0; t.th0 = d.th0;
+  t.s_lo = d.s_lo; t.R = d.R; t.prev = d.prev; t.next = d.next;
   t.lg = c->lg.p; t.lb = c->lb.p; t.c2 = c->c2.p;
   // flow-row / angle-row positions
   std::vector<int8_t> fpos(5 * static_cast<size_t>(L)), apos(2 * static_cast<size_t>(L));
@@ -742,7 +743,9 @@ bool opf_kkt_prepare(gn_kkt* K) {
 
   // Verify the enumeration against the generic CSC (row index of every slot).
   const int64_t blocks = assemble_blocks(t);
-  bool ok = nfree_ent * d.T == K->n;
+  t.n_owned = static_cast<int32_t>(nfree_ent * d.T);
+  const bool shard = d.prev || d.next;  // the contract kernels assume a whole horizon
+  bool ok = !shard && nfree_ent * d.T == K->n;
   if (ok && blocks > 0) {
     DBuf<int32_t> rows, bad;
     rows.alloc(static_cast<size_t>(K->mnnz) + 1);
@@ -767,7 +770,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
     }
   }
   X->ready = ok;
-  X->fused_ready = ok && opf_fused_verify(K);
+  X->fused_ready = (nfree_ent * d.T + (d.next ? d.GR : 0) == K->n) && opf_fused_verify(K);
   return ok;
 }
 
@@ -781,6 +784,7 @@ void opf_kkt_free(gn_kkt* K) {
 void opf_set_jacobian(gn_kkt* K, const double* Jfull) {
   const OpfKktTab& t = K->opf->t;
   if (K->m <= 0) return;
+  KTimer kt("k_opf_set_jac", K->stream);
   k_opf_set_jac<<<(unsigned)((K->m + 255) / 256), 256, 0, K->stream>>>(t, K->m, Jfull, K->avals.p);
   count_launch();
   GN_CK(cudaGetLastError());
@@ -792,6 +796,7 @@ void opf_assemble(gn_kkt* K, const double* Hfull, const double* sx, const double
   const int64_t blocks = assemble_blocks(t);
   if (blocks <= 0) return;
   In in{Hfull, K->avals.p, sx, ss, dw, dc};
+  KTimer kt("k_opf_assemble", K->stream);
   k_opf_assemble<false><<<(unsigned)blocks, kMB, 0, K->stream>>>(t, in, K->mvals.p, nullptr, nullptr);
   count_launch();
   GN_CK(cudaGetLastError());

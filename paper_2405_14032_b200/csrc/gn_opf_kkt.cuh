@@ -33,6 +33,8 @@ struct OpfKktTab {
   const double *lg, *lb, *c2;           // line G, B; generator c2
   const int32_t* nb_inc;                // [nb] index of the nb entry in the bus's bl list
   int32_t maxdeg;                       // max incident lines of a bus
+  int32_t s_lo, R, prev, next;          // ramp steps of a period shard (OpfDims)
+  int32_t n_owned;                      // lifted columns owned (next ghosts follow)
   const int32_t* bprog_ptr;             // [N+1] per-bus slot programs of the v(n)/th(n) columns
   const unsigned long long* bprog;      // (row entity << 35 | type << 32 | lane mask)
 };

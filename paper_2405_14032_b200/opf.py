@@ -71,7 +71,11 @@ def load_profile(n_load: int, periods: int, resolution: float = 60.0, seed: int 
 class OpfNlp:
     """Multi-period OPF on one B200 — the NlpProblem the reference's PatternNlp exposes."""
 
-    def __init__(self, net: Network, periods: int, scale: np.ndarray, device: int = 0):
+    def __init__(self, net: Network, periods: int, scale: np.ndarray, device: int = 0,
+                 shard: tuple[int, int] | None = None):
+        """shard = (periods_total, first_period): this object is the period shard
+        [first_period, first_period + periods) of a periods_total horizon
+        (gn_ctx_create_shard); scale is that slice of the demand table."""
         self.lib = abi.lib()
         self.net = net
         self._cnet = net.to_c()
@@ -80,8 +84,13 @@ class OpfNlp:
             raise GridError(abi.GN_ERR_INVALID, "opf: load profile does not match network loads")
         h = C.c_void_p()
         err = GnError()
-        _check(self.lib.gn_ctx_create(C.byref(self._cnet), periods, _f64(self._scale), device,
-                                      C.byref(h), C.byref(err)), err, "gn_ctx_create")
+        if shard is None:
+            rc = self.lib.gn_ctx_create(C.byref(self._cnet), periods, _f64(self._scale), device,
+                                        C.byref(h), C.byref(err))
+        else:
+            rc = self.lib.gn_ctx_create_shard(C.byref(self._cnet), shard[0], shard[1], periods,
+                                              _f64(self._scale), device, C.byref(h), C.byref(err))
+        _check(rc, err, "gn_ctx_create")
         self.h = h
         self.device = device
         self.last_failure = ""
@@ -204,6 +213,16 @@ class OpfNlp:
         else:
             raise ValueError(which)
         return self._record(rc, err)
+
+    def shard_info(self) -> dict:
+        info = (C.c_int64 * 12)()
+        gens = np.zeros(max(self.net.n_gen, 1), np.int32)
+        _check(self.lib.gn_ctx_shard_info(self.h, info, _i32(gens)))
+        keys = ("t0", "T_total", "prev", "next", "n_ramp_gens", "n_base", "ghost_prev0",
+                "ghost_next0", "ramp_row0", "ramp_rows_per_gen", "first_step", "owned_lifted")
+        d = dict(zip(keys, list(info)))
+        d["ramp_gens"] = gens[: d["n_ramp_gens"]].copy()
+        return d
 
     def status(self):
         err = GnError()

@@ -1,0 +1,164 @@
+"""Period sharding of the multi-period OPF — host-side logic.
+
+The horizon [0, T_total) is split into contiguous period ranges, one per rank.
+Rank r's device problem (gn_ctx_create_shard) is the reference layout
+(power/opf.hpp:16-60) over its own periods plus ghost generator set-points:
+
+* ghost_prev[k] = pg(ramp_gen k, t0 - 1): fixed, filled with rank r-1's value;
+* ghost_next[k] = pg(ramp_gen k, t1):     free; it appears only in the ramp rows
+  of step t1, which rank r carries as *ghost rows* (owned by rank r+1, whose
+  sigma_s values rank r receives).
+
+The ramp row of step t belongs to the rank that owns period t.  With the halo
+filled, every owned row value, Jacobian/Hessian record and lifted M column of
+a shard equals the global problem's, bit for bit (tests/test_shard.py).  The
+only exchanges per IPM iteration are G-sized: the boundary set-points
+(forward and backward) and the sigma_s of the boundary ramp rows (backward).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+
+def partition(T_total: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous (first_period, periods) per rank; the first T_total % world ranks get one more."""
+    if world < 1 or T_total < world:
+        raise ValueError("need at least one period per rank")
+    base, extra = divmod(T_total, world)
+    out, t0 = [], 0
+    for r in range(world):
+        T = base + (1 if r < extra else 0)
+        out.append((t0, T))
+        t0 += T
+    return out
+
+
+@dataclass
+class Layout:
+    """OpfLayout offsets for a horizon of T periods (opf.hpp:135-230)."""
+    N: int
+    L: int
+    G: int
+    LT: int
+    GR: int
+    T: int
+    R: int      # ramp rows per ramp generator
+    s_lo: int   # first ramp step
+
+    @property
+    def var_blocks(self):  # (offset, count) of pg, qg, p, q, v, th
+        G, L, N, T = self.G, self.L, self.N, self.T
+        offs = np.cumsum([0, G * T, G * T, L * T, L * T, N * T])
+        return list(zip(offs.tolist(), [G, G, L, L, N, N]))
+
+    @property
+    def row_blocks(self):  # bal_p, bal_q, flow_p, flow_q, thermal, angle
+        N, L, LT, T = self.N, self.L, self.LT, self.T
+        offs = np.cumsum([0, N * T, N * T, L * T, L * T, LT * T])
+        return list(zip(offs.tolist(), [N, N, L, L, LT, L]))
+
+    @property
+    def n_base(self):
+        return 2 * self.T * (self.G + self.L + self.N)
+
+    @property
+    def ramp0(self):
+        return (2 * self.N + 3 * self.L + self.LT) * self.T
+
+
+class ShardMap:
+    """Local <-> global index maps of rank r's shard [t0, t0 + T)."""
+
+    def __init__(self, N: int, L: int, G: int, LT: int, ramp_gens, T_total: int, t0: int, T: int):
+        self.ramp_gens = np.asarray(ramp_gens, np.int64)
+        GR = len(self.ramp_gens) if T_total >= 2 else 0
+        self.T_total, self.t0, self.T = T_total, t0, T
+        self.prev, self.next = t0 > 0, t0 + T < T_total
+        self.glob = Layout(N, L, G, LT, GR, T_total, max(T_total - 1, 0), 1)
+        self.loc = Layout(N, L, G, LT, GR, T, T - 1 + self.prev + self.next, 0 if self.prev else 1)
+        self.GR = GR
+
+    # ------------------------------------------------------------- variables
+    @property
+    def n_local(self):
+        return self.loc.n_base + self.GR * (self.prev + self.next)
+
+    def var_global(self) -> np.ndarray:
+        """Global index of every local variable (ghosts included)."""
+        out = []
+        t = np.arange(self.T)
+        for (lo, cnt), (go, _) in zip(self.loc.var_blocks, self.glob.var_blocks):
+            e = np.arange(cnt)[:, None]
+            out.append((go + e * self.T_total + self.t0 + t[None, :]).reshape(-1))
+        if self.prev:
+            out.append(self.ramp_gens * self.T_total + self.t0 - 1)
+        if self.next:
+            out.append(self.ramp_gens * self.T_total + self.t0 + self.T)
+        return np.concatenate(out).astype(np.int64)
+
+    def ghost_prev(self) -> np.ndarray:
+        return np.arange(self.GR) + self.loc.n_base if self.prev else np.zeros(0, np.int64)
+
+    def ghost_next(self) -> np.ndarray:
+        start = self.loc.n_base + (self.GR if self.prev else 0)
+        return np.arange(self.GR) + start if self.next else np.zeros(0, np.int64)
+
+    # ------------------------------------------------------------------ rows
+    def ramp_steps(self) -> np.ndarray:
+        return np.arange(self.loc.s_lo, self.loc.s_lo + self.loc.R)
+
+    @property
+    def m_local(self):
+        return self.loc.ramp0 + self.GR * self.loc.R
+
+    def row_global(self) -> np.ndarray:
+        out = []
+        t = np.arange(self.T)
+        for (lo, cnt), (go, _) in zip(self.loc.row_blocks, self.glob.row_blocks):
+            e = np.arange(cnt)[:, None]
+            out.append((go + e * self.T_total + self.t0 + t[None, :]).reshape(-1))
+        if self.GR and self.loc.R > 0:
+            k = np.arange(self.GR)[:, None]
+            step = self.t0 + self.ramp_steps()[None, :]  # global step t
+            out.append((self.glob.ramp0 + k * self.glob.R + step - 1).reshape(-1))
+        return np.concatenate(out).astype(np.int64) if out else np.zeros(0, np.int64)
+
+    def row_owned(self) -> np.ndarray:
+        """Ramp rows of step t1 (local step T) are ghosts owned by the next rank."""
+        own = np.ones(self.m_local, bool)
+        if self.next and self.GR:
+            k = np.arange(self.GR)
+            own[self.loc.ramp0 + k * self.loc.R + (self.T - self.loc.s_lo)] = False
+        return own
+
+    # ------------------------------------------------------------------ halo
+    def first_ramp_rows(self) -> np.ndarray:
+        """Local rows of step t0 (the boundary rows this rank owns when prev)."""
+        k = np.arange(self.GR)
+        return self.loc.ramp0 + k * self.loc.R if self.prev else np.zeros(0, np.int64)
+
+    def ghost_rows(self) -> np.ndarray:
+        k = np.arange(self.GR)
+        return (self.loc.ramp0 + k * self.loc.R + (self.T - self.loc.s_lo)) if self.next \
+            else np.zeros(0, np.int64)
+
+    def pg_first(self) -> np.ndarray:
+        """Local indices of pg(ramp gen k, first period) — sent to the previous rank."""
+        return self.ramp_gens * self.T
+
+    def pg_last(self) -> np.ndarray:
+        """Local indices of pg(ramp gen k, last period) — sent to the next rank."""
+        return self.ramp_gens * self.T + self.T - 1
+
+
+def halo_exchange(maps: list[ShardMap], xs: list[np.ndarray], sigma_s: list[np.ndarray]):
+    """In-process halo fill (all ranks' arrays at hand): what the distributed
+    exchange in bench.py / tests/test_shard_gloo.py does with send/recv."""
+    for r, mp in enumerate(maps):
+        if mp.prev:
+            xs[r][mp.ghost_prev()] = xs[r - 1][maps[r - 1].pg_last()]
+        if mp.next:
+            xs[r][mp.ghost_next()] = xs[r + 1][maps[r + 1].pg_first()]
+            sigma_s[r][mp.ghost_rows()] = sigma_s[r + 1][maps[r + 1].first_ramp_rows()]
