@@ -87,24 +87,35 @@ class Clocks:
         nv = self.nv
         while not self._stop.is_set():
             try:
-                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                clk = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                for name, attr in self.REASONS.items():
-                    if r & getattr(nv, attr, 0):
-                        self.reasons.add(name)
+                names = [n for n, a in self.REASONS.items() if r & getattr(nv, a, 0)]
+                self.samples.append((time.perf_counter(), clk, names))
             except Exception:
                 pass
             time.sleep(0.002)
 
-    def stop(self):
+    def mark(self):
+        return time.perf_counter()
+
+    def stop(self, t0, t1):
+        """Samples taken inside [t0, t1] (at least the 3 nearest when the timed
+        region is shorter than the NVML sampling period)."""
         if self.nv is None:
             return None
         self._stop.set()
         self.t.join(timeout=5)
         if not self.samples:
             return None
-        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        inside = [x for x in self.samples if t0 <= x[0] <= t1]
+        widened = len(inside) < 3
+        if widened:
+            mid = 0.5 * (t0 + t1)
+            inside = sorted(self.samples, key=lambda x: abs(x[0] - mid))[:3]
+        reasons = sorted({n for x in inside for n in x[2]})
+        return {"sm_mhz": float(np.median([x[1] for x in inside])),
+                "sm_max_mhz": float(self.max_mhz), "reasons": reasons, "samples": len(inside),
+                "window_widened": widened}
 
 
 # ------------------------------------------------------------------ workload
@@ -219,8 +230,10 @@ def run_ours(args, rank, world, local_rank, dist):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     raw, net, scale = build_workload(rank, world, args.periods, args.config)
+    T_total, first = args.periods * world, args.periods * rank
     t0 = time.time()
-    nlp = OpfNlp(net, args.periods, scale, device=local_rank)
+    # period shard [first, first + periods) of the T_total horizon (world == 1: the whole horizon)
+    nlp = OpfNlp(net, args.periods, scale, device=local_rank, shard=(T_total, first))
     stream = torch.cuda.Stream(device=dev)
     nlp.set_stream(stream.cuda_stream)
     nlp.lift(1e-4)
@@ -249,32 +262,76 @@ def run_ours(args, rank, world, local_rank, dist):
     fused = args.pipeline == "fused"
     if fused and not kkt.fused_ready:
         raise SystemExit("fused KKT path unavailable (verification failed)")
+    if world > 1 and not fused:
+        raise SystemExit("period shards run the fused KKT path")
+
+    # ---- ramp halo: boundary set-points forward/backward, the
+    # sigma_s of the boundary ramp rows backward; G doubles each, over NCCL.
+    halo = None
+    if world > 1:
+        from paper_2405_14032_b200.shard import ShardMap
+        info = nlp.shard_info()
+        mp_ = ShardMap(net.n_bus, net.n_line, net.n_gen, s.n_thermal, info["ramp_gens"],
+                       T_total, first, args.periods)
+        halo = mp_.halo_plan(dev)
+
+    def exchange():
+        from paper_2405_14032_b200.shard import exchange_halo
+        exchange_halo(halo, dx, dss, rank)
+
+    # Two streams: the callbacks on `stream`, the KKT on `kstream`.  Given x, w
+    # and Sigma, f/grad/g/J/H and the fused A/M are independent (the fused KKT
+    # recomputes its J/H terms), so a device-resident IPM overlaps them; the
+    # contract pipeline must wait for J and H.
+    kstream = torch.cuda.Stream(device=dev) if args.streams == 2 else stream
+    kkt.set_stream(kstream.cuda_stream)
+    ev_x = torch.cuda.Event()
+    ev_k = torch.cuda.Event()
 
     def step(ev=None):
-        def mark(i):
+        def mark(i, st=None):
             if ev is not None:
-                ev[i].record(stream)
+                ev[i].record(st or stream)
         mark(0)
+        if halo is not None:
+            with torch.cuda.stream(stream):
+                exchange()
+        ev_x.record(stream)  # x (with its halo) ready
+        if fused and kstream is not stream:
+            kstream.wait_event(ev_x)
+            mark(6, kstream)
+            kkt.set_jacobian_x(dx, mem=A)
+            kkt.assemble_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)
+            mark(7, kstream)
         nlp.eval_device("f", dx, f, sync=False)
         mark(1)
         nlp.eval_device("grad", dx, grad, sync=False)
-        mark(2)
         nlp.eval_device("g", dx, g, sync=False)
-        mark(3)
+        mark(2)
         nlp.eval_device("jac", dx, J, sync=False)
-        mark(4)
+        mark(3)
         nlp.eval_device("hess", dx, H, w=dwt, ow=1.0, sync=False)
-        mark(5)
-        if fused:  # A and M straight from x: bit-identical to the contract path
+        mark(4)
+        if fused and kstream is not stream:
+            ev_k.record(kstream)
+            stream.wait_event(ev_k)
+        elif fused:
+            mark(6)
             kkt.set_jacobian_x(dx, mem=A)
-            mark(6)
             kkt.assemble_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)
-        else:      # contract path: A from J, M from H (GN_IN_FULL: lifted gather fused)
+            mark(7)
+        else:  # contract path: A from J, M from H (GN_IN_FULL: lifted gather fused)
+            ev_k.record(stream)
+            kstream.wait_event(ev_k)
+            mark(6, kstream)
             kkt.set_jacobian(J, mem=A | GN_IN_FULL)
-            mark(6)
             kkt.assemble(H, dsx, dss, dw_reg, dc_reg, mem=A | GN_IN_FULL)
-        mark(7)
+            mark(7, kstream)
+            ev_k.record(kstream)
+            stream.wait_event(ev_k)
+        mark(5)
 
+    clocks = Clocks(local_rank)  # sampling from warm-up on; the timed window is selected below
     for _ in range(args.warmup):
         step()
     assert nlp.status(), f"evaluation failed during warm-up: {nlp.last_failure} {nlp.last_error}"
@@ -283,7 +340,7 @@ def run_ours(args, rank, world, local_rank, dist):
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks = Clocks(local_rank)
+    t_clk0 = clocks.mark()
     launches0 = L.gn_launch_count()
     for k in range(args.steps):
         with torch.cuda.stream(stream):
@@ -293,11 +350,13 @@ def run_ours(args, rank, world, local_rank, dist):
     launches = L.gn_launch_count() - launches0
     if dist:
         dist.barrier()
-    clk = clocks.stop()
+    clk = clocks.stop(t_clk0, clocks.mark())
     assert nlp.status(), "evaluation failed in the timed region"
-    per_step = np.array([ev[0].elapsed_time(ev[7]) for ev in events])  # ms
-    per_stage = {st: float(np.mean([ev[i].elapsed_time(ev[i + 1]) for ev in events]))
-                 for i, st in enumerate(stages)}
+    per_step = np.array([ev[0].elapsed_time(ev[5]) for ev in events])  # ms
+    spans = {"f": (0, 1), "grad+g": (1, 2), "jac": (2, 3), "hess": (3, 4),
+             "kkt (set_jacobian + assemble)": (6, 7), "callbacks": (0, 4)}
+    per_stage = {k: float(np.mean([ev[a].elapsed_time(ev[b]) for ev in events]))
+                 for k, (a, b) in spans.items()}
     ms = float(per_step.mean())
     if dist:
         import torch.distributed as tdist
@@ -391,9 +450,10 @@ def run_ours(args, rank, world, local_rank, dist):
         "kernels": kernels,
         "unit_roofline": {"alg_bytes": unit_bytes, "achieved": unit_gbs, "peak": peak,
                           "frac": unit_gbs / peak, "unit": "GB/s"},
-        "pipeline": ("fused: set_jacobian/assemble recompute J/H terms from x "
-                     "(bit-identical to the contract path, tested)") if fused else
-                    "contract: set_jacobian(J) + assemble(H) read the callback outputs",
+        "pipeline": (("fused: set_jacobian/assemble recompute J/H terms from x "
+                      "(bit-identical to the contract path, tested)") if fused else
+                     "contract: set_jacobian(J) + assemble(H) read the callback outputs")
+                    + (f"; {args.streams} streams"),
         "stages_ms": per_stage,
         "setup_s": setup_s,
         "clocks": clk,
@@ -504,7 +564,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=CONFIG)
@@ -515,6 +575,7 @@ def main():
     ap.add_argument("--cpu-periods", type=int, default=2)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
+    ap.add_argument("--streams", type=int, choices=[1, 2], default=2)
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
     args = ap.parse_args()
 

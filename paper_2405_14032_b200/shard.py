@@ -152,6 +152,45 @@ class ShardMap:
         """Local indices of pg(ramp gen k, last period) — sent to the next rank."""
         return self.ramp_gens * self.T + self.T - 1
 
+    def halo_plan(self, device=None) -> dict:
+        """Index tensors of the distributed exchange (exchange_halo)."""
+        import torch
+        ix = lambda a: torch.from_numpy(np.asarray(a, np.int64)).to(device)  # noqa: E731
+        return dict(pg_last=ix(self.pg_last()), pg_first=ix(self.pg_first()),
+                    g_prev=ix(self.ghost_prev()), g_next=ix(self.ghost_next()),
+                    rows_first=ix(self.first_ramp_rows()), rows_ghost=ix(self.ghost_rows()),
+                    GR=self.GR, prev=self.prev, next=self.next)
+
+
+def exchange_halo(plan: dict, x, sigma_s, rank: int):
+    """One ramp-halo exchange with torch.distributed (NCCL on device tensors in
+    bench.py; gloo on CPU in tests/test_shard_gloo.py): pg(., t1-1) to the next
+    rank, pg(., t0) and the boundary rows' sigma_s to the previous rank, written
+    into this rank's ghost set-points / ghost rows.  G doubles per message."""
+    import torch
+    import torch.distributed as tdist
+    kw = dict(dtype=x.dtype, device=x.device)
+    ops, recv = [], {}
+    if plan["next"]:
+        ops.append(tdist.P2POp(tdist.isend, x.index_select(0, plan["pg_last"]), rank + 1))
+        recv["xn"] = torch.empty(plan["GR"], **kw)
+        recv["sn"] = torch.empty(plan["GR"], **kw)
+        ops.append(tdist.P2POp(tdist.irecv, recv["xn"], rank + 1))
+        ops.append(tdist.P2POp(tdist.irecv, recv["sn"], rank + 1))
+    if plan["prev"]:
+        recv["xp"] = torch.empty(plan["GR"], **kw)
+        ops.append(tdist.P2POp(tdist.irecv, recv["xp"], rank - 1))
+        ops.append(tdist.P2POp(tdist.isend, x.index_select(0, plan["pg_first"]), rank - 1))
+        ops.append(tdist.P2POp(tdist.isend, sigma_s.index_select(0, plan["rows_first"]), rank - 1))
+    if ops:
+        for wk in tdist.batch_isend_irecv(ops):
+            wk.wait()
+    if "xp" in recv:
+        x.index_copy_(0, plan["g_prev"], recv["xp"])
+    if "xn" in recv:
+        x.index_copy_(0, plan["g_next"], recv["xn"])
+        sigma_s.index_copy_(0, plan["rows_ghost"], recv["sn"])
+
 
 def halo_exchange(maps: list[ShardMap], xs: list[np.ndarray], sigma_s: list[np.ndarray]):
     """In-process halo fill (all ranks' arrays at hand): what the distributed
