@@ -307,6 +307,9 @@ class CondensedKkt:
                                      GN_MEM_HOST))
         return js, hs, ps, ds
 
+    def set_stream(self, stream_handle: int):
+        _check(self.lib.gn_kkt_set_stream(self.h, C.c_void_p(stream_handle)))
+
     def set_algorithm(self, algo: int):
         _check(self.lib.gn_kkt_set_algorithm(self.h, algo))
 
