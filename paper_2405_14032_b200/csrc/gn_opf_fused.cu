@@ -71,7 +71,8 @@ struct Ctx {
 
 // p(l) and q(l) columns of line l at period c.tt (thread per (l, t)).
 template <bool STRUCT>
-__device__ void fz_line_cols(const Ctx& c, int32_t l, double* M, int32_t* rows, int32_t* bad) {
+__device__ void fz_line_cols(const Ctx& c, int32_t l, double* Mp, double* Mq, int64_t basep,
+                             int64_t baseq, int32_t* rows, int32_t* bad) {
   const OpfKktTab& t = c.t;
   const FIn& in = c.in;
   const int32_t T = c.T, tt = c.tt;
@@ -92,7 +93,7 @@ __device__ void fz_line_cols(const Ctx& c, int32_t l, double* M, int32_t* rows, 
 #pragma unroll
     for (int Q = 0; Q < 2; ++Q) {
       const int32_t cc = c.col(Q ? c.off_q : c.off_p, l);
-      FOut<STRUCT> o{M, rows, __ldg(t.colptr + cc), 0};
+      FOut<STRUCT> o{Q ? Mq : Mp, rows, __ldg(t.colptr + cc) - (Q ? baseq : basep), 0};
       const int32_t bal0 = Q ? t.bal_q0 : t.bal_p0, flow0 = Q ? t.flow_q0 : t.flow_p0;
       double jt = 0.0, jp = 0.0;
       if (k >= 0) {
@@ -145,7 +146,7 @@ __device__ void fz_line_cols(const Ctx& c, int32_t l, double* M, int32_t* rows, 
           }
           o.put(acc, cr);
         }
-      check(o, cc);
+      if (STRUCT && o.base + (Q ? baseq : basep) + o.j != __ldg(t.colptr + cc + 1)) atomicOr(bad, 1);
     }
   }
 }
@@ -224,16 +225,50 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
   if (r < m) dv[r] = dvec(ss[r], dw, dc);
 }
 
+// p(l)/q(l) columns, one thread per (l, t).  Consecutive (l, t) own consecutive
+// lifted columns, so a CTA's p (and q) columns are one contiguous span of M:
+// staged in shared memory and written back coalesced.
+constexpr int kFL = 128, kFLCap = kFL * 16;
 template <bool STRUCT>
-__global__ void __launch_bounds__(256) k_fz_line(OpfKktTab t, FIn in, const double* __restrict__ dv,
+__global__ void __launch_bounds__(kFL) k_fz_line(OpfKktTab t, FIn in, const double* __restrict__ dv,
                                                  double* __restrict__ M, int32_t* __restrict__ rows,
                                                  int32_t* __restrict__ bad) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= (int64_t)t.L * t.T) return;
-  const int32_t l = (int32_t)(r / t.T), tt = (int32_t)(r - (int64_t)l * t.T);
-  Ctx c{t, in, 0, tt, t.T, 0, 0, nullptr, 0, dv,
-        0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
-  fz_line_cols<STRUCT>(c, l, M, rows, bad);
+  __shared__ double sp[STRUCT ? 1 : kFLCap], sq[STRUCT ? 1 : kFLCap];
+  const int64_t nrec = (int64_t)t.L * t.T;
+  const int64_t r0 = (int64_t)blockIdx.x * kFL, r = r0 + threadIdx.x;
+  const int64_t rl = min(nrec, r0 + kFL) - 1;
+  const bool valid = r < nrec;
+  const int32_t T = t.T;
+  const int32_t offp = 2 * t.G, offq = 2 * t.G + t.L;
+  auto colof = [&](int32_t off, int64_t rec) {
+    const int32_t l = (int32_t)(rec / T), tt = (int32_t)(rec - (int64_t)l * T);
+    return __ldg(t.lent + off + l) * T + tt;
+  };
+  int64_t bp = 0, bq = 0;
+  bool staged = false;
+  if constexpr (!STRUCT) {
+    bp = __ldg(t.colptr + colof(offp, r0));
+    bq = __ldg(t.colptr + colof(offq, r0));
+    const int64_t ep = __ldg(t.colptr + colof(offp, rl) + 1), eq = __ldg(t.colptr + colof(offq, rl) + 1);
+    staged = (ep - bp) <= kFLCap && (eq - bq) <= kFLCap;
+    if (valid) {
+      const int32_t l = (int32_t)(r / T), tt = (int32_t)(r - (int64_t)l * T);
+      Ctx c{t, in, 0, tt, T, 0, 0, nullptr, 0, dv,
+            0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
+      if (staged) fz_line_cols<false>(c, l, sp, sq, bp, bq, rows, bad);
+      else fz_line_cols<false>(c, l, M, M, 0, 0, rows, bad);
+    }
+    if (staged) {
+      __syncthreads();
+      for (int64_t i = threadIdx.x; i < ep - bp; i += kFL) M[bp + i] = sp[i];
+      for (int64_t i = threadIdx.x; i < eq - bq; i += kFL) M[bq + i] = sq[i];
+    }
+  } else if (valid) {
+    const int32_t l = (int32_t)(r / T), tt = (int32_t)(r - (int64_t)l * T);
+    Ctx c{t, in, 0, tt, T, 0, 0, nullptr, 0, dv,
+          0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
+    fz_line_cols<true>(c, l, M, M, 0, 0, rows, bad);
+  }
 }
 
 template <bool STRUCT>
@@ -249,22 +284,18 @@ __global__ void __launch_bounds__(256) k_fz_gen(OpfKktTab t, FIn in, const doubl
 }
 
 // ------------------------------------------------------ A straight from x
-__global__ void __launch_bounds__(256) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
-                                                           const double* __restrict__ x,
-                                                           double* __restrict__ A) {
-  const int64_t r64 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r64 >= m) return;
-  const int32_t r = (int32_t)r64, T = t.T;
-  const int32_t rp = __ldg(t.rowptr + r);
-  if (r < t.flow_p0) {  // balance rows: generators (J = 1) then flows (J = +-1)
+__device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const double* __restrict__ x,
+                                       double* __restrict__ dst) {
+  const int32_t T = t.T;
+  if (r < t.flow_p0) {  // balance rows: free generators (J = 1) then flows (J = +-1)
     const bool Q = r >= t.bal_q0;
     const int32_t rr = r - (Q ? t.bal_q0 : t.bal_p0);
     const int32_t b = rr / T;
     const int32_t nf = __ldg((Q ? t.ngq : t.ngp) + b);
-    for (int32_t i = 0; i < nf; ++i) A[rp + i] = 0.0 + 1.0;
+    for (int32_t i = 0; i < nf; ++i) dst[i] = 0.0 + 1.0;
     const int32_t b0 = __ldg(t.bl_ptr + b), b1 = __ldg(t.bl_ptr + b + 1);
-    for (int32_t i = b0; i < b1; ++i) A[rp + nf + (i - b0)] = 0.0 + ((__ldg(t.bl + i) & 1) ? -1.0 : 1.0);
-  } else if (r < t.therm0) {
+    for (int32_t i = b0; i < b1; ++i) dst[nf + (i - b0)] = 0.0 + ((__ldg(t.bl + i) & 1) ? -1.0 : 1.0);
+  } else if (r < t.therm0) {  // flow definitions: J from the line state
     const bool Q = r >= t.flow_q0;
     const int32_t rr = r - (Q ? t.flow_q0 : t.flow_p0);
     const int32_t l = rr / T, tt = rr - l * T;
@@ -275,38 +306,48 @@ __global__ void __launch_bounds__(256) k_opf_set_jac_fused(OpfKktTab t, int32_t 
 #pragma unroll
     for (int fl = 0; fl < 5; ++fl) {
       const int p = __ldg(t.fpos + 5 * l + fl);
-      if (p >= 0) A[rp + p] = 0.0 + (Q ? j_flow_q(s, G, B, fl) : j_flow_p(s, G, B, fl));
+      if (p >= 0) dst[p] = 0.0 + (Q ? j_flow_q(s, G, B, fl) : j_flow_p(s, G, B, fl));
     }
-  } else if (r < t.ang0) {  // thermal rows: k_opf_set_jac_thermal (needs the rated line)
-    return;
-  } else if (r < t.ramp0) {
-    const int32_t rr = r - t.ang0, l = rr / T;
+  } else if (r < t.ang0) {  // thermal [p, q]: (2p, 2q)
+    const int32_t rr = r - t.therm0, k = rr / T, tt = rr - k * T;
+    const int32_t l = __ldg(t.th_line + k);
+    dst[0] = 0.0 + j_thermal(x[t.p0 + (int64_t)l * T + tt]);
+    dst[1] = 0.0 + j_thermal(x[t.q0 + (int64_t)l * T + tt]);
+  } else if (r < t.ramp0) {  // angle [th_f, th_t]: (1, -1)
+    const int32_t l = (r - t.ang0) / T;
     const int pf = __ldg(t.apos + 2 * l), pt = __ldg(t.apos + 2 * l + 1);
-    if (pf >= 0) A[rp + pf] = 0.0 + 1.0;
-    if (pt >= 0) A[rp + pt] = 0.0 + (-1.0);
-  } else {
-    const int32_t len = __ldg(t.rowptr + r + 1) - rp;
+    if (pf >= 0) dst[pf] = 0.0 + 1.0;
+    if (pt >= 0) dst[pt] = 0.0 + (-1.0);
+  } else {  // ramp [pg_{s-1}, pg_s]: (-1, 1); a shard's first row keeps pg_s only
+    const int32_t len = __ldg(t.rowptr + r + 1) - __ldg(t.rowptr + r);
     if (len == 2) {
-      A[rp] = 0.0 + (-1.0);
-      A[rp + 1] = 0.0 + 1.0;
-    } else if (len == 1) {  // shard boundary row: its pg(s-1) is a fixed ghost
-      A[rp] = 0.0 + 1.0;
+      dst[0] = 0.0 + (-1.0);
+      dst[1] = 0.0 + 1.0;
+    } else if (len == 1) {
+      dst[0] = 0.0 + 1.0;
     }
   }
 }
 
-// thermal rows need the rated line of the slot: one thread per (line, t) of rated lines
-__global__ void k_opf_set_jac_thermal(OpfKktTab t, const double* __restrict__ x,
-                                      double* __restrict__ A) {
-  const int64_t r64 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r64 >= (int64_t)t.L * t.T) return;
-  const int32_t l = (int32_t)(r64 / t.T), tt = (int32_t)(r64 - (int64_t)l * t.T);
-  const int32_t k = __ldg(t.l_therm + l);
-  if (k < 0) return;
-  const int32_t r = t.therm0 + k * t.T + tt;
-  const int32_t rp = __ldg(t.rowptr + r);
-  A[rp] = 0.0 + j_thermal(x[t.p0 + r64]);
-  A[rp + 1] = 0.0 + j_thermal(x[t.q0 + r64]);
+// A = set_jacobian(eval_jac(x)) straight from x.  One thread per CSR row; the
+// rows of a CTA occupy one contiguous span of A, staged in shared memory and
+// written back as a single coalesced stream.
+constexpr int kSJ = 256, kSJCap = kSJ * 8;
+__global__ void __launch_bounds__(kSJ) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
+                                                           const double* __restrict__ x,
+                                                           double* __restrict__ A) {
+  __shared__ double sm[kSJCap];
+  const int32_t r0 = blockIdx.x * kSJ;
+  const int32_t r = r0 + threadIdx.x;
+  const int32_t rend = min(m, r0 + kSJ);
+  const int32_t base = __ldg(t.rowptr + r0), span = __ldg(t.rowptr + rend) - base;
+  if (span > kSJCap) {  // unusually long rows: write in place
+    if (r < m) sj_row(t, r, x, A + __ldg(t.rowptr + r));
+    return;
+  }
+  if (r < m) sj_row(t, r, x, sm + (__ldg(t.rowptr + r) - base));
+  __syncthreads();
+  for (int i = threadIdx.x; i < span; i += kSJ) A[base + i] = sm[i];
 }
 
 // ------------------------------------------------------------------ host
@@ -320,7 +361,7 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
     KTimer kt("k_fz_line", s);
-    k_fz_line<STRUCT><<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
+    k_fz_line<STRUCT><<<(unsigned)((nl + kFL - 1) / kFL), kFL, 0, s>>>(t, in, dv, M, rows, bad);
     count_launch();
   }
   if (ng > 0) {
@@ -349,15 +390,10 @@ void opf_set_jacobian_fused(gn_kkt* K, const double* x) {
   if (K->m <= 0) return;
   {
     KTimer kt("k_opf_set_jac_fused", K->stream);
-    k_opf_set_jac_fused<<<(unsigned)((K->m + 255) / 256), 256, 0, K->stream>>>(t, K->m, x, K->avals.p);
+    k_opf_set_jac_fused<<<(unsigned)((K->m + kSJ - 1) / kSJ), kSJ, 0, K->stream>>>(t, K->m, x,
+                                                                                   K->avals.p);
   }
   count_launch();
-  const int64_t nl = (int64_t)t.L * t.T;
-  if (nl > 0 && t.therm0 < t.ang0) {
-    KTimer kt("k_opf_set_jac_thermal", K->stream);
-    k_opf_set_jac_thermal<<<(unsigned)((nl + 255) / 256), 256, 0, K->stream>>>(t, x, K->avals.p);
-    count_launch();
-  }
   GN_CK(cudaGetLastError());
 }
 

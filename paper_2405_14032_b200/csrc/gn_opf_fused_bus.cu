@@ -196,137 +196,6 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   }
 }
 
-// Small-degree variant (deg <= kSmallDeg): the state of every incident line lives
-// in registers (fully unrolled over the line slots), so each slot's ordered sum
-// is straight-line arithmetic with no shared-memory or address traffic.
-template <bool STRUCT>
-__global__ void __launch_bounds__(kBW3 * 32) k_fz_bus_small(OpfKktTab t, const int32_t* __restrict__ buses,
-                                                            int32_t n_buses, FIn in,
-                                                            const double* __restrict__ dv,
-                                                            double* __restrict__ M,
-                                                            int32_t* __restrict__ rows,
-                                                            int32_t* __restrict__ bad) {
-  constexpr int K = kSmallDeg;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kBW3 + warp;
-  const int64_t n64 = w / t.tchunks;
-  if (n64 >= n_buses) return;
-  const int32_t n = __ldg(buses + n64), T = t.T;
-  const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
-  if (tt >= T) return;
-  const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
-  const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
-
-  LineState S[K];
-  double G[K], B[K], w7[K], w8[K], d7[K], d8[K], d10[K];
-  int fr[K];
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    S[k] = LineState{};
-    G[k] = B[k] = w7[k] = w8[k] = d7[k] = d8[k] = d10[k] = 0.0;
-    fr[k] = 0;
-    if constexpr (!STRUCT) {
-      if (k < deg) {
-        const int32_t e = __ldg(t.bl + b0 + k), l = e >> 1;
-        fr[k] = e & 1;
-        G[k] = __ldg(t.lg + l);
-        B[k] = __ldg(t.lb + l);
-        const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
-        S[k] = line_state(G[k], B[k], in.x[t.v0 + (int64_t)f * T + tt],
-                          in.x[t.v0 + (int64_t)to * T + tt], in.x[t.th0 + (int64_t)f * T + tt],
-                          in.x[t.th0 + (int64_t)to * T + tt]);
-        const int64_t lt_ = (int64_t)l * T + tt;
-        w7[k] = in.w[t.flow_p0 + lt_];
-        w8[k] = in.w[t.flow_q0 + lt_];
-        d7[k] = dv[t.flow_p0 + lt_];
-        d8[k] = dv[t.flow_q0 + lt_];
-        d10[k] = dv[t.ang0 + lt_];
-      }
-    }
-  }
-  // J of this bus's side (other = the far end; theta = angle field)
-#define JP(k, other, theta) \
-  j_flow_p(S[k], G[k], B[k], (theta) ? ((fr[k] ^ (other)) ? 3 : 4) : ((fr[k] ^ (other)) ? 1 : 2))
-#define JQ(k, other, theta) \
-  j_flow_q(S[k], G[k], B[k], (theta) ? ((fr[k] ^ (other)) ? 3 : 4) : ((fr[k] ^ (other)) ? 1 : 2))
-#define PASS(expr)                               \
-  _Pragma("unroll") for (int k = 0; k < K; ++k)  \
-    if ((mask >> k) & 1u) acc += (expr);
-
-  auto col = [&](int32_t off, int32_t e) {
-    const int32_t kk = __ldg(t.lent + off + e);
-    return kk < 0 ? -1 : kk * T + tt;
-  };
-  const int32_t cv = col(off_v, n), ct = col(off_th, n);
-  const int64_t posv = cv >= 0 ? (int64_t)__ldg(t.colptr + cv) : 0;
-  const int64_t post = ct >= 0 ? (int64_t)__ldg(t.colptr + ct) : 0;
-  int jv = 0, jt = 0;
-  const int32_t p0 = __ldg(t.bprog_ptr + n), p1 = __ldg(t.bprog_ptr + n + 1);
-  for (int32_t q = p0; q < p1; ++q) {
-    const unsigned long long code = __ldg(t.bprog + q);
-    const uint32_t mask = (uint32_t)code;
-    const int type = (int)((code >> 32) & 7);
-    const int32_t rent = (int32_t)(code >> 35);
-    double acc = 0.0;
-    if constexpr (!STRUCT) {
-      switch (type) {
-        case 0:
-          PASS(h_flow_p(S[k], G[k], w7[k], fr[k] ? 5 : 9));
-          PASS(h_flow_q(S[k], B[k], w8[k], fr[k] ? 5 : 9));
-          PASS(pair_term(d7[k], JP(k, 0, 0), JP(k, 0, 0)));
-          PASS(pair_term(d8[k], JQ(k, 0, 0), JQ(k, 0, 0)));
-          acc += in.dw + in.sx[cv];
-          break;
-        case 1:
-          PASS(h_flow_p(S[k], G[k], w7[k], 6));
-          PASS(h_flow_q(S[k], B[k], w8[k], 6));
-          PASS(pair_term(d7[k], JP(k, 1, 0), JP(k, 0, 0)));
-          PASS(pair_term(d8[k], JQ(k, 1, 0), JQ(k, 0, 0)));
-          break;
-        case 2:
-          PASS(h_flow_p(S[k], G[k], w7[k], fr[k] ? 7 : 11));
-          PASS(h_flow_q(S[k], B[k], w8[k], fr[k] ? 7 : 11));
-          PASS(pair_term(d7[k], JP(k, 0, 1), JP(k, 0, 0)));
-          PASS(pair_term(d8[k], JQ(k, 0, 1), JQ(k, 0, 0)));
-          break;
-        case 3:
-          PASS(h_flow_p(S[k], G[k], w7[k], fr[k] ? 8 : 10));
-          PASS(h_flow_q(S[k], B[k], w8[k], fr[k] ? 8 : 10));
-          PASS(pair_term(d7[k], JP(k, 1, 1), JP(k, 0, 0)));
-          PASS(pair_term(d8[k], JQ(k, 1, 1), JQ(k, 0, 0)));
-          break;
-        case 4:
-          PASS(h_flow_p(S[k], G[k], w7[k], fr[k] ? 12 : 14));
-          PASS(h_flow_q(S[k], B[k], w8[k], fr[k] ? 12 : 14));
-          PASS(pair_term(d7[k], JP(k, 0, 1), JP(k, 0, 1)));
-          PASS(pair_term(d8[k], JQ(k, 0, 1), JQ(k, 0, 1)));
-          PASS(pair_term(d10[k], fr[k] ? 1.0 : -1.0, fr[k] ? 1.0 : -1.0));
-          acc += in.dw + in.sx[ct];
-          break;
-        default:
-          PASS(h_flow_p(S[k], G[k], w7[k], 13));
-          PASS(h_flow_q(S[k], B[k], w8[k], 13));
-          PASS(pair_term(d7[k], JP(k, 1, 1), JP(k, 0, 1)));
-          PASS(pair_term(d8[k], JQ(k, 1, 1), JQ(k, 0, 1)));
-          PASS(pair_term(d10[k], fr[k] ? -1.0 : 1.0, fr[k] ? 1.0 : -1.0));
-          break;
-      }
-    }
-    const bool in_v = type < 4;
-    const int64_t at = in_v ? posv + jv : post + jt;
-    if constexpr (STRUCT) rows[at] = col((type == 0 || type == 1) ? off_v : off_th, rent);
-    else M[at] = acc;
-    if (in_v) ++jv; else ++jt;
-  }
-#undef PASS
-#undef JP
-#undef JQ
-  if (STRUCT) {
-    if (cv >= 0 && posv + jv != __ldg(t.colptr + cv + 1)) atomicOr(bad, 1);
-    if (ct >= 0 && post + jt != __ldg(t.colptr + ct + 1)) atomicOr(bad, 1);
-  }
-}
-
 void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
                    const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
                    cudaStream_t s) {
@@ -341,20 +210,7 @@ void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, in
     GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  static const bool use_small = [] {
-    const char* e = std::getenv("GRIDNLP_B200_BUS_SMALL");
-    return !(e && e[0] == '0');
-  }();
-  if (maxdeg <= kSmallDeg && use_small) {  // register-resident variant
-    KTimer kt("k_fz_bus_small", s);
-    if (rows)
-      k_fz_bus_small<true><<<blocks, kBW3 * 32, 0, s>>>(t, buses, n_buses, in, dv, M, rows, bad);
-    else
-      k_fz_bus_small<false><<<blocks, kBW3 * 32, 0, s>>>(t, buses, n_buses, in, dv, M, rows, bad);
-    count_launch();
-    return;
-  }
-  KTimer kt("k_fz_bus3<large>", s);
+  KTimer kt(maxdeg > kSmallDeg ? "k_fz_bus3<large>" : "k_fz_bus3<small>", s);
   if (rows)
     k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else

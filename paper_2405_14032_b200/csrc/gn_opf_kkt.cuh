@@ -31,6 +31,7 @@ struct OpfKktTab {
   // fused (recompute-from-x) path
   int32_t pg0, qg0, p0, q0, v0, th0;    // variable block offsets (full x)
   const double *lg, *lb, *c2;           // line G, B; generator c2
+  const int32_t* th_line;               // [LT] line of each thermal slot
   const int32_t* nb_inc;                // [nb] index of the nb entry in the bus's bl list
   int32_t maxdeg;                       // max incident lines of a bus
   int32_t s_lo, R, prev, next;          // ramp steps of a period shard (OpfDims)
