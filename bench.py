@@ -171,15 +171,18 @@ def kernel_bytes(s, kkt, nlp, net, T):
     bounds = np.cumsum([0, G * T, G * T, L * T, L * T, N * T, N * T])
     blk = np.searchsorted(bounds, f2f, side="right") - 1  # 0 pg 1 qg 2 p 3 q 4 v 5 th
     deg = np.bincount(np.concatenate([net.line_from, net.line_to]), minlength=N)
-    small = deg <= 4
     ent = np.where(blk >= 4, (f2f - bounds[np.minimum(blk, 5)]) // T, -1)
-    vth = blk >= 4
-    m_small = int(lens[vth & small[np.maximum(ent, 0)]].sum())
-    m_large = int(lens[vth & ~small[np.maximum(ent, 0)]].sum())
+    vth = (blk == 4) | (blk == 5)
     m_pq = int(lens[(blk == 2) | (blk == 3)].sum())
     m_g = int(lens[blk <= 1].sum())
-    fs = float(deg[small].sum()) / max(2 * L, 1)
-    nsm, nlg = int(small.sum()) * T, int((~small).sum()) * T
+    # bus-column kernel, per degree class: its M slots, x(v, th) + Sx(v, th) of its
+    # buses, and its share (half per line end) of the line inputs
+    # w(flow_p, flow_q), d(flow_p, flow_q, angle)
+    cls = np.where(deg <= 1, 0, np.minimum(deg, 5) - 1)
+    m_cls = [int(lens[vth & (cls[np.clip(ent, 0, N - 1)] == k)].sum()) for k in range(5)]
+    bus_cls = {f"k_fz_bus3<{nm}>": m_cls[k] + 4 * int((cls == k).sum()) * T
+               + 2.5 * int(deg[cls == k].sum()) * T
+               for k, nm in enumerate(["d1", "d2", "d3", "d4", "large"])}
     b = {
         "k_gen<F>": G * T, "k_gen<GRAD>": 2 * G * T,
         "k_bus<G>": 2 * N * T + 2 * L * T + 2 * G * T + 2 * D * T,
@@ -192,8 +195,7 @@ def kernel_bytes(s, kkt, nlp, net, T):
         "k_opf_set_jac_fused": annz - 2 * LTh * T + 2 * N * T,
         "k_opf_set_jac_thermal": 4 * LTh * T,
         "k_fz_dvec": 2 * m,
-        "k_fz_bus3<small>": m_small + 4 * nsm + fs * 5 * L * T,
-        "k_fz_bus3<large>": m_large + 4 * nlg + (1 - fs) * 5 * L * T,
+        **bus_cls,
         "k_fz_line": m_pq + 2 * L * T + 2 * N * T + 2 * N * T + 2 * L * T + 2 * LTh * T + 2 * L * T,
         "k_fz_gen": m_g + 2 * G * T + GR * R + 2 * G * T,
         "k_opf_set_jac": 2 * annz, "k_set_jac_generic": 2 * annz,

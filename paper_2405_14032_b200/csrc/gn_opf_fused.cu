@@ -225,50 +225,21 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
   if (r < m) dv[r] = dvec(ss[r], dw, dc);
 }
 
-// p(l)/q(l) columns, one thread per (l, t).  Consecutive (l, t) own consecutive
-// lifted columns, so a CTA's p (and q) columns are one contiguous span of M:
-// staged in shared memory and written back coalesced.
-constexpr int kFL = 128, kFLCap = kFL * 16;
+// p(l)/q(l) columns, one thread per (l, t).  (Staging the CTA's contiguous span
+// of M through shared memory was measured slower: the kernel is latency-bound
+// on its dependent index loads, not on write coalescing.)
+constexpr int kFL = 256;
 template <bool STRUCT>
 __global__ void __launch_bounds__(kFL) k_fz_line(OpfKktTab t, FIn in, const double* __restrict__ dv,
                                                  double* __restrict__ M, int32_t* __restrict__ rows,
                                                  int32_t* __restrict__ bad) {
-  __shared__ double sp[STRUCT ? 1 : kFLCap], sq[STRUCT ? 1 : kFLCap];
-  const int64_t nrec = (int64_t)t.L * t.T;
-  const int64_t r0 = (int64_t)blockIdx.x * kFL, r = r0 + threadIdx.x;
-  const int64_t rl = min(nrec, r0 + kFL) - 1;
-  const bool valid = r < nrec;
+  const int64_t r = (int64_t)blockIdx.x * kFL + threadIdx.x;
+  if (r >= (int64_t)t.L * t.T) return;
   const int32_t T = t.T;
-  const int32_t offp = 2 * t.G, offq = 2 * t.G + t.L;
-  auto colof = [&](int32_t off, int64_t rec) {
-    const int32_t l = (int32_t)(rec / T), tt = (int32_t)(rec - (int64_t)l * T);
-    return __ldg(t.lent + off + l) * T + tt;
-  };
-  int64_t bp = 0, bq = 0;
-  bool staged = false;
-  if constexpr (!STRUCT) {
-    bp = __ldg(t.colptr + colof(offp, r0));
-    bq = __ldg(t.colptr + colof(offq, r0));
-    const int64_t ep = __ldg(t.colptr + colof(offp, rl) + 1), eq = __ldg(t.colptr + colof(offq, rl) + 1);
-    staged = (ep - bp) <= kFLCap && (eq - bq) <= kFLCap;
-    if (valid) {
-      const int32_t l = (int32_t)(r / T), tt = (int32_t)(r - (int64_t)l * T);
-      Ctx c{t, in, 0, tt, T, 0, 0, nullptr, 0, dv,
-            0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
-      if (staged) fz_line_cols<false>(c, l, sp, sq, bp, bq, rows, bad);
-      else fz_line_cols<false>(c, l, M, M, 0, 0, rows, bad);
-    }
-    if (staged) {
-      __syncthreads();
-      for (int64_t i = threadIdx.x; i < ep - bp; i += kFL) M[bp + i] = sp[i];
-      for (int64_t i = threadIdx.x; i < eq - bq; i += kFL) M[bq + i] = sq[i];
-    }
-  } else if (valid) {
-    const int32_t l = (int32_t)(r / T), tt = (int32_t)(r - (int64_t)l * T);
-    Ctx c{t, in, 0, tt, T, 0, 0, nullptr, 0, dv,
-          0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
-    fz_line_cols<true>(c, l, M, M, 0, 0, rows, bad);
-  }
+  const int32_t l = (int32_t)(r / T), tt = (int32_t)(r - (int64_t)l * T);
+  Ctx c{t, in, 0, tt, T, 0, 0, nullptr, 0, dv,
+        0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
+  fz_line_cols<STRUCT>(c, l, M, M, 0, 0, rows, bad);
 }
 
 template <bool STRUCT>
@@ -356,8 +327,9 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
                          int32_t* bad) {
   const OpfKktTab& t = K->opf->t;
   cudaStream_t s = K->stream;
-  launch_fz_bus(t, K->opf->bus_small.p, K->opf->n_bus_small, kSmallDeg, in, dv, M, rows, bad, s);
-  launch_fz_bus(t, K->opf->bus_large.p, K->opf->n_bus_large, t.maxdeg, in, dv, M, rows, bad, s);
+  for (int k = 0; k < kBusClasses; ++k)
+    launch_fz_bus(t, K->opf->bus_cls[k].p, K->opf->n_bus_cls[k], k < 4 ? k + 1 : t.maxdeg, k, in, dv,
+                  M, rows, bad, s);
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
     KTimer kt("k_fz_line", s);
@@ -407,14 +379,16 @@ bool opf_fused_verify(gn_kkt* K) {
     GN_CK(cudaMemcpyAsync(bp.data(), t.bl_ptr, sizeof(int32_t) * (t.N + 1), cudaMemcpyDeviceToHost,
                           K->stream));
     GN_CK(cudaStreamSynchronize(K->stream));
-    std::vector<int32_t> small, large;
-    for (int32_t n = 0; n < t.N; ++n) (bp[n + 1] - bp[n] <= kSmallDeg ? small : large).push_back(n);
-    K->opf->bus_small.upload(small.data(), small.size(), K->stream);
-    K->opf->bus_large.upload(large.data(), large.size(), K->stream);
-    if (small.empty()) K->opf->bus_small.alloc(1);
-    if (large.empty()) K->opf->bus_large.alloc(1);
-    K->opf->n_bus_small = static_cast<int32_t>(small.size());
-    K->opf->n_bus_large = static_cast<int32_t>(large.size());
+    std::vector<int32_t> cls[kBusClasses];
+    for (int32_t n = 0; n < t.N; ++n) {
+      const int32_t deg = bp[n + 1] - bp[n];
+      cls[deg <= 1 ? 0 : (deg <= 4 ? deg - 1 : 4)].push_back(n);  // isolated buses too (diagonal)
+    }
+    for (int k = 0; k < kBusClasses; ++k) {
+      K->opf->bus_cls[k].upload(cls[k].data(), cls[k].size(), K->stream);
+      if (cls[k].empty()) K->opf->bus_cls[k].alloc(1);
+      K->opf->n_bus_cls[k] = static_cast<int32_t>(cls[k].size());
+    }
   }
   cudaStream_t s = K->stream;
   DBuf<int32_t> rows, bad, diff;

@@ -26,6 +26,7 @@
 namespace gnb {
 
 constexpr int kBW3 = 4;  // warps per CTA
+constexpr int kSV = 11;  // shared doubles per (line, lane): Cs Sn cs sn vf vt w7 w8 d7 d8 d10
 
 // One warp per (bus n, 32 consecutive periods), lane = period.  The
 // trigonometric state (Cs, Sn, cs, sn) of each incident line is computed once
@@ -46,13 +47,14 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   const int32_t n = __ldg(buses + n64), T = t.T;
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
   const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
-  double* S = bsm + (size_t)warp * maxdeg * 6 * 32 + lane;
+  // per (line, lane): 6 state values + the 5 row inputs it contributes with
+  double* S = bsm + (size_t)warp * maxdeg * kSV * 32 + lane;
   // per-line warp-uniform data, filled by lanes 0..deg-1 in parallel
   struct LU {
     double G, B;
     int32_t l, fr;
   };
-  LU* U = reinterpret_cast<LU*>(bsm + (size_t)kBW3 * maxdeg * 6 * 32) + warp * maxdeg;
+  LU* U = reinterpret_cast<LU*>(bsm + (size_t)kBW3 * maxdeg * kSV * 32) + warp * maxdeg;
   if (lane < deg) {
     const int32_t e = __ldg(t.bl + b0 + lane);
     LU u;
@@ -67,24 +69,36 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
 
   if constexpr (!STRUCT) {
+    // every global input of the slot program is read exactly once, up front
+    // (independent loads in flight together); the slot loop reads only smem
     for (int i = 0; i < deg; ++i) {
       const LU u = U[i];
       const int32_t f = __ldg(t.lf + u.l), to = __ldg(t.lt + u.l);
+      const int64_t rl = (int64_t)u.l * T + tt;
+      const double w7 = in.w[t.flow_p0 + rl], w8 = in.w[t.flow_q0 + rl];
+      const double d7 = dv[t.flow_p0 + rl], d8 = dv[t.flow_q0 + rl], d10 = dv[t.ang0 + rl];
       const LineState s = line_state(u.G, u.B,
                                      in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
                                      in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
-      S[(i * 6 + 0) * 32] = s.Cs;
-      S[(i * 6 + 1) * 32] = s.Sn;
-      S[(i * 6 + 2) * 32] = s.cs;
-      S[(i * 6 + 3) * 32] = s.sn;
-      S[(i * 6 + 4) * 32] = s.vf;
-      S[(i * 6 + 5) * 32] = s.vt;
+      double* q = S + (size_t)i * kSV * 32;
+      q[0 * 32] = s.Cs;
+      q[1 * 32] = s.Sn;
+      q[2 * 32] = s.cs;
+      q[3 * 32] = s.sn;
+      q[4 * 32] = s.vf;
+      q[5 * 32] = s.vt;
+      q[6 * 32] = w7;
+      q[7 * 32] = w8;
+      q[8 * 32] = d7;
+      q[9 * 32] = d8;
+      q[10 * 32] = d10;
     }
   }
   // line k of the bus: state + the per-row inputs of this period
   struct LV {
     LineState s;
     double G, B;
+    double w7, w8, d7, d8, d10;
     int32_t l, fr;
   };
   auto lv = [&](int k) {
@@ -94,21 +108,26 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
     r.fr = u.fr;
     r.G = u.G;
     r.B = u.B;
-    r.s.Cs = S[(k * 6 + 0) * 32];
-    r.s.Sn = S[(k * 6 + 1) * 32];
-    r.s.cs = S[(k * 6 + 2) * 32];
-    r.s.sn = S[(k * 6 + 3) * 32];
-    r.s.vf = S[(k * 6 + 4) * 32];
-    r.s.vt = S[(k * 6 + 5) * 32];
+    const double* q = S + (size_t)k * kSV * 32;
+    r.s.Cs = q[0 * 32];
+    r.s.Sn = q[1 * 32];
+    r.s.cs = q[2 * 32];
+    r.s.sn = q[3 * 32];
+    r.s.vf = q[4 * 32];
+    r.s.vt = q[5 * 32];
     r.s.vfvt = r.s.vf * r.s.vt;
+    r.w7 = q[6 * 32];
+    r.w8 = q[7 * 32];
+    r.d7 = q[8 * 32];
+    r.d8 = q[9 * 32];
+    r.d10 = q[10 * 32];
     return r;
   };
-  auto rowp = [&](int32_t base0, int32_t l) { return base0 + (int64_t)l * T + tt; };
-  auto w7 = [&](const LV& r) { return in.w[rowp(t.flow_p0, r.l)]; };
-  auto w8 = [&](const LV& r) { return in.w[rowp(t.flow_q0, r.l)]; };
-  auto d7 = [&](const LV& r) { return dv[rowp(t.flow_p0, r.l)]; };
-  auto d8 = [&](const LV& r) { return dv[rowp(t.flow_q0, r.l)]; };
-  auto d10 = [&](const LV& r) { return dv[rowp(t.ang0, r.l)]; };
+  auto w7 = [](const LV& r) { return r.w7; };
+  auto w8 = [](const LV& r) { return r.w8; };
+  auto d7 = [](const LV& r) { return r.d7; };
+  auto d8 = [](const LV& r) { return r.d8; };
+  auto d10 = [](const LV& r) { return r.d10; };
   // fields of this bus's side (n = from -> v_f / th_f)
   auto JP = [&](const LV& r, bool other, bool theta) {
     const int f = theta ? ((r.fr ^ other) ? 3 : 4) : ((r.fr ^ other) ? 1 : 2);
@@ -197,20 +216,21 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
 }
 
 void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
-                   const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
+                   int klass, const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
                    cudaStream_t s) {
   if (n_buses <= 0) return;
   const int64_t warps = (int64_t)n_buses * t.tchunks;
   const unsigned blocks = (unsigned)((warps + kBW3 - 1) / kBW3);
   const int md = maxdeg > 0 ? maxdeg : 1;
-  const size_t smem = (size_t)kBW3 * md * (6 * 32 * sizeof(double) + 24);
+  const size_t smem = (size_t)kBW3 * md * (kSV * 32 * sizeof(double) + 24);
   static bool attr = false;
   if (!attr) {
     GN_CK(cudaFuncSetAttribute(k_fz_bus3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  KTimer kt(maxdeg > kSmallDeg ? "k_fz_bus3<large>" : "k_fz_bus3<small>", s);
+  static const char* names[] = {"k_fz_bus3<d1>", "k_fz_bus3<d2>", "k_fz_bus3<d3>", "k_fz_bus3<d4>"};
+  KTimer kt(klass < 4 ? names[klass] : "k_fz_bus3<large>", s);
   if (rows)
     k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else

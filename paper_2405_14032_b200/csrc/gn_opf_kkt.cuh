@@ -52,10 +52,12 @@ struct FIn {
 
 // Bus-column kernel (v(n), th(n) columns): one warp per (bus, period chunk);
 // lanes = (32/P periods) x (P incident-line slots), P = next pow2 >= degree.
+// klass 0..3: buses of klass+1 lines (klass 0: at most one), shared memory sized to
+// the degree; klass 4: every bus with more lines (maxdeg = the network's maximum).
 void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
-                   const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
-                   cudaStream_t s);
-constexpr int kSmallDeg = 4;  // buses with <= kSmallDeg lines run in the low-smem launch
+                   int klass, const FIn& in, const double* dv, double* M, int32_t* rows,
+                   int32_t* bad, cudaStream_t s);
+constexpr int kBusClasses = 5;
 
 struct OpfKkt {
   bool ready = false;
@@ -66,8 +68,8 @@ struct OpfKkt {
   bool fused_ready = false;
   DBuf<int32_t> bprog_ptr;
   DBuf<unsigned long long> bprog;
-  DBuf<int32_t> bus_small, bus_large;  // buses by degree class (bus-column kernel)
-  int32_t n_bus_small = 0, n_bus_large = 0;
+  DBuf<int32_t> bus_cls[kBusClasses];  // buses by degree class (bus-column kernel)
+  int32_t n_bus_cls[kBusClasses] = {};
 };
 
 void count_diff(const int32_t* a, const int32_t* b, int64_t n, int32_t* diff, cudaStream_t s);
