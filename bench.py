@@ -178,11 +178,11 @@ def kernel_bytes(s, kkt, nlp, net, T):
     # bus-column kernel, per degree class: its M slots, x(v, th) + Sx(v, th) of its
     # buses, and its share (half per line end) of the line inputs
     # w(flow_p, flow_q), d(flow_p, flow_q, angle)
-    cls = np.where(deg <= 1, 0, np.minimum(deg, 5) - 1)
-    m_cls = [int(lens[vth & (cls[np.clip(ent, 0, N - 1)] == k)].sum()) for k in range(5)]
+    cls = np.where(deg <= 1, 0, np.minimum(deg, 7) - 1)
+    m_cls = [int(lens[vth & (cls[np.clip(ent, 0, N - 1)] == k)].sum()) for k in range(7)]
     bus_cls = {f"k_fz_bus3<{nm}>": m_cls[k] + 4 * int((cls == k).sum()) * T
                + 2.5 * int(deg[cls == k].sum()) * T
-               for k, nm in enumerate(["d1", "d2", "d3", "d4", "large"])}
+               for k, nm in enumerate(["d1", "d2", "d3", "d4", "d5", "d6", "large"])}
     b = {
         "k_gen<F>": G * T, "k_gen<GRAD>": 2 * G * T,
         "k_bus<G>": 2 * N * T + 2 * L * T + 2 * G * T + 2 * D * T,

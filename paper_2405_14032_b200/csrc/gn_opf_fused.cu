@@ -16,6 +16,8 @@
 // The warp owns the columns v(n), th(n), p(l)/q(l) of the lines whose smaller
 // terminal is n, and pg(g)/qg(g) of the generators at n.  Each incident line's
 // trigonometric state is computed once per lane and kept in shared memory.
+#include <cstdlib>
+
 #include "gn_opf_kkt.cuh"
 #include "gn_opf_math.cuh"
 
@@ -68,88 +70,6 @@ struct Ctx {
     return k < 0 ? -1 : k * T + tt;
   }
 };
-
-// p(l) and q(l) columns of line l at period c.tt (thread per (l, t)).
-template <bool STRUCT>
-__device__ void fz_line_cols(const Ctx& c, int32_t l, double* Mp, double* Mq, int64_t basep,
-                             int64_t baseq, int32_t* rows, int32_t* bad) {
-  const OpfKktTab& t = c.t;
-  const FIn& in = c.in;
-  const int32_t T = c.T, tt = c.tt;
-  auto check = [&](const FOut<STRUCT>& o, int32_t cc) {
-    if (STRUCT && o.base + o.j != __ldg(t.colptr + cc + 1)) atomicOr(bad, 1);
-  };
-  {
-    const int32_t f = __ldg(t.lf + l), to = __ldg(t.lt + l);
-    const int32_t blo = min(f, to), bhi = max(f, to);
-    const int32_t k = __ldg(t.l_therm + l);
-    const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-    const int64_t r = (int64_t)l * T + tt;
-    const double sgn_lo = (blo == to) ? 1.0 : -1.0, sgn_hi = (bhi == to) ? 1.0 : -1.0;
-    LineState s{};
-    if constexpr (!STRUCT)
-      s = line_state(G, B, in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
-                     in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
-#pragma unroll
-    for (int Q = 0; Q < 2; ++Q) {
-      const int32_t cc = c.col(Q ? c.off_q : c.off_p, l);
-      FOut<STRUCT> o{Q ? Mq : Mp, rows, __ldg(t.colptr + cc) - (Q ? baseq : basep), 0};
-      const int32_t bal0 = Q ? t.bal_q0 : t.bal_p0, flow0 = Q ? t.flow_q0 : t.flow_p0;
-      double jt = 0.0, jp = 0.0;
-      if (k >= 0) {
-        jt = j_thermal(in.x[(Q ? t.q0 : t.p0) + r]);
-        jp = j_thermal(in.x[t.p0 + r]);
-      }
-      {  // diagonal: thermal H (2w) then pairs bal(lo), bal(hi), flow, thermal, diag
-        double acc = 0.0;
-        if constexpr (!STRUCT) {
-          if (k >= 0) acc += h_thermal_diag(c.wt(t.therm0 + k * T + tt));
-          acc += pair_term(c.d(bal0 + blo * T + tt), sgn_lo, sgn_lo);
-          acc += pair_term(c.d(bal0 + bhi * T + tt), sgn_hi, sgn_hi);
-          acc += pair_term(c.d(flow0 + (int32_t)r), 1.0, 1.0);
-          if (k >= 0) acc += pair_term(c.d(t.therm0 + k * T + tt), jt, jt);
-          acc += in.dw + in.sx[cc];
-        }
-        o.put(acc, cc);
-      }
-      // flows l' > l sharing a bus
-      const int32_t a0 = __ldg(t.lnb_ptr + l), a1 = __ldg(t.lnb_ptr + l + 1);
-      for (int32_t a = a0; a < a1; ++a) {
-        const int32_t code = __ldg(t.lnb + a), l2 = code >> 2, bits = code & 3;
-        double acc = 0.0;
-        if constexpr (!STRUCT) {
-          const int32_t to2 = __ldg(t.lt + l2);
-          if (bits & 1) acc += pair_term(c.d(bal0 + blo * T + tt), blo == to2 ? 1.0 : -1.0, sgn_lo);
-          if (bits & 2) acc += pair_term(c.d(bal0 + bhi * T + tt), bhi == to2 ? 1.0 : -1.0, sgn_hi);
-        }
-        o.put(acc, c.col(Q ? c.off_q : c.off_p, l2));
-      }
-      if (!Q && k >= 0) {  // (q(l), p(l)): thermal pair (2q)(2p)
-        double acc = 0.0;
-        if constexpr (!STRUCT) {
-          acc += pair_term(c.d(t.therm0 + k * T + tt), j_thermal(in.x[t.q0 + r]), jp);
-        }
-        o.put(acc, c.col(c.off_q, l));
-      }
-#pragma unroll
-      for (int blk = 0; blk < 2; ++blk)
-#pragma unroll
-        for (int sdx = 0; sdx < 2; ++sdx) {
-          const int32_t b = sdx == 0 ? blo : bhi;
-          const int field = blk == 0 ? (b == f ? 1 : 2) : (b == f ? 3 : 4);
-          const int32_t cr = c.col(blk == 0 ? c.off_v : c.off_th, b);
-          if (cr < 0) continue;
-          double acc = 0.0;
-          if constexpr (!STRUCT) {
-            const double ja = Q ? j_flow_q(s, G, B, field) : j_flow_p(s, G, B, field);
-            acc += pair_term(c.d(flow0 + (int32_t)r), ja, 1.0);
-          }
-          o.put(acc, cr);
-        }
-      if (STRUCT && o.base + (Q ? baseq : basep) + o.j != __ldg(t.colptr + cc + 1)) atomicOr(bad, 1);
-    }
-  }
-}
 
 // pg(g) and qg(g) columns of generator g at period c.tt (thread per (g, t)).
 template <bool STRUCT>
@@ -225,21 +145,153 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
   if (r < m) dv[r] = dvec(ss[r], dw, dc);
 }
 
-// p(l)/q(l) columns, one thread per (l, t).  (Staging the CTA's contiguous span
-// of M through shared memory was measured slower: the kernel is latency-bound
-// on its dependent index loads, not on write coalescing.)
-constexpr int kFL = 256;
+// p(l) and q(l) columns of line l, one warp per (l, 32 consecutive periods),
+// lane = period.
+//
+//   rows of p(l): p(l) | p(l') for l' > l sharing a bus | q(l) if thermal | v(lo) v(hi) th(lo) th(hi)
+//   rows of q(l): q(l) | q(l') ...                                         | v(lo) v(hi) th(lo) th(hi)
+//
+// (lo, hi = min / max terminal; v/th rows only where free.)  Every input comes
+// from one level of per-line descriptors (independent loads, restrict-qualified
+// so none waits behind an M store).  The columns of consecutive periods are
+// consecutive in M, so a warp's p (then q) columns form one contiguous span:
+// lanes stage their column in shared memory ([slot][lane], conflict-free) and
+// the warp writes the span back coalesced.  Direct per-lane writes would make
+// every 8-byte store its own L2 sector write (4x the write transactions, and
+// partial-sector fills from HBM).
+constexpr int kFLW = 8;     // warps per CTA
+constexpr int kFLCap = 16;  // staged slots per column (longer columns are written in place)
 template <bool STRUCT>
-__global__ void __launch_bounds__(kFL) k_fz_line(OpfKktTab t, FIn in, const double* __restrict__ dv,
-                                                 double* __restrict__ M, int32_t* __restrict__ rows,
-                                                 int32_t* __restrict__ bad) {
-  const int64_t r = (int64_t)blockIdx.x * kFL + threadIdx.x;
-  if (r >= (int64_t)t.L * t.T) return;
+__global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, const double* __restrict__ x,
+                                                      const double* __restrict__ w,
+                                                      const double* __restrict__ sx, double dw,
+                                                      const double* __restrict__ dv,
+                                                      double* __restrict__ M,
+                                                      int32_t* __restrict__ rows,
+                                                      int32_t* __restrict__ bad) {
+  __shared__ double stg_all[STRUCT ? 1 : kFLW * kFLCap * 33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t T = t.T;
-  const int32_t l = (int32_t)(r / T), tt = (int32_t)(r - (int64_t)l * T);
-  Ctx c{t, in, 0, tt, T, 0, 0, nullptr, 0, dv,
-        0, t.G, 2 * t.G, 2 * t.G + t.L, 2 * t.G + 2 * t.L, 2 * t.G + 2 * t.L + t.N};
-  fz_line_cols<STRUCT>(c, l, M, M, 0, 0, rows, bad);
+  const int64_t wg = (int64_t)blockIdx.x * kFLW + warp;
+  const int32_t l = (int32_t)(wg / t.tchunks);
+  if (l >= t.L) return;  // warp-uniform
+  const int32_t c0 = (int32_t)(wg - (int64_t)l * t.tchunks) * 32;
+  const int32_t tt = c0 + lane, nt = min(32, T - c0);
+  const bool valid = lane < nt;
+  const int4 d0 = __ldg(t.ldesc0 + l), d1 = __ldg(t.ldesc1 + l);
+  const int32_t f = d0.x, to = d0.y, k = d0.z, fl = d0.w;
+  const int32_t blo = min(f, to), bhi = max(f, to);
+  const int32_t nl = d1.y - d1.x, nvt = __popc(fl & 15);
+  const int32_t lenp = 1 + nl + (k >= 0 ? 1 : 0) + nvt, lenq = 1 + nl + nvt;
+  const int32_t ccp = d1.z * T + tt, ccq = d1.w * T + tt;
+  const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
+  if constexpr (STRUCT) {
+    if (!valid) return;
+    const int64_t posp = __ldg(t.colptr + ccp), posq = __ldg(t.colptr + ccq);
+    int32_t jp = 0, jq = 0;
+    rows[posp + jp++] = ccp;
+    rows[posq + jq++] = ccq;
+    for (int32_t a = d1.x; a < d1.y; ++a) {
+      const int32_t l2 = __ldg(t.lnbx + a) >> 4;
+      rows[posp + jp++] = __ldg(t.lent + 2 * t.G + l2) * T + tt;
+      rows[posq + jq++] = __ldg(t.lent + 2 * t.G + t.L + l2) * T + tt;
+    }
+    if (k >= 0) rows[posp + jp++] = ccq;
+    for (int i = 0; i < 4; ++i) {
+      if (!(fl & (1 << i))) continue;
+      const int32_t b = (i & 1) ? bhi : blo;
+      const int32_t cr = __ldg(t.lent + ((i & 2) ? off_th : off_v) + b) * T + tt;
+      rows[posp + jp++] = cr;
+      rows[posq + jq++] = cr;
+    }
+    if (jp != lenp || jq != lenq || posp + jp != __ldg(t.colptr + ccp + 1) ||
+        posq + jq != __ldg(t.colptr + ccq + 1))
+      atomicOr(bad, 1);
+    return;
+  }
+  double* stg = stg_all + warp * (kFLCap * 33);
+  // ---- loads (every lane; invalid lanes clamp to the chunk's first period)
+  const int32_t ts = valid ? tt : c0, r = l * T + ts;
+  const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
+  const double vf = x[t.v0 + f * T + ts], vt = x[t.v0 + to * T + ts];
+  const double thf = x[t.th0 + f * T + ts], tht = x[t.th0 + to * T + ts];
+  const double xp = x[t.p0 + r], xq = x[t.q0 + r];
+  const double dfp = dv[t.flow_p0 + r], dfq = dv[t.flow_q0 + r];
+  const double dbp_lo = dv[t.bal_p0 + blo * T + ts], dbp_hi = dv[t.bal_p0 + bhi * T + ts];
+  const double dbq_lo = dv[t.bal_q0 + blo * T + ts], dbq_hi = dv[t.bal_q0 + bhi * T + ts];
+  const int32_t cps = d1.z * T + ts, cqs = d1.w * T + ts;
+  const double sxp = sx[cps], sxq = sx[cqs];
+  double wth = 0.0, dth = 0.0;
+  if (k >= 0) {
+    wth = w[t.therm0 + k * T + ts];
+    dth = dv[t.therm0 + k * T + ts];
+  }
+  const int64_t basep = __ldg(t.colptr + d1.z * T + c0), baseq = __ldg(t.colptr + d1.w * T + c0);
+  const bool stp = lenp <= kFLCap, stq = lenq <= kFLCap;  // warp-uniform
+  const LineState s = line_state(G, B, vf, vt, thf, tht);
+  const double jtp = j_thermal(xp), jtq = j_thermal(xq);
+  // ---- values, slot by slot (column p into the stage, column q kept in registers
+  // order-free: q is written after p's span has been flushed)
+  auto flush = [&](int64_t base, int32_t len) {
+    __syncwarp();
+    const int32_t q32 = 32 / len, r32 = 32 - q32 * len;
+    int32_t tq = lane / len, rj = lane - tq * len;
+    for (int32_t e = lane; e < nt * len; e += 32) {
+      M[base + e] = stg[rj * 33 + tq];
+      tq += q32;
+      rj += r32;
+      if (rj >= len) {
+        rj -= len;
+        ++tq;
+      }
+    }
+    __syncwarp();
+  };
+  for (int Q = 0; Q < 2; ++Q) {
+    const bool st = Q ? stq : stp;
+    const int64_t pos = st ? 0 : (valid ? (int64_t)__ldg(t.colptr + (Q ? cqs : cps)) : 0);
+    auto put = [&](int32_t j, double v) {
+      if (st) stg[j * 33 + lane] = v;
+      else if (valid) M[pos + j] = v;
+    };
+    const double dlo = Q ? dbq_lo : dbp_lo, dhi = Q ? dbq_hi : dbp_hi, dfl = Q ? dfq : dfp;
+    const double jt = Q ? jtq : jtp;
+    {  // diagonal: thermal H (2w) then pairs bal(lo), bal(hi), flow, thermal, dw + Sx
+      const double sgn_lo = (fl & 16) ? 1.0 : -1.0, sgn_hi = (fl & 32) ? 1.0 : -1.0;
+      double acc = 0.0;
+      if (k >= 0) acc += h_thermal_diag(wth);
+      acc += pair_term(dlo, sgn_lo, sgn_lo);
+      acc += pair_term(dhi, sgn_hi, sgn_hi);
+      acc += pair_term(dfl, 1.0, 1.0);
+      if (k >= 0) acc += pair_term(dth, jt, jt);
+      acc += dw + (Q ? sxq : sxp);
+      put(0, acc);
+    }
+    for (int32_t a = 0; a < nl; ++a) {  // flows l' > l sharing a bus: balance-row pairs
+      const int32_t code = __ldg(t.lnbx + d1.x + a);
+      const double sgn_lo = (fl & 16) ? 1.0 : -1.0, sgn_hi = (fl & 32) ? 1.0 : -1.0;
+      double acc = 0.0;
+      if (code & 1) acc += pair_term(dlo, (code & 4) ? 1.0 : -1.0, sgn_lo);
+      if (code & 2) acc += pair_term(dhi, (code & 8) ? 1.0 : -1.0, sgn_hi);
+      put(1 + a, acc);
+    }
+    int32_t j = 1 + nl;
+    if (!Q && k >= 0) {  // (q(l), p(l)): thermal pair (2q)(2p)
+      double acc = 0.0;
+      acc += pair_term(dth, jtq, jtp);
+      put(j++, acc);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // v(lo) v(hi) th(lo) th(hi): flow-row pairs
+      if (!(fl & (1 << i))) continue;
+      const int32_t b = (i & 1) ? bhi : blo;
+      const int field = (i & 2) ? (b == f ? 3 : 4) : (b == f ? 1 : 2);
+      double acc = 0.0;
+      acc += pair_term(dfl, Q ? j_flow_q(s, G, B, field) : j_flow_p(s, G, B, field), 1.0);
+      put(j++, acc);
+    }
+    if (st) flush(Q ? baseq : basep, Q ? lenq : lenp);
+  }
 }
 
 template <bool STRUCT>
@@ -328,12 +380,14 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   const OpfKktTab& t = K->opf->t;
   cudaStream_t s = K->stream;
   for (int k = 0; k < kBusClasses; ++k)
-    launch_fz_bus(t, K->opf->bus_cls[k].p, K->opf->n_bus_cls[k], k < 4 ? k + 1 : t.maxdeg, k, in, dv,
+    launch_fz_bus(t, K->opf->bus_cls[k].p, K->opf->n_bus_cls[k], k < kBusClasses - 1 ? k + 1 : t.maxdeg, k, in, dv,
                   M, rows, bad, s);
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
     KTimer kt("k_fz_line", s);
-    k_fz_line<STRUCT><<<(unsigned)((nl + kFL - 1) / kFL), kFL, 0, s>>>(t, in, dv, M, rows, bad);
+    const int64_t warps = (int64_t)t.L * t.tchunks;
+    k_fz_line<STRUCT><<<(unsigned)((warps + kFLW - 1) / kFLW), kFLW * 32, 0, s>>>(
+        t, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
     count_launch();
   }
   if (ng > 0) {
@@ -382,7 +436,7 @@ bool opf_fused_verify(gn_kkt* K) {
     std::vector<int32_t> cls[kBusClasses];
     for (int32_t n = 0; n < t.N; ++n) {
       const int32_t deg = bp[n + 1] - bp[n];
-      cls[deg <= 1 ? 0 : (deg <= 4 ? deg - 1 : 4)].push_back(n);  // isolated buses too (diagonal)
+      cls[deg <= 1 ? 0 : std::min(deg, kBusClasses) - 1].push_back(n);  // isolated buses too (diagonal)
     }
     for (int k = 0; k < kBusClasses; ++k) {
       K->opf->bus_cls[k].upload(cls[k].data(), cls[k].size(), K->stream);

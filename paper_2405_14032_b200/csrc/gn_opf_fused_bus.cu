@@ -229,8 +229,10 @@ void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, in
     GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  static const char* names[] = {"k_fz_bus3<d1>", "k_fz_bus3<d2>", "k_fz_bus3<d3>", "k_fz_bus3<d4>"};
-  KTimer kt(klass < 4 ? names[klass] : "k_fz_bus3<large>", s);
+  static const char* names[kBusClasses] = {"k_fz_bus3<d1>", "k_fz_bus3<d2>", "k_fz_bus3<d3>",
+                                           "k_fz_bus3<d4>", "k_fz_bus3<d5>", "k_fz_bus3<d6>",
+                                           "k_fz_bus3<large>"};
+  KTimer kt(names[klass], s);
   if (rows)
     k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else

@@ -703,7 +703,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
     apos[2 * l + 1] = to == lo ? a_lo : a_hi;
   }
   // line neighbours l' > l sharing a bus; bits: 1 = shares min(f,to), 2 = shares max
-  std::vector<int32_t> lnb_ptr(L + 1, 0), lnb;
+  std::vector<int32_t> lnb_ptr(L + 1, 0), lnb, lnbx;
   for (int32_t l = 0; l < L; ++l) {
     const int32_t f = c->line_from[l], to = c->line_to[l];
     const int32_t lo = std::min(f, to), hi = std::max(f, to);
@@ -720,8 +720,21 @@ bool opf_kkt_prepare(gn_kkt* K) {
       int32_t bits = 0, l2 = v[i].first;
       while (i < v.size() && v[i].first == l2) bits |= v[i++].second;
       lnb.push_back((l2 << 2) | bits);
+      // fused line kernel: + the balance-row signs of l2 at the shared buses
+      const int32_t to2 = c->line_to[l2];
+      lnbx.push_back((l2 << 4) | bits | (lo == to2 ? 4 : 0) | (hi == to2 ? 8 : 0));
     }
     lnb_ptr[l + 1] = static_cast<int32_t>(lnb.size());
+  }
+  // per-line descriptors of the fused line kernel (one level of independent loads)
+  std::vector<int4> ldesc0(L), ldesc1(L);
+  for (int32_t l = 0; l < L; ++l) {
+    const int32_t f = c->line_from[l], to = c->line_to[l];
+    const int32_t lo = std::min(f, to), hi = std::max(f, to);
+    const int32_t flags = (vfree(lo) ? 1 : 0) | (vfree(hi) ? 2 : 0) | (tfree(lo) ? 4 : 0) |
+                          (tfree(hi) ? 8 : 0) | (lo == to ? 16 : 0) | (hi == to ? 32 : 0);
+    ldesc0[l] = make_int4(f, to, l_therm[l], flags);
+    ldesc1[l] = make_int4(lnb_ptr[l], lnb_ptr[l + 1], lent[offs[C_P] + l], lent[offs[C_Q] + l]);
   }
   up(X->lent, lent, s); up(X->items, items, s);
   up(X->lf, c->line_from, s); up(X->lt, c->line_to, s); up(X->l_therm, l_therm, s);
@@ -729,14 +742,16 @@ bool opf_kkt_prepare(gn_kkt* K) {
   up(X->gbus, c->gen_bus, s); up(X->ppos, ppos, s); up(X->qpos, qpos, s); up(X->g_ramp, g_ramp, s);
   up(X->ngp, ngp, s); up(X->ngq, ngq, s); up(X->bl_ptr, bl_ptr, s); up(X->bl, bl, s);
   up(X->bg_ptr, bg_ptr, s); up(X->bg, bg, s); up(X->nb_ptr, nb_ptr, s); up(X->nb, nb, s); up(X->nb_inc, nb_inc, s);
-  up(X->lnb_ptr, lnb_ptr, s); up(X->lnb, lnb, s);
+  up(X->lnb_ptr, lnb_ptr, s); up(X->lnb, lnb, s); up(X->lnbx, lnbx, s);
+  up(X->ldesc0, ldesc0, s); up(X->ldesc1, ldesc1, s);
   up(X->bprog_ptr, bprog_ptr, s); up(X->bprog, bprog, s);
   t.lent = X->lent.p; t.items = X->items.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
   t.fpos = X->fpos.p; t.apos = X->apos.p; t.lidx_to = X->lidx_to.p; t.lidx_from = X->lidx_from.p;
   t.gbus = X->gbus.p; t.ppos = X->ppos.p; t.qpos = X->qpos.p; t.g_ramp = X->g_ramp.p;
   t.ngp = X->ngp.p; t.ngq = X->ngq.p; t.bl_ptr = X->bl_ptr.p; t.bl = X->bl.p;
   t.bg_ptr = X->bg_ptr.p; t.bg = X->bg.p; t.nb_ptr = X->nb_ptr.p; t.nb = X->nb.p; t.nb_inc = X->nb_inc.p;
-  t.lnb_ptr = X->lnb_ptr.p; t.lnb = X->lnb.p;
+  t.lnb_ptr = X->lnb_ptr.p; t.lnb = X->lnb.p; t.lnbx = X->lnbx.p;
+  t.ldesc0 = X->ldesc0.p; t.ldesc1 = X->ldesc1.p;
   t.bprog_ptr = X->bprog_ptr.p; t.bprog = X->bprog.p;
   t.rowptr = K->A.ptr.p; t.colptr = K->M.ptr.p;
   GN_CK(cudaStreamSynchronize(s));

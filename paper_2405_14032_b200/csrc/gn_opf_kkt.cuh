@@ -36,6 +36,11 @@ struct OpfKktTab {
   int32_t maxdeg;                       // max incident lines of a bus
   int32_t s_lo, R, prev, next;          // ramp steps of a period shard (OpfDims)
   int32_t n_owned;                      // lifted columns owned (next ghosts follow)
+  // fused line kernel descriptors
+  const int4* ldesc0;                   // [L] (f, t, thermal slot or -1, flags: v/th free at
+                                        //  min/max terminal bits 0-3, min==t bit 4, max==t bit 5)
+  const int4* ldesc1;                   // [L] (lnb begin, lnb end, lifted p rank, lifted q rank)
+  const int32_t* lnbx;                  // [lnb] l' << 4 | t(l') == max << 3 | t(l') == min << 2 | bits
   const int32_t* bprog_ptr;             // [N+1] per-bus slot programs of the v(n)/th(n) columns
   const unsigned long long* bprog;      // (row entity << 35 | type << 32 | lane mask)
 };
@@ -52,12 +57,12 @@ struct FIn {
 
 // Bus-column kernel (v(n), th(n) columns): one warp per (bus, period chunk);
 // lanes = (32/P periods) x (P incident-line slots), P = next pow2 >= degree.
-// klass 0..3: buses of klass+1 lines (klass 0: at most one), shared memory sized to
-// the degree; klass 4: every bus with more lines (maxdeg = the network's maximum).
+// klass 0..5: buses of klass+1 lines (klass 0: at most one), shared memory sized to
+// the degree; klass 6: every bus with more lines (maxdeg = the network's maximum).
 void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows,
                    int32_t* bad, cudaStream_t s);
-constexpr int kBusClasses = 5;
+constexpr int kBusClasses = 7;
 
 struct OpfKkt {
   bool ready = false;
@@ -66,6 +71,8 @@ struct OpfKkt {
       ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb, nb_inc;
   DBuf<int8_t> fpos, apos;
   bool fused_ready = false;
+  DBuf<int32_t> lnbx;
+  DBuf<int4> ldesc0, ldesc1;
   DBuf<int32_t> bprog_ptr;
   DBuf<unsigned long long> bprog;
   DBuf<int32_t> bus_cls[kBusClasses];  // buses by degree class (bus-column kernel)
