@@ -426,7 +426,7 @@ void opf_set_jacobian_fused(gn_kkt* K, const double* x) {
 // Structure check of the fused enumeration (row index of every slot, column lengths).
 bool opf_fused_verify(gn_kkt* K) {
   const OpfKktTab& t = K->opf->t;
-  if (t.maxdeg > 32) return false;  // bus-column kernel holds one line per lane
+  if (!fz_bus_fits(t.maxdeg)) return false;  // one line per lane, one warp's shared memory
   K->dvals.alloc(static_cast<size_t>(K->m) + 1);
   {  // bus lists of the bus-column kernel, by degree class (shared-memory footprint)
     std::vector<int32_t> bp(t.N + 1);

@@ -26,7 +26,8 @@
 namespace gnb {
 
 constexpr int kBW3 = 4;  // warps per CTA
-constexpr int kSV = 11;  // shared doubles per (line, lane): Cs Sn cs sn vf vt w7 w8 d7 d8 d10
+constexpr int kSV = 11;
+constexpr int kBusSmemMax = 200 * 1024;  // dynamic shared memory cap of the bus kernel  // shared doubles per (line, lane): Cs Sn cs sn vf vt w7 w8 d7 d8 d10
 
 // One warp per (bus n, 32 consecutive periods), lane = period.  The
 // trigonometric state (Cs, Sn, cs, sn) of each incident line is computed once
@@ -40,8 +41,9 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
                                                        int32_t* __restrict__ rows,
                                                        int32_t* __restrict__ bad) {
   extern __shared__ double bsm[];
+  const int nw = blockDim.x >> 5;  // warps per CTA (fewer for very-high-degree classes)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kBW3 + warp;
+  const int64_t w = (int64_t)blockIdx.x * nw + warp;
   const int64_t n64 = w / t.tchunks;
   if (n64 >= n_buses) return;  // warp-uniform
   const int32_t n = __ldg(buses + n64), T = t.T;
@@ -54,7 +56,7 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
     double G, B;
     int32_t l, fr;
   };
-  LU* U = reinterpret_cast<LU*>(bsm + (size_t)kBW3 * maxdeg * kSV * 32) + warp * maxdeg;
+  LU* U = reinterpret_cast<LU*>(bsm + (size_t)nw * maxdeg * kSV * 32) + warp * maxdeg;
   if (lane < deg) {
     const int32_t e = __ldg(t.bl + b0 + lane);
     LU u;
@@ -152,8 +154,13 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
     const LV r = lv(__ffs(mm) - 1);                \
     acc += (expr);                                 \
   }
+  // loop-invariant / next-iteration global loads issued ahead of their use
+  const double sxv = (!STRUCT && cv >= 0) ? in.sx[cv] : 0.0;
+  const double sxt = (!STRUCT && ct >= 0) ? in.sx[ct] : 0.0;
+  unsigned long long code_next = p0 < p1 ? __ldg(t.bprog + p0) : 0ull;
   for (int32_t q = p0; q < p1; ++q) {
-    const unsigned long long code = __ldg(t.bprog + q);
+    const unsigned long long code = code_next;
+    if (q + 1 < p1) code_next = __ldg(t.bprog + q + 1);
     const uint32_t mask = (uint32_t)code;
     const int type = (int)((code >> 32) & 7);
     const int32_t rent = (int32_t)(code >> 35);
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
           PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 5 : 9));
           PASS(pair_term(d7(r), JP(r, false, false), JP(r, false, false)));
           PASS(pair_term(d8(r), JQ(r, false, false), JQ(r, false, false)));
-          acc += in.dw + in.sx[cv];
+          acc += in.dw + sxv;
           break;
         case 1:  // (v_o, v_n), o > n
           PASS(h_flow_p(r.s, r.G, w7(r), 6));
@@ -191,7 +198,7 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
           PASS(pair_term(d7(r), JP(r, false, true), JP(r, false, true)));
           PASS(pair_term(d8(r), JQ(r, false, true), JQ(r, false, true)));
           PASS(pair_term(d10(r), r.fr ? 1.0 : -1.0, r.fr ? 1.0 : -1.0));
-          acc += in.dw + in.sx[ct];
+          acc += in.dw + sxt;
           break;
         default:  // (th_o, th_n), o > n
           PASS(h_flow_p(r.s, r.G, w7(r), 13));
@@ -215,18 +222,26 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   }
 }
 
+bool fz_bus_fits(int32_t maxdeg) {
+  const size_t md = maxdeg > 0 ? maxdeg : 1;
+  return maxdeg <= 32 && md * (kSV * 32 * sizeof(double) + 24) <= kBusSmemMax;
+}
+
 void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
                    cudaStream_t s) {
   if (n_buses <= 0) return;
   const int64_t warps = (int64_t)n_buses * t.tchunks;
-  const unsigned blocks = (unsigned)((warps + kBW3 - 1) / kBW3);
   const int md = maxdeg > 0 ? maxdeg : 1;
-  const size_t smem = (size_t)kBW3 * md * (kSV * 32 * sizeof(double) + 24);
+  int nw = kBW3;
+  while (nw > 1 && (size_t)nw * md * (kSV * 32 * sizeof(double) + 24) > kBusSmemMax) nw >>= 1;
+  const size_t smem = (size_t)nw * md * (kSV * 32 * sizeof(double) + 24);
+  if (smem > kBusSmemMax) throw Error(GN_ERR_UNSUPPORTED, "bus degree too large for the fused kernel");
+  const unsigned blocks = (unsigned)((warps + nw - 1) / nw);
   static bool attr = false;
   if (!attr) {
-    GN_CK(cudaFuncSetAttribute(k_fz_bus3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    GN_CK(cudaFuncSetAttribute(k_fz_bus3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBusSmemMax));
+    GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBusSmemMax));
     attr = true;
   }
   static const char* names[kBusClasses] = {"k_fz_bus3<d1>", "k_fz_bus3<d2>", "k_fz_bus3<d3>",
@@ -234,9 +249,9 @@ void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, in
                                            "k_fz_bus3<large>"};
   KTimer kt(names[klass], s);
   if (rows)
-    k_fz_bus3<true><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
+    k_fz_bus3<true><<<blocks, nw * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else
-    k_fz_bus3<false><<<blocks, kBW3 * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
+    k_fz_bus3<false><<<blocks, nw * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   count_launch();
 }
 

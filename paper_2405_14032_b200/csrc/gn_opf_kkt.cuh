@@ -63,6 +63,7 @@ void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, in
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows,
                    int32_t* bad, cudaStream_t s);
 constexpr int kBusClasses = 7;
+bool fz_bus_fits(int32_t maxdeg);  // one warp's shared memory fits (else: no fused path)
 
 struct OpfKkt {
   bool ready = false;
