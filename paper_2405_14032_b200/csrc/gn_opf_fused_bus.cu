@@ -158,6 +158,43 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   const double sxv = (!STRUCT && cv >= 0) ? in.sx[cv] : 0.0;
   const double sxt = (!STRUCT && ct >= 0) ? in.sx[ct] : 0.0;
   unsigned long long code_next = p0 < p1 ? __ldg(t.bprog + p0) : 0ull;
+  // The three own slots (v,v) (th,v) (th,th) run over every incident line with
+  // the same pass structure: one fused sweep, each line's data read once per pass.
+  double own0 = 0.0, own2 = 0.0, own4 = 0.0;
+  if constexpr (!STRUCT) {
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      own0 += h_flow_p(r.s, r.G, r.w7, r.fr ? 5 : 9);
+      own2 += h_flow_p(r.s, r.G, r.w7, r.fr ? 7 : 11);
+      own4 += h_flow_p(r.s, r.G, r.w7, r.fr ? 12 : 14);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      own0 += h_flow_q(r.s, r.B, r.w8, r.fr ? 5 : 9);
+      own2 += h_flow_q(r.s, r.B, r.w8, r.fr ? 7 : 11);
+      own4 += h_flow_q(r.s, r.B, r.w8, r.fr ? 12 : 14);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      const double jv_ = JP(r, false, false), jt_ = JP(r, false, true);
+      own0 += pair_term(r.d7, jv_, jv_);
+      own2 += pair_term(r.d7, jt_, jv_);
+      own4 += pair_term(r.d7, jt_, jt_);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      const double jv_ = JQ(r, false, false), jt_ = JQ(r, false, true);
+      own0 += pair_term(r.d8, jv_, jv_);
+      own2 += pair_term(r.d8, jt_, jv_);
+      own4 += pair_term(r.d8, jt_, jt_);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      own4 += pair_term(r.d10, r.fr ? 1.0 : -1.0, r.fr ? 1.0 : -1.0);
+    }
+    own0 += in.dw + sxv;
+    own4 += in.dw + sxt;
+  }
   for (int32_t q = p0; q < p1; ++q) {
     const unsigned long long code = code_next;
     if (q + 1 < p1) code_next = __ldg(t.bprog + q + 1);
@@ -166,47 +203,53 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
     const int32_t rent = (int32_t)(code >> 35);
     double acc = 0.0;
     if constexpr (!STRUCT) {
-      switch (type) {
-        case 0:  // (v_n, v_n)
-          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 5 : 9));
-          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 5 : 9));
-          PASS(pair_term(d7(r), JP(r, false, false), JP(r, false, false)));
-          PASS(pair_term(d8(r), JQ(r, false, false), JQ(r, false, false)));
-          acc += in.dw + sxv;
-          break;
-        case 1:  // (v_o, v_n), o > n
-          PASS(h_flow_p(r.s, r.G, w7(r), 6));
-          PASS(h_flow_q(r.s, r.B, w8(r), 6));
-          PASS(pair_term(d7(r), JP(r, true, false), JP(r, false, false)));
-          PASS(pair_term(d8(r), JQ(r, true, false), JQ(r, false, false)));
-          break;
-        case 2:  // (th_n, v_n)
-          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 7 : 11));
-          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 7 : 11));
-          PASS(pair_term(d7(r), JP(r, false, true), JP(r, false, false)));
-          PASS(pair_term(d8(r), JQ(r, false, true), JQ(r, false, false)));
-          break;
-        case 3:  // (th_o, v_n)
-          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 8 : 10));
-          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 8 : 10));
-          PASS(pair_term(d7(r), JP(r, true, true), JP(r, false, false)));
-          PASS(pair_term(d8(r), JQ(r, true, true), JQ(r, false, false)));
-          break;
-        case 4:  // (th_n, th_n)
-          PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 12 : 14));
-          PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 12 : 14));
-          PASS(pair_term(d7(r), JP(r, false, true), JP(r, false, true)));
-          PASS(pair_term(d8(r), JQ(r, false, true), JQ(r, false, true)));
-          PASS(pair_term(d10(r), r.fr ? 1.0 : -1.0, r.fr ? 1.0 : -1.0));
-          acc += in.dw + sxt;
-          break;
-        default:  // (th_o, th_n), o > n
-          PASS(h_flow_p(r.s, r.G, w7(r), 13));
-          PASS(h_flow_q(r.s, r.B, w8(r), 13));
-          PASS(pair_term(d7(r), JP(r, true, true), JP(r, false, true)));
-          PASS(pair_term(d8(r), JQ(r, true, true), JQ(r, false, true)));
-          PASS(pair_term(d10(r), r.fr ? -1.0 : 1.0, r.fr ? 1.0 : -1.0));
-          break;
+      if (type == 0) {
+        acc = own0;
+      } else if (type == 2) {
+        acc = own2;
+      } else if (type == 4) {
+        acc = own4;
+      } else if ((mask & (mask - 1)) == 0) {  // one line to the neighbour: its terms in pass order
+        const LV r = lv(__ffs(mask) - 1);
+        if (type == 1) {  // (v_o, v_n), o > n
+          acc += h_flow_p(r.s, r.G, r.w7, 6);
+          acc += h_flow_q(r.s, r.B, r.w8, 6);
+          acc += pair_term(r.d7, JP(r, true, false), JP(r, false, false));
+          acc += pair_term(r.d8, JQ(r, true, false), JQ(r, false, false));
+        } else if (type == 3) {  // (th_o, v_n)
+          acc += h_flow_p(r.s, r.G, r.w7, r.fr ? 8 : 10);
+          acc += h_flow_q(r.s, r.B, r.w8, r.fr ? 8 : 10);
+          acc += pair_term(r.d7, JP(r, true, true), JP(r, false, false));
+          acc += pair_term(r.d8, JQ(r, true, true), JQ(r, false, false));
+        } else {  // (th_o, th_n), o > n
+          acc += h_flow_p(r.s, r.G, r.w7, 13);
+          acc += h_flow_q(r.s, r.B, r.w8, 13);
+          acc += pair_term(r.d7, JP(r, true, true), JP(r, false, true));
+          acc += pair_term(r.d8, JQ(r, true, true), JQ(r, false, true));
+          acc += pair_term(r.d10, r.fr ? -1.0 : 1.0, r.fr ? 1.0 : -1.0);
+        }
+      } else {  // parallel lines: pass-major over the group
+        switch (type) {
+          case 1:  // (v_o, v_n), o > n
+            PASS(h_flow_p(r.s, r.G, w7(r), 6));
+            PASS(h_flow_q(r.s, r.B, w8(r), 6));
+            PASS(pair_term(d7(r), JP(r, true, false), JP(r, false, false)));
+            PASS(pair_term(d8(r), JQ(r, true, false), JQ(r, false, false)));
+            break;
+          case 3:  // (th_o, v_n)
+            PASS(h_flow_p(r.s, r.G, w7(r), r.fr ? 8 : 10));
+            PASS(h_flow_q(r.s, r.B, w8(r), r.fr ? 8 : 10));
+            PASS(pair_term(d7(r), JP(r, true, true), JP(r, false, false)));
+            PASS(pair_term(d8(r), JQ(r, true, true), JQ(r, false, false)));
+            break;
+          default:  // (th_o, th_n), o > n
+            PASS(h_flow_p(r.s, r.G, w7(r), 13));
+            PASS(h_flow_q(r.s, r.B, w8(r), 13));
+            PASS(pair_term(d7(r), JP(r, true, true), JP(r, false, true)));
+            PASS(pair_term(d8(r), JQ(r, true, true), JQ(r, false, true)));
+            PASS(pair_term(d10(r), r.fr ? -1.0 : 1.0, r.fr ? 1.0 : -1.0));
+            break;
+        }
       }
     }
     const bool in_v = type < 4;
