@@ -352,25 +352,133 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
   }
 }
 
-// A = set_jacobian(eval_jac(x)) straight from x.  One thread per CSR row; the
-// rows of a CTA occupy one contiguous span of A, staged in shared memory and
-// written back as a single coalesced stream.
-constexpr int kSJ = 256, kSJCap = kSJ * 8;
-__global__ void __launch_bounds__(kSJ) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
-                                                           const double* __restrict__ x,
-                                                           double* __restrict__ A) {
-  __shared__ double sm[kSJCap];
-  const int32_t r0 = blockIdx.x * kSJ;
-  const int32_t r = r0 + threadIdx.x;
-  const int32_t rend = min(m, r0 + kSJ);
-  const int32_t base = __ldg(t.rowptr + r0), span = __ldg(t.rowptr + rend) - base;
-  if (span > kSJCap) {  // unusually long rows: write in place
-    if (r < m) sj_row(t, r, x, A + __ldg(t.rowptr + r));
+// A = set_jacobian(eval_jac(x)) straight from x, one warp per task.  The rows of
+// one entity over consecutive periods are consecutive CSR rows, i.e. one
+// contiguous span of A, and every span is written coalesced:
+//   * balance rows of a bus (all periods): constants (+1 per free generator,
+//     +-1 per incident line, held by lane j = slot j and broadcast by shuffle);
+//   * flow_p and flow_q rows of (line, 32 periods): the line state is computed
+//     once for both rows, staged ([slot][lane]) and written back;
+//   * thermal rows of a thermal line (all periods): (2p, 2q);
+//   * angle rows of a line (all periods): (+1, -1) at the free angle slots;
+//   * ramp rows: one thread per row.
+constexpr int kSJW = 8;  // warps per CTA
+__device__ __forceinline__ void warp_flush(double* __restrict__ A, int64_t base, const double* stg,
+                                           int32_t len, int32_t nt, int lane) {
+  __syncwarp();
+  const int32_t q32 = 32 / len, r32 = 32 - q32 * len;
+  int32_t tq = lane / len, rj = lane - tq * len;
+  for (int32_t e = lane; e < nt * len; e += 32) {
+    A[base + e] = stg[rj * 33 + tq];
+    tq += q32;
+    rj += r32;
+    if (rj >= len) {
+      rj -= len;
+      ++tq;
+    }
+  }
+  __syncwarp();
+}
+
+// span of T rows of `len` constant slots; lane j < len holds slot j's value
+__device__ __forceinline__ void warp_const_rows(double* __restrict__ A, int64_t base, double v,
+                                                int32_t len, int32_t T, int lane) {
+  const int32_t r32 = 32 % len, n = T * len;
+  int32_t rj = lane % len;
+  for (int32_t e0 = 0; e0 < n; e0 += 32) {  // warp-uniform trip count (full-mask shuffle)
+    const double val = __shfl_sync(0xffffffffu, v, rj);
+    if (e0 + lane < n) A[base + e0 + lane] = val;
+    rj += r32;
+    if (rj >= len) rj -= len;
+  }
+}
+
+__global__ void __launch_bounds__(kSJW * 32) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
+                                                                const double* __restrict__ x,
+                                                                double* __restrict__ A) {
+  __shared__ double stg_all[kSJW * 5 * 33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t T = t.T, tch = t.tchunks;
+  const int32_t LT = (t.ang0 - t.therm0) / (T > 0 ? T : 1);
+  int64_t wg = (int64_t)blockIdx.x * kSJW + warp;
+  if (wg < 2ll * t.N) {  // balance rows of bus b, all periods
+    const bool Q = wg >= t.N;
+    const int32_t b = (int32_t)(wg - (Q ? t.N : 0));
+    const int32_t nf = __ldg((Q ? t.ngq : t.ngp) + b);
+    const int32_t b0 = __ldg(t.bl_ptr + b), len = nf + __ldg(t.bl_ptr + b + 1) - b0;
+    if (len == 0) return;
+    const int64_t base = __ldg(t.rowptr + (Q ? t.bal_q0 : t.bal_p0) + b * T);
+    if (len > 32) {  // (very high degree: slot by slot)
+      for (int32_t e = lane; e < T * len; e += 32) {
+        const int32_t j = e % len;
+        A[base + e] = j < nf ? 0.0 + 1.0 : 0.0 + ((__ldg(t.bl + b0 + j - nf) & 1) ? -1.0 : 1.0);
+      }
+      return;
+    }
+    double v = 0.0 + 1.0;
+    if (lane >= nf && lane < len) v = 0.0 + ((__ldg(t.bl + b0 + lane - nf) & 1) ? -1.0 : 1.0);
+    warp_const_rows(A, base, v, len, T, lane);
     return;
   }
-  if (r < m) sj_row(t, r, x, sm + (__ldg(t.rowptr + r) - base));
-  __syncthreads();
-  for (int i = threadIdx.x; i < span; i += kSJ) A[base + i] = sm[i];
+  wg -= 2ll * t.N;
+  if (wg < (int64_t)t.L * tch) {  // flow_p / flow_q rows of (line, 32 periods)
+    double* stg = stg_all + warp * (5 * 33);
+    const int32_t l = (int32_t)(wg / tch), c0 = (int32_t)(wg - (int64_t)l * tch) * 32;
+    const int32_t nt = min(32, T - c0), ts = lane < nt ? c0 + lane : c0;
+    const int4 d0 = __ldg(t.ldesc0 + l);
+    const int32_t f = d0.x, to = d0.y, len = 1 + __popc(d0.w & 15);
+    const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
+    const LineState s = line_state(G, B, x[t.v0 + f * T + ts], x[t.v0 + to * T + ts],
+                                   x[t.th0 + f * T + ts], x[t.th0 + to * T + ts]);
+    const int64_t bp = __ldg(t.rowptr + t.flow_p0 + l * T + c0);
+    const int64_t bq = __ldg(t.rowptr + t.flow_q0 + l * T + c0);
+    int pos[5];
+#pragma unroll
+    for (int fl = 0; fl < 5; ++fl) pos[fl] = __ldg(t.fpos + 5 * l + fl);
+#pragma unroll
+    for (int fl = 0; fl < 5; ++fl)
+      if (pos[fl] >= 0) stg[pos[fl] * 33 + lane] = 0.0 + j_flow_p(s, G, B, fl);
+    warp_flush(A, bp, stg, len, nt, lane);
+#pragma unroll
+    for (int fl = 0; fl < 5; ++fl)
+      if (pos[fl] >= 0) stg[pos[fl] * 33 + lane] = 0.0 + j_flow_q(s, G, B, fl);
+    warp_flush(A, bq, stg, len, nt, lane);
+    return;
+  }
+  wg -= (int64_t)t.L * tch;
+  if (wg < LT) {  // thermal rows of thermal slot k, all periods: [p, q] -> (2p, 2q)
+    const int32_t k = (int32_t)wg, l = __ldg(t.th_line + k);
+    const int64_t base = __ldg(t.rowptr + t.therm0 + k * T);
+    for (int32_t e = lane; e < 2 * T; e += 32) {
+      const int32_t tt = e >> 1;
+      A[base + e] = 0.0 + j_thermal(x[((e & 1) ? t.q0 : t.p0) + l * T + tt]);
+    }
+    return;
+  }
+  wg -= LT;
+  if (wg < t.L) {  // angle rows of line l, all periods: [th_f, th_t] -> (1, -1)
+    const int32_t l = (int32_t)wg;
+    const int pf = __ldg(t.apos + 2 * l), pt = __ldg(t.apos + 2 * l + 1);
+    const int32_t len = (pf >= 0) + (pt >= 0);
+    if (len == 0) return;
+    const int64_t base = __ldg(t.rowptr + t.ang0 + l * T);
+    const double v = lane == pf ? 0.0 + 1.0 : 0.0 + (-1.0);
+    warp_const_rows(A, base, v, len, T, lane);
+    return;
+  }
+  wg -= t.L;
+  const int64_t r = (int64_t)t.ramp0 + wg * 32 + lane;  // ramp rows, one thread each
+  if (r >= m) return;
+  const int32_t ri = (int32_t)r;
+  double* dst = A + __ldg(t.rowptr + ri);
+  // [pg_{s-1}, pg_s]: (-1, 1); a shard's first row keeps pg_s only
+  const int32_t len = __ldg(t.rowptr + ri + 1) - __ldg(t.rowptr + ri);
+  if (len == 2) {
+    dst[0] = 0.0 + (-1.0);
+    dst[1] = 0.0 + 1.0;
+  } else if (len == 1) {
+    dst[0] = 0.0 + 1.0;
+  }
 }
 
 // ------------------------------------------------------------------ host
@@ -416,8 +524,10 @@ void opf_set_jacobian_fused(gn_kkt* K, const double* x) {
   if (K->m <= 0) return;
   {
     KTimer kt("k_opf_set_jac_fused", K->stream);
-    k_opf_set_jac_fused<<<(unsigned)((K->m + kSJ - 1) / kSJ), kSJ, 0, K->stream>>>(t, K->m, x,
-                                                                                   K->avals.p);
+    const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
+    const int64_t warps = 2ll * t.N + (int64_t)t.L * t.tchunks + LT + t.L + (K->m - t.ramp0 + 31) / 32;
+    k_opf_set_jac_fused<<<(unsigned)((warps + kSJW - 1) / kSJW), kSJW * 32, 0, K->stream>>>(
+        t, K->m, x, K->avals.p);
   }
   count_launch();
   GN_CK(cudaGetLastError());

@@ -1,4 +1,4 @@
-python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+python -m pytest tests -m gpu -x -q 2>&1 | tail -15 | grep -v "^\s*$" | tail -8
 for s in 1 2; do python bench.py --steps 20 --warmup 5 --no-e2e --no-cpu-baseline --streams $s > gpurun_out/bq_$s.json 2> gpurun_out/bq_$s.err || tail -5 gpurun_out/bq_$s.err; done
 python - <<'PY'
 import json
