@@ -538,22 +538,6 @@ bool opf_fused_verify(gn_kkt* K) {
   const OpfKktTab& t = K->opf->t;
   if (!fz_bus_fits(t.maxdeg)) return false;  // one line per lane, one warp's shared memory
   K->dvals.alloc(static_cast<size_t>(K->m) + 1);
-  {  // bus lists of the bus-column kernel, by degree class (shared-memory footprint)
-    std::vector<int32_t> bp(t.N + 1);
-    GN_CK(cudaMemcpyAsync(bp.data(), t.bl_ptr, sizeof(int32_t) * (t.N + 1), cudaMemcpyDeviceToHost,
-                          K->stream));
-    GN_CK(cudaStreamSynchronize(K->stream));
-    std::vector<int32_t> cls[kBusClasses];
-    for (int32_t n = 0; n < t.N; ++n) {
-      const int32_t deg = bp[n + 1] - bp[n];
-      cls[deg <= 1 ? 0 : std::min(deg, kBusClasses) - 1].push_back(n);  // isolated buses too (diagonal)
-    }
-    for (int k = 0; k < kBusClasses; ++k) {
-      K->opf->bus_cls[k].upload(cls[k].data(), cls[k].size(), K->stream);
-      if (cls[k].empty()) K->opf->bus_cls[k].alloc(1);
-      K->opf->n_bus_cls[k] = static_cast<int32_t>(cls[k].size());
-    }
-  }
   cudaStream_t s = K->stream;
   DBuf<int32_t> rows, bad, diff;
   rows.alloc(static_cast<size_t>(K->mnnz) + 1);

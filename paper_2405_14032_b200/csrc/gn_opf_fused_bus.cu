@@ -34,7 +34,7 @@ constexpr int kBusSmemMax = 200 * 1024;  // dynamic shared memory cap of the bus
 // per lane into shared memory; the bus's slot program (host-built: lane mask of
 // the lines of each slot + slot type) then drives the ordered sums.
 template <bool STRUCT>
-__global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int32_t* __restrict__ buses,
+__global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int4* __restrict__ buses,
                                                        int32_t n_buses, int32_t maxdeg, FIn in,
                                                        const double* __restrict__ dv,
                                                        double* __restrict__ M,
@@ -46,9 +46,9 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   const int64_t w = (int64_t)blockIdx.x * nw + warp;
   const int64_t n64 = w / t.tchunks;
   if (n64 >= n_buses) return;  // warp-uniform
-  const int32_t n = __ldg(buses + n64), T = t.T;
+  const int4 bd0 = __ldg(buses + 2 * n64), bd1 = __ldg(buses + 2 * n64 + 1);
+  const int32_t n = bd0.x, b0 = bd0.y, deg = bd0.z & 255, T = t.T;
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
-  const int32_t b0 = __ldg(t.bl_ptr + n), deg = __ldg(t.bl_ptr + n + 1) - b0;
   // per (line, lane): 6 state values + the 5 row inputs it contributes with
   double* S = bsm + (size_t)warp * maxdeg * kSV * 32 + lane;
   // per-line warp-uniform data, filled by lanes 0..deg-1 in parallel
@@ -58,13 +58,9 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   };
   LU* U = reinterpret_cast<LU*>(bsm + (size_t)nw * maxdeg * kSV * 32) + warp * maxdeg;
   if (lane < deg) {
-    const int32_t e = __ldg(t.bl + b0 + lane);
-    LU u;
-    u.l = e >> 1;
-    u.fr = e & 1;
-    u.G = __ldg(t.lg + u.l);
-    u.B = __ldg(t.lb + u.l);
-    U[lane] = u;
+    const int2 e = __ldg(t.blx + b0 + lane);
+    const double2 gb = __ldg(t.blgb + b0 + lane);
+    U[lane] = LU{gb.x, gb.y, e.x >> 1, e.x & 1};
   }
   __syncwarp();
   if (tt >= T) return;  // no warp collectives below
@@ -73,15 +69,16 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   if constexpr (!STRUCT) {
     // every global input of the slot program is read exactly once, up front
     // (independent loads in flight together); the slot loop reads only smem
+#pragma unroll 4
     for (int i = 0; i < deg; ++i) {
-      const LU u = U[i];
-      const int32_t f = __ldg(t.lf + u.l), to = __ldg(t.lt + u.l);
-      const int64_t rl = (int64_t)u.l * T + tt;
+      const int2 e = __ldg(t.blx + b0 + i);
+      const double2 gb = __ldg(t.blgb + b0 + i);
+      const int32_t l = e.x >> 1, f = (e.x & 1) ? n : e.y, to = (e.x & 1) ? e.y : n;
+      const int32_t rl = l * T + tt;
       const double w7 = in.w[t.flow_p0 + rl], w8 = in.w[t.flow_q0 + rl];
       const double d7 = dv[t.flow_p0 + rl], d8 = dv[t.flow_q0 + rl], d10 = dv[t.ang0 + rl];
-      const LineState s = line_state(u.G, u.B,
-                                     in.x[t.v0 + (int64_t)f * T + tt], in.x[t.v0 + (int64_t)to * T + tt],
-                                     in.x[t.th0 + (int64_t)f * T + tt], in.x[t.th0 + (int64_t)to * T + tt]);
+      const LineState s = line_state(gb.x, gb.y, in.x[t.v0 + f * T + tt], in.x[t.v0 + to * T + tt],
+                                     in.x[t.th0 + f * T + tt], in.x[t.th0 + to * T + tt]);
       double* q = S + (size_t)i * kSV * 32;
       q[0 * 32] = s.Cs;
       q[1 * 32] = s.Sn;
@@ -144,11 +141,11 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
     const int32_t k = __ldg(t.lent + off + e);
     return k < 0 ? -1 : k * T + tt;
   };
-  const int32_t cv = col(off_v, n), ct = col(off_th, n);
+  const int32_t cv = bd1.x < 0 ? -1 : bd1.x * T + tt, ct = bd1.y < 0 ? -1 : bd1.y * T + tt;
   const int64_t posv = cv >= 0 ? (int64_t)__ldg(t.colptr + cv) : 0;
   const int64_t post = ct >= 0 ? (int64_t)__ldg(t.colptr + ct) : 0;
   int jv = 0, jt = 0;
-  const int32_t p0 = __ldg(t.bprog_ptr + n), p1 = __ldg(t.bprog_ptr + n + 1);
+  const int32_t p0 = bd0.w, p1 = p0 + (bd0.z >> 8);
 #define PASS(expr)                                 \
   for (uint32_t mm = mask; mm; mm &= mm - 1) {     \
     const LV r = lv(__ffs(mm) - 1);                \
@@ -270,7 +267,7 @@ bool fz_bus_fits(int32_t maxdeg) {
   return maxdeg <= 32 && md * (kSV * 32 * sizeof(double) + 24) <= kBusSmemMax;
 }
 
-void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
+void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32_t maxdeg,
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
                    cudaStream_t s) {
   if (n_buses <= 0) return;

@@ -745,12 +745,45 @@ bool opf_kkt_prepare(gn_kkt* K) {
   up(X->lnb_ptr, lnb_ptr, s); up(X->lnb, lnb, s); up(X->lnbx, lnbx, s);
   up(X->ldesc0, ldesc0, s); up(X->ldesc1, ldesc1, s);
   up(X->bprog_ptr, bprog_ptr, s); up(X->bprog, bprog, s);
+  {  // bus-column kernel: per incident line (bl order) its (l<<1|is_from, other bus) and (G, B);
+     // per degree class the bus descriptors (n, bl begin, deg | program length << 8,
+     // program begin) + (lifted v rank, lifted th rank)
+    std::vector<int2> blx(bl.size());
+    std::vector<double2> blgb(bl.size());
+    std::vector<double> lg_h(L), lb_h(L);
+    if (L > 0) {
+      GN_CK(cudaMemcpyAsync(lg_h.data(), c->lg.p, sizeof(double) * L, cudaMemcpyDeviceToHost, s));
+      GN_CK(cudaMemcpyAsync(lb_h.data(), c->lb.p, sizeof(double) * L, cudaMemcpyDeviceToHost, s));
+      GN_CK(cudaStreamSynchronize(s));
+    }
+    for (size_t i = 0; i < bl.size(); ++i) {
+      const int32_t e = bl[i], l = e >> 1;
+      blx[i] = make_int2(e, (e & 1) ? c->line_to[l] : c->line_from[l]);
+      blgb[i] = make_double2(lg_h[l], lb_h[l]);
+    }
+    up(X->blx, blx, s);
+    up(X->blgb, blgb, s);
+    std::vector<int4> cls[kBusClasses];
+    for (int32_t n = 0; n < N; ++n) {
+      const int32_t deg = bl_ptr[n + 1] - bl_ptr[n];
+      const int32_t np = bprog_ptr[n + 1] - bprog_ptr[n];
+      auto& v = cls[deg <= 1 ? 0 : std::min(deg, kBusClasses) - 1];  // isolated buses too (diagonal)
+      v.push_back(make_int4(n, bl_ptr[n], deg | (np << 8), bprog_ptr[n]));
+      v.push_back(make_int4(lent[offs[C_V] + n], lent[offs[C_TH] + n], 0, 0));
+    }
+    for (int k = 0; k < kBusClasses; ++k) {
+      up(X->bus_cls[k], cls[k], s);
+      if (cls[k].empty()) X->bus_cls[k].alloc(2);
+      X->n_bus_cls[k] = static_cast<int32_t>(cls[k].size() / 2);
+    }
+  }
   t.lent = X->lent.p; t.items = X->items.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
   t.fpos = X->fpos.p; t.apos = X->apos.p; t.lidx_to = X->lidx_to.p; t.lidx_from = X->lidx_from.p;
   t.gbus = X->gbus.p; t.ppos = X->ppos.p; t.qpos = X->qpos.p; t.g_ramp = X->g_ramp.p;
   t.ngp = X->ngp.p; t.ngq = X->ngq.p; t.bl_ptr = X->bl_ptr.p; t.bl = X->bl.p;
   t.bg_ptr = X->bg_ptr.p; t.bg = X->bg.p; t.nb_ptr = X->nb_ptr.p; t.nb = X->nb.p; t.nb_inc = X->nb_inc.p;
   t.lnb_ptr = X->lnb_ptr.p; t.lnb = X->lnb.p; t.lnbx = X->lnbx.p;
+  t.blx = X->blx.p; t.blgb = X->blgb.p;
   t.ldesc0 = X->ldesc0.p; t.ldesc1 = X->ldesc1.p;
   t.bprog_ptr = X->bprog_ptr.p; t.bprog = X->bprog.p;
   t.rowptr = K->A.ptr.p; t.colptr = K->M.ptr.p;

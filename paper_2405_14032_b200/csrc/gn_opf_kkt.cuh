@@ -41,6 +41,8 @@ struct OpfKktTab {
                                         //  min/max terminal bits 0-3, min==t bit 4, max==t bit 5)
   const int4* ldesc1;                   // [L] (lnb begin, lnb end, lifted p rank, lifted q rank)
   const int32_t* lnbx;                  // [lnb] l' << 4 | t(l') == max << 3 | t(l') == min << 2 | bits
+  const int2* blx;                      // [bl] (l << 1 | is_from, other bus) per incident line
+  const double2* blgb;                  // [bl] (G, B) per incident line
   const int32_t* bprog_ptr;             // [N+1] per-bus slot programs of the v(n)/th(n) columns
   const unsigned long long* bprog;      // (row entity << 35 | type << 32 | lane mask)
 };
@@ -59,7 +61,7 @@ struct FIn {
 // lanes = (32/P periods) x (P incident-line slots), P = next pow2 >= degree.
 // klass 0..5: buses of klass+1 lines (klass 0: at most one), shared memory sized to
 // the degree; klass 6: every bus with more lines (maxdeg = the network's maximum).
-void launch_fz_bus(const OpfKktTab& t, const int32_t* buses, int32_t n_buses, int32_t maxdeg,
+void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32_t maxdeg,
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows,
                    int32_t* bad, cudaStream_t s);
 constexpr int kBusClasses = 7;
@@ -76,7 +78,9 @@ struct OpfKkt {
   DBuf<int4> ldesc0, ldesc1;
   DBuf<int32_t> bprog_ptr;
   DBuf<unsigned long long> bprog;
-  DBuf<int32_t> bus_cls[kBusClasses];  // buses by degree class (bus-column kernel)
+  DBuf<int4> bus_cls[kBusClasses];  // bus descriptors by degree class (bus-column kernel)
+  DBuf<int2> blx;
+  DBuf<double2> blgb;
   int32_t n_bus_cls[kBusClasses] = {};
 };
 
