@@ -215,7 +215,9 @@ int gn_kkt_set_jacobian_x(gn_kkt* kkt, const double* x, int mem);
 int gn_kkt_assemble_x(gn_kkt* kkt, const double* x, const double* row_weights,
                       double obj_weight, const double* sigma_x, const double* sigma_s,
                       double delta_w, double delta_c, int mem);
-/* jacobian_values() / values() (condensed.hpp:94-96). */
+/* jacobian_values() / values() (condensed.hpp:94-96).  In the device modes the
+ * destinations may be any UVA-addressable memory: device buffers or pinned host
+ * buffers (an asynchronous read-back overlapping later work on the stream). */
 int gn_kkt_values(gn_kkt* kkt, double* a_vals, double* m_vals, int mem);
 /* Selects the assembly algorithm: 0 = auto, 1 = generic contributor lists,
  * 2 = OPF-specialised (lifted KKTs only). */

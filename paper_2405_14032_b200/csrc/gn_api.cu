@@ -712,7 +712,8 @@ int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
   if (!K) return GN_ERR_INVALID;
   API_TRY
   set_device(K->device);
-  const auto kind = is_device(mem) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+  // device modes accept any UVA-addressable destination (device or pinned host memory)
+  const auto kind = is_device(mem) ? cudaMemcpyDefault : cudaMemcpyDeviceToHost;
   if (av && K->annz) GN_CK(cudaMemcpyAsync(av, K->avals.p, sizeof(double) * K->annz, kind, K->stream));
   if (mv && K->mnnz) GN_CK(cudaMemcpyAsync(mv, K->mvals.p, sizeof(double) * K->mnnz, kind, K->stream));
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
