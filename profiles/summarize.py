@@ -34,7 +34,28 @@ def short(name: str) -> str:
     return name.split("(")[0].replace("void ", "").strip()
 
 
+MODES = {"0": "F", "1": "GRAD", "2": "G", "3": "J", "4": "H"}
+
+
+def pretty(name: str) -> str:
+    """gnb::k_line<4> -> k_line<H>; value-mode fused kernels <0> -> plain name."""
+    n = name.replace("gnb::", "")
+    for k in ("k_line", "k_gen", "k_thermal", "k_ramp"):
+        if n.startswith(k + "<") and n[len(k) + 1:-1] in MODES:
+            return f"{k}<{MODES[n[len(k) + 1:-1]]}>"
+    for k in ("k_fz_bus3", "k_fz_line", "k_fz_gen", "k_opf_assemble"):
+        if n == k + "<0>":
+            return k
+        if n == k + "<1>":
+            return k + " (structure check)"
+    return n
+
+
 def launches(path: str, out: str):
+    """Per-step kernel table of an ncu launch list of `bench.py --steps K --warmup W`:
+    kernels launched a multiple of S times (S = warm-up + timed + profiled steps,
+    the most common launch count) are the step's kernels; the rest ran once at setup."""
+    from collections import Counter
     text = open(path).read().splitlines()
     start = next(i for i, l in enumerate(text) if l.startswith('"ID"'))
     rows = [r for r in csv.DictReader(text[start:]) if r.get("Metric Name") == "gpu__time_duration.sum"]
@@ -42,13 +63,24 @@ def launches(path: str, out: str):
     for r in rows:
         v = float(r["Metric Value"].replace(",", ""))
         unit = r.get("Metric Unit", "ns")
-        us = v / 1000.0 if unit == "nsecond" or unit == "ns" else (v * 1000.0 if unit in ("msecond", "ms") else v)
+        us = v / 1000.0 if unit in ("nsecond", "ns") else (v * 1000.0 if unit in ("msecond", "ms") else v)
         agg.setdefault(short(r["Kernel Name"]), []).append(us)
-    total = sum(sum(v) for v in agg.values())
-    lines = ["| kernel | launches | total us | mean us | share |", "|---|---:|---:|---:|---:|"]
-    for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        lines.append(f"| `{k}` | {len(v)} | {sum(v):.1f} | {sum(v)/len(v):.2f} | {sum(v)/total:.1%} |")
-    lines.append(f"\n{len(rows)} launches, {total/1000:.3f} ms total device time (cold-cache, serialised).")
+    counts = Counter(len(v) for k, v in agg.items() if k.startswith("gnb::"))
+    S = max(counts, key=lambda c: (counts[c], c))
+    step = {k: v for k, v in agg.items() if len(v) % S == 0 and k.startswith("gnb::")}
+    setup = {k: v for k, v in agg.items() if k not in step}
+    tot = sum(sum(v) for v in step.values()) / S
+    lines = [f"Per-step kernels ({S} steps in the capture: warm-up + timed + profiled; "
+             "ncu serialises launches and runs them cold, so the SHARE column is the "
+             "comparable figure, not the absolute time).", "",
+             "| kernel | launches / step | us / step | us / launch | share of step |",
+             "|---|---:|---:|---:|---:|"]
+    for k, v in sorted(step.items(), key=lambda kv: -sum(kv[1])):
+        lines.append(f"| `{pretty(k)}` | {len(v) // S} | {sum(v) / S:.1f} | {sum(v) / len(v):.2f} "
+                     f"| {sum(v) / S / tot:.1%} |")
+    lines.append(f"\n{tot / 1000:.3f} ms of kernel time per step.  Setup (once per context / KKT "
+                 f"object, not in the step): {len(setup)} kernels, "
+                 f"{sum(sum(v) for v in setup.values()) / 1000:.3f} ms.")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
@@ -61,8 +93,12 @@ def full(rep: str, out: str, traffic_json: str | None = None):
     lines = ["| kernel | " + " | ".join(lbl for _, lbl in KEYS) + " |",
              "|---|" + "---:|" * len(KEYS)]
     traffic = {}
+    seen: dict = {}
     for r in rows[2:]:
-        name = short(r[head.index("Kernel Name")])
+        name = pretty(short(r[head.index("Kernel Name")]))
+        seen[name] = seen.get(name, 0) + 1
+        if seen[name] > 1:  # e.g. one launch per degree class
+            name = f"{name} #{seen[name]}"
         cells = []
         for key, _ in KEYS:
             try:
