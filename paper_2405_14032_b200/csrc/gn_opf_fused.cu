@@ -488,7 +488,8 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   const OpfKktTab& t = K->opf->t;
   cudaStream_t s = K->stream;
   for (int k = 0; k < kBusClasses; ++k)
-    launch_fz_bus(t, K->opf->bus_cls[k].p, K->opf->n_bus_cls[k], k < kBusClasses - 1 ? k + 1 : t.maxdeg, k, in, dv,
+    launch_fz_bus(t, K->opf->bus_cls[k].p, K->opf->n_bus_cls[k],
+                  k < kBusRegMax ? k + 1 : (k == kBusRegMax ? 8 : K->opf->maxdeg_rest), k, in, dv,
                   M, rows, bad, s);
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {

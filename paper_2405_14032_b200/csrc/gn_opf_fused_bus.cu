@@ -262,6 +262,188 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   }
 }
 
+// Register-resident variant for buses of exactly DEG lines and no parallel lines
+// (almost every bus of a transmission network): each lane holds its period's
+// state and row inputs of all DEG lines in registers; the own slots are one
+// pass-major sweep, each neighbour slot is its line's terms in pass order, and
+// every value goes to its precomputed offset in the column (bpos, boff).
+template <int DEG, bool STRUCT>
+__global__ void __launch_bounds__(kBW3 * 32) k_fz_busr(OpfKktTab t, const int4* __restrict__ buses,
+                                                    int32_t n_buses, FIn in,
+                                                    const double* __restrict__ dv,
+                                                    double* __restrict__ M,
+                                                    int32_t* __restrict__ rows,
+                                                    int32_t* __restrict__ bad) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * kBW3 + warp;
+  const int64_t n64 = w / t.tchunks;
+  if (n64 >= n_buses) return;
+  const int32_t T = t.T;
+  const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
+  if (tt >= T) return;
+  const int4 bd0 = __ldg(buses + 2 * n64), bd1 = __ldg(buses + 2 * n64 + 1);
+  const int32_t n = bd0.x, b0 = bd0.y, boff = bd0.w;
+  const int32_t cv = bd1.x < 0 ? -1 : bd1.x * T + tt, ct = bd1.y < 0 ? -1 : bd1.y * T + tt;
+  int2 e[DEG];
+  int32_t pp[DEG];
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    e[i] = __ldg(t.blx + b0 + i);
+    pp[i] = __ldg(t.bpos + b0 + i);
+  }
+  const int64_t posv = cv >= 0 ? (int64_t)__ldg(t.colptr + cv) : 0;
+  const int64_t post = ct >= 0 ? (int64_t)__ldg(t.colptr + ct) : 0;
+  if constexpr (STRUCT) {
+    const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
+    auto col = [&](int32_t off, int32_t ent) {
+      const int32_t k = __ldg(t.lent + off + ent);
+      return k < 0 ? -1 : k * T + tt;
+    };
+    int32_t nv = 0, nt_ = 0;
+    if (cv >= 0) {
+      rows[posv] = cv;
+      ++nv;
+      if (ct >= 0) {
+        rows[posv + boff] = ct;
+        ++nv;
+      }
+    }
+    if (ct >= 0) {
+      rows[post] = ct;
+      ++nt_;
+    }
+#pragma unroll
+    for (int i = 0; i < DEG; ++i) {
+      const int32_t o = e[i].y, p1 = pp[i] & 0xff, p3 = (pp[i] >> 8) & 0xff, p5 = (pp[i] >> 16) & 0xff;
+      if (p1 != 0xff && cv >= 0) { rows[posv + p1] = col(off_v, o); ++nv; }
+      if (p3 != 0xff && cv >= 0) { rows[posv + p3] = col(off_th, o); ++nv; }
+      if (p5 != 0xff && ct >= 0) { rows[post + p5] = col(off_th, o); ++nt_; }
+    }
+    if ((cv >= 0 && posv + nv != __ldg(t.colptr + cv + 1)) ||
+        (ct >= 0 && post + nt_ != __ldg(t.colptr + ct + 1)) || (cv >= 0 && ct >= 0 && boff < 0))
+      atomicOr(bad, 1);
+    return;
+  }
+  // ---- loads (all independent), then the line states
+  double2 gb[DEG];
+  double xvf[DEG], xvt[DEG], xtf[DEG], xtt[DEG], w7[DEG], w8[DEG], d7[DEG], d8[DEG], d10[DEG];
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    gb[i] = __ldg(t.blgb + b0 + i);
+    const bool fr = e[i].x & 1;
+    const int32_t l = e[i].x >> 1, o = e[i].y, f = fr ? n : o, to = fr ? o : n;
+    const int32_t rl = l * T + tt;
+    xvf[i] = in.x[t.v0 + f * T + tt];
+    xvt[i] = in.x[t.v0 + to * T + tt];
+    xtf[i] = in.x[t.th0 + f * T + tt];
+    xtt[i] = in.x[t.th0 + to * T + tt];
+    w7[i] = in.w[t.flow_p0 + rl];
+    w8[i] = in.w[t.flow_q0 + rl];
+    d7[i] = dv[t.flow_p0 + rl];
+    d8[i] = dv[t.flow_q0 + rl];
+    d10[i] = dv[t.ang0 + rl];
+  }
+  const double sxv = cv >= 0 ? in.sx[cv] : 0.0, sxt = ct >= 0 ? in.sx[ct] : 0.0;
+  LineState st[DEG];
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) st[i] = line_state(gb[i].x, gb[i].y, xvf[i], xvt[i], xtf[i], xtt[i]);
+  // own slots, pass-major over the lines (ascending l)
+  double own0 = 0.0, own2 = 0.0, own4 = 0.0;
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    const bool fr = e[i].x & 1;
+    own0 += h_flow_p(st[i], gb[i].x, w7[i], fr ? 5 : 9);
+    own2 += h_flow_p(st[i], gb[i].x, w7[i], fr ? 7 : 11);
+    own4 += h_flow_p(st[i], gb[i].x, w7[i], fr ? 12 : 14);
+  }
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    const bool fr = e[i].x & 1;
+    own0 += h_flow_q(st[i], gb[i].y, w8[i], fr ? 5 : 9);
+    own2 += h_flow_q(st[i], gb[i].y, w8[i], fr ? 7 : 11);
+    own4 += h_flow_q(st[i], gb[i].y, w8[i], fr ? 12 : 14);
+  }
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    const bool fr = e[i].x & 1;
+    const double jv = j_flow_p(st[i], gb[i].x, gb[i].y, fr ? 1 : 2);
+    const double jt = j_flow_p(st[i], gb[i].x, gb[i].y, fr ? 3 : 4);
+    own0 += pair_term(d7[i], jv, jv);
+    own2 += pair_term(d7[i], jt, jv);
+    own4 += pair_term(d7[i], jt, jt);
+  }
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    const bool fr = e[i].x & 1;
+    const double jv = j_flow_q(st[i], gb[i].x, gb[i].y, fr ? 1 : 2);
+    const double jt = j_flow_q(st[i], gb[i].x, gb[i].y, fr ? 3 : 4);
+    own0 += pair_term(d8[i], jv, jv);
+    own2 += pair_term(d8[i], jt, jv);
+    own4 += pair_term(d8[i], jt, jt);
+  }
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    const bool fr = e[i].x & 1;
+    own4 += pair_term(d10[i], fr ? 1.0 : -1.0, fr ? 1.0 : -1.0);
+  }
+  own0 += in.dw + sxv;
+  own4 += in.dw + sxt;
+  if (cv >= 0) {
+    M[posv] = own0;
+    if (ct >= 0) M[posv + boff] = own2;
+  }
+  if (ct >= 0) M[post] = own4;
+  // neighbour slots: one line each, its terms in pass order
+#pragma unroll
+  for (int i = 0; i < DEG; ++i) {
+    const bool fr = e[i].x & 1;
+    const double G = gb[i].x, B = gb[i].y;
+    const LineState& s = st[i];
+    const int fvn = fr ? 1 : 2, fvo = fr ? 2 : 1, ftn = fr ? 3 : 4, fto = fr ? 4 : 3;
+    const int32_t p1 = pp[i] & 0xff, p3 = (pp[i] >> 8) & 0xff, p5 = (pp[i] >> 16) & 0xff;
+    if (p1 != 0xff && cv >= 0) {  // (v(o), v(n)), o > n
+      double acc = 0.0;
+      acc += h_flow_p(s, G, w7[i], 6);
+      acc += h_flow_q(s, B, w8[i], 6);
+      acc += pair_term(d7[i], j_flow_p(s, G, B, fvo), j_flow_p(s, G, B, fvn));
+      acc += pair_term(d8[i], j_flow_q(s, G, B, fvo), j_flow_q(s, G, B, fvn));
+      M[posv + p1] = acc;
+    }
+    if (p3 != 0xff && cv >= 0) {  // (th(o), v(n))
+      double acc = 0.0;
+      acc += h_flow_p(s, G, w7[i], fr ? 8 : 10);
+      acc += h_flow_q(s, B, w8[i], fr ? 8 : 10);
+      acc += pair_term(d7[i], j_flow_p(s, G, B, fto), j_flow_p(s, G, B, fvn));
+      acc += pair_term(d8[i], j_flow_q(s, G, B, fto), j_flow_q(s, G, B, fvn));
+      M[posv + p3] = acc;
+    }
+    if (p5 != 0xff && ct >= 0) {  // (th(o), th(n)), o > n
+      double acc = 0.0;
+      acc += h_flow_p(s, G, w7[i], 13);
+      acc += h_flow_q(s, B, w8[i], 13);
+      acc += pair_term(d7[i], j_flow_p(s, G, B, fto), j_flow_p(s, G, B, ftn));
+      acc += pair_term(d8[i], j_flow_q(s, G, B, fto), j_flow_q(s, G, B, ftn));
+      acc += pair_term(d10[i], fr ? -1.0 : 1.0, fr ? 1.0 : -1.0);
+      M[post + p5] = acc;
+    }
+  }
+}
+
+template <int DEG>
+static void launch_busr(const OpfKktTab& t, const int4* buses, int32_t n_buses, const FIn& in,
+                        const double* dv, double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
+  static const char* names[] = {"", "k_fz_busr<d1>", "k_fz_busr<d2>", "k_fz_busr<d3>",
+                                "k_fz_busr<d4>", "k_fz_busr<d5>", "k_fz_busr<d6>"};
+  const int64_t warps = (int64_t)n_buses * t.tchunks;
+  const unsigned blocks = (unsigned)((warps + kBW3 - 1) / kBW3);
+  KTimer kt(names[DEG], s);
+  if (rows)
+    k_fz_busr<DEG, true><<<blocks, kBW3 * 32, 0, s>>>(t, buses, n_buses, in, dv, M, rows, bad);
+  else
+    k_fz_busr<DEG, false><<<blocks, kBW3 * 32, 0, s>>>(t, buses, n_buses, in, dv, M, rows, bad);
+  count_launch();
+}
+
 bool fz_bus_fits(int32_t maxdeg) {
   const size_t md = maxdeg > 0 ? maxdeg : 1;
   return maxdeg <= 32 && md * (kSV * 32 * sizeof(double) + 24) <= kBusSmemMax;
@@ -271,6 +453,16 @@ void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
                    cudaStream_t s) {
   if (n_buses <= 0) return;
+  static_assert(kBusRegMax == 6, "register classes d1..d6");
+  switch (klass) {
+    case 0: return launch_busr<1>(t, buses, n_buses, in, dv, M, rows, bad, s);
+    case 1: return launch_busr<2>(t, buses, n_buses, in, dv, M, rows, bad, s);
+    case 2: return launch_busr<3>(t, buses, n_buses, in, dv, M, rows, bad, s);
+    case 3: return launch_busr<4>(t, buses, n_buses, in, dv, M, rows, bad, s);
+    case 4: return launch_busr<5>(t, buses, n_buses, in, dv, M, rows, bad, s);
+    case 5: return launch_busr<6>(t, buses, n_buses, in, dv, M, rows, bad, s);
+    default: break;
+  }
   const int64_t warps = (int64_t)n_buses * t.tchunks;
   const int md = maxdeg > 0 ? maxdeg : 1;
   int nw = kBW3;
@@ -284,10 +476,7 @@ void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32
     GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBusSmemMax));
     attr = true;
   }
-  static const char* names[kBusClasses] = {"k_fz_bus3<d1>", "k_fz_bus3<d2>", "k_fz_bus3<d3>",
-                                           "k_fz_bus3<d4>", "k_fz_bus3<d5>", "k_fz_bus3<d6>",
-                                           "k_fz_bus3<large>"};
-  KTimer kt(names[klass], s);
+  KTimer kt(klass == kBusRegMax ? "k_fz_bus3<le8>" : "k_fz_bus3<rest>", s);
   if (rows)
     k_fz_bus3<true><<<blocks, nw * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else

@@ -763,19 +763,50 @@ bool opf_kkt_prepare(gn_kkt* K) {
     }
     up(X->blx, blx, s);
     up(X->blgb, blgb, s);
+    // Register-resident classes (buses of exactly DEG = 1..6 lines, no parallel lines):
+    // per incidence the in-column offsets of its neighbour slots, read off the slot
+    // program: (v(o), v(n)) | (th(o), v(n)) << 8 | (th(o), th(n)) << 16, 0xff = absent.
+    std::vector<int32_t> bpos(bl.size(), 0xffffff);
     std::vector<int4> cls[kBusClasses];
     for (int32_t n = 0; n < N; ++n) {
       const int32_t deg = bl_ptr[n + 1] - bl_ptr[n];
       const int32_t np = bprog_ptr[n + 1] - bprog_ptr[n];
-      auto& v = cls[deg <= 1 ? 0 : std::min(deg, kBusClasses) - 1];  // isolated buses too (diagonal)
-      v.push_back(make_int4(n, bl_ptr[n], deg | (np << 8), bprog_ptr[n]));
+      bool simple = deg >= 1 && deg <= kBusRegMax;
+      int32_t jv = 0, jt = 0, boff_n = -1;
+      for (int32_t q = bprog_ptr[n]; q < bprog_ptr[n + 1]; ++q) {
+        const unsigned long long code = bprog[q];
+        const uint32_t mask = static_cast<uint32_t>(code);
+        const int type = static_cast<int>((code >> 32) & 7);
+        const int32_t j = type < 4 ? jv++ : jt++;
+        if (type == 2) boff_n = j;
+        if (type == 1 || type == 3 || type == 5) {
+          if (mask & (mask - 1)) {  // parallel lines: generic kernel
+            simple = false;
+            continue;
+          }
+          const int i = __builtin_ctz(mask), sh = type == 1 ? 0 : (type == 3 ? 8 : 16);
+          int32_t& b = bpos[bl_ptr[n] + i];
+          b = (b & ~(0xff << sh)) | (j << sh);
+        }
+      }
+      if (simple) {
+        cls[deg - 1].push_back(make_int4(n, bl_ptr[n], deg, boff_n));
+      } else {
+        cls[deg <= 8 ? kBusClasses - 2 : kBusClasses - 1].push_back(
+            make_int4(n, bl_ptr[n], deg | (np << 8), bprog_ptr[n]));
+      }
+      auto& v = simple ? cls[deg - 1] : cls[deg <= 8 ? kBusClasses - 2 : kBusClasses - 1];
       v.push_back(make_int4(lent[offs[C_V] + n], lent[offs[C_TH] + n], 0, 0));
     }
+    up(X->bpos, bpos, s);
     for (int k = 0; k < kBusClasses; ++k) {
       up(X->bus_cls[k], cls[k], s);
       if (cls[k].empty()) X->bus_cls[k].alloc(2);
       X->n_bus_cls[k] = static_cast<int32_t>(cls[k].size() / 2);
     }
+    int32_t md = 0;
+    for (size_t i = 0; i < cls[kBusClasses - 1].size(); i += 2) md = std::max(md, cls[kBusClasses - 1][i].z & 255);
+    X->maxdeg_rest = md;
   }
   t.lent = X->lent.p; t.items = X->items.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
   t.fpos = X->fpos.p; t.apos = X->apos.p; t.lidx_to = X->lidx_to.p; t.lidx_from = X->lidx_from.p;
@@ -783,7 +814,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
   t.ngp = X->ngp.p; t.ngq = X->ngq.p; t.bl_ptr = X->bl_ptr.p; t.bl = X->bl.p;
   t.bg_ptr = X->bg_ptr.p; t.bg = X->bg.p; t.nb_ptr = X->nb_ptr.p; t.nb = X->nb.p; t.nb_inc = X->nb_inc.p;
   t.lnb_ptr = X->lnb_ptr.p; t.lnb = X->lnb.p; t.lnbx = X->lnbx.p;
-  t.blx = X->blx.p; t.blgb = X->blgb.p;
+  t.blx = X->blx.p; t.blgb = X->blgb.p; t.bpos = X->bpos.p;
   t.ldesc0 = X->ldesc0.p; t.ldesc1 = X->ldesc1.p;
   t.bprog_ptr = X->bprog_ptr.p; t.bprog = X->bprog.p;
   t.rowptr = K->A.ptr.p; t.colptr = K->M.ptr.p;

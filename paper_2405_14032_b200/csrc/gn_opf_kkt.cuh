@@ -43,6 +43,7 @@ struct OpfKktTab {
   const int32_t* lnbx;                  // [lnb] l' << 4 | t(l') == max << 3 | t(l') == min << 2 | bits
   const int2* blx;                      // [bl] (l << 1 | is_from, other bus) per incident line
   const double2* blgb;                  // [bl] (G, B) per incident line
+  const int32_t* bpos;                  // [bl] neighbour-slot offsets (register bus classes)
   const int32_t* bprog_ptr;             // [N+1] per-bus slot programs of the v(n)/th(n) columns
   const unsigned long long* bprog;      // (row entity << 35 | type << 32 | lane mask)
 };
@@ -59,12 +60,15 @@ struct FIn {
 
 // Bus-column kernel (v(n), th(n) columns): one warp per (bus, period chunk);
 // lanes = (32/P periods) x (P incident-line slots), P = next pow2 >= degree.
-// klass 0..5: buses of klass+1 lines (klass 0: at most one), shared memory sized to
-// the degree; klass 6: every bus with more lines (maxdeg = the network's maximum).
+// Bus-column kernel over one class of buses.  klass 0..5: buses of exactly klass+1
+// lines without parallel lines (line state in registers); klass 6: the other buses
+// of at most 8 lines, klass 7: the rest (slot-program kernel, line state in shared
+// memory sized by maxdeg).
 void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32_t maxdeg,
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows,
                    int32_t* bad, cudaStream_t s);
-constexpr int kBusClasses = 7;
+constexpr int kBusRegMax = 6;
+constexpr int kBusClasses = kBusRegMax + 2;
 bool fz_bus_fits(int32_t maxdeg);  // one warp's shared memory fits (else: no fused path)
 
 struct OpfKkt {
@@ -80,6 +84,8 @@ struct OpfKkt {
   DBuf<unsigned long long> bprog;
   DBuf<int4> bus_cls[kBusClasses];  // bus descriptors by degree class (bus-column kernel)
   DBuf<int2> blx;
+  DBuf<int32_t> bpos;
+  int32_t maxdeg_rest = 0;
   DBuf<double2> blgb;
   int32_t n_bus_cls[kBusClasses] = {};
 };
