@@ -20,6 +20,7 @@
 
 #include "gn_opf_kkt.cuh"
 #include "gn_opf_math.cuh"
+#include "gn_span.cuh"
 
 namespace gnb {
 
@@ -227,71 +228,58 @@ __global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, const double
     dth = dv[t.therm0 + k * T + ts];
   }
   const int64_t basep = __ldg(t.colptr + d1.z * T + c0), baseq = __ldg(t.colptr + d1.w * T + c0);
-  const bool stp = lenp <= kFLCap, stq = lenq <= kFLCap;  // warp-uniform
   const LineState s = line_state(G, B, vf, vt, thf, tht);
   const double jtp = j_thermal(xp), jtq = j_thermal(xq);
-  // ---- values, slot by slot (column p into the stage, column q kept in registers
-  // order-free: q is written after p's span has been flushed)
-  auto flush = [&](int64_t base, int32_t len) {
-    __syncwarp();
-    const int32_t q32 = 32 / len, r32 = 32 - q32 * len;
-    int32_t tq = lane / len, rj = lane - tq * len;
-    for (int32_t e = lane; e < nt * len; e += 32) {
-      M[base + e] = stg[rj * 33 + tq];
-      tq += q32;
-      rj += r32;
-      if (rj >= len) {
-        rj -= len;
-        ++tq;
+  // ---- values, slot by slot; column p, then column q.  Staged (the common case:
+  // both columns <= kFLCap slots) or written in place, a warp-uniform choice.
+  auto columns = [&](auto staged) {
+    constexpr bool ST = decltype(staged)::value;
+    for (int Q = 0; Q < 2; ++Q) {
+      const int64_t pos = ST ? 0 : (valid ? (int64_t)__ldg(t.colptr + (Q ? cqs : cps)) : 0);
+      auto put = [&](int32_t j, double v) {
+        if constexpr (ST) stg[j * 33 + lane] = v;
+        else if (valid) M[pos + j] = v;
+      };
+      const double dlo = Q ? dbq_lo : dbp_lo, dhi = Q ? dbq_hi : dbp_hi, dfl = Q ? dfq : dfp;
+      const double jt = Q ? jtq : jtp;
+      const double sgn_lo = (fl & 16) ? 1.0 : -1.0, sgn_hi = (fl & 32) ? 1.0 : -1.0;
+      {  // diagonal: thermal H (2w) then pairs bal(lo), bal(hi), flow, thermal, dw + Sx
+        double acc = 0.0;
+        if (k >= 0) acc += h_thermal_diag(wth);
+        acc += pair_term(dlo, sgn_lo, sgn_lo);
+        acc += pair_term(dhi, sgn_hi, sgn_hi);
+        acc += pair_term(dfl, 1.0, 1.0);
+        if (k >= 0) acc += pair_term(dth, jt, jt);
+        acc += dw + (Q ? sxq : sxp);
+        put(0, acc);
       }
-    }
-    __syncwarp();
-  };
-  for (int Q = 0; Q < 2; ++Q) {
-    const bool st = Q ? stq : stp;
-    const int64_t pos = st ? 0 : (valid ? (int64_t)__ldg(t.colptr + (Q ? cqs : cps)) : 0);
-    auto put = [&](int32_t j, double v) {
-      if (st) stg[j * 33 + lane] = v;
-      else if (valid) M[pos + j] = v;
-    };
-    const double dlo = Q ? dbq_lo : dbp_lo, dhi = Q ? dbq_hi : dbp_hi, dfl = Q ? dfq : dfp;
-    const double jt = Q ? jtq : jtp;
-    {  // diagonal: thermal H (2w) then pairs bal(lo), bal(hi), flow, thermal, dw + Sx
-      const double sgn_lo = (fl & 16) ? 1.0 : -1.0, sgn_hi = (fl & 32) ? 1.0 : -1.0;
-      double acc = 0.0;
-      if (k >= 0) acc += h_thermal_diag(wth);
-      acc += pair_term(dlo, sgn_lo, sgn_lo);
-      acc += pair_term(dhi, sgn_hi, sgn_hi);
-      acc += pair_term(dfl, 1.0, 1.0);
-      if (k >= 0) acc += pair_term(dth, jt, jt);
-      acc += dw + (Q ? sxq : sxp);
-      put(0, acc);
-    }
-    for (int32_t a = 0; a < nl; ++a) {  // flows l' > l sharing a bus: balance-row pairs
-      const int32_t code = __ldg(t.lnbx + d1.x + a);
-      const double sgn_lo = (fl & 16) ? 1.0 : -1.0, sgn_hi = (fl & 32) ? 1.0 : -1.0;
-      double acc = 0.0;
-      if (code & 1) acc += pair_term(dlo, (code & 4) ? 1.0 : -1.0, sgn_lo);
-      if (code & 2) acc += pair_term(dhi, (code & 8) ? 1.0 : -1.0, sgn_hi);
-      put(1 + a, acc);
-    }
-    int32_t j = 1 + nl;
-    if (!Q && k >= 0) {  // (q(l), p(l)): thermal pair (2q)(2p)
-      double acc = 0.0;
-      acc += pair_term(dth, jtq, jtp);
-      put(j++, acc);
-    }
+      for (int32_t a = 0; a < nl; ++a) {  // flows l' > l sharing a bus: balance-row pairs
+        const int32_t code = __ldg(t.lnbx + d1.x + a);
+        double acc = 0.0;
+        if (code & 1) acc += pair_term(dlo, (code & 4) ? 1.0 : -1.0, sgn_lo);
+        if (code & 2) acc += pair_term(dhi, (code & 8) ? 1.0 : -1.0, sgn_hi);
+        put(1 + a, acc);
+      }
+      int32_t j = 1 + nl;
+      if (!Q && k >= 0) {  // (q(l), p(l)): thermal pair (2q)(2p)
+        double acc = 0.0;
+        acc += pair_term(dth, jtq, jtp);
+        put(j++, acc);
+      }
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {  // v(lo) v(hi) th(lo) th(hi): flow-row pairs
-      if (!(fl & (1 << i))) continue;
-      const int32_t b = (i & 1) ? bhi : blo;
-      const int field = (i & 2) ? (b == f ? 3 : 4) : (b == f ? 1 : 2);
-      double acc = 0.0;
-      acc += pair_term(dfl, Q ? j_flow_q(s, G, B, field) : j_flow_p(s, G, B, field), 1.0);
-      put(j++, acc);
+      for (int i = 0; i < 4; ++i) {  // v(lo) v(hi) th(lo) th(hi): flow-row pairs
+        if (!(fl & (1 << i))) continue;
+        const int32_t b = (i & 1) ? bhi : blo;
+        const int field = (i & 2) ? (b == f ? 3 : 4) : (b == f ? 1 : 2);
+        double acc = 0.0;
+        acc += pair_term(dfl, Q ? j_flow_q(s, G, B, field) : j_flow_p(s, G, B, field), 1.0);
+        put(j++, acc);
+      }
+      if constexpr (ST) warp_span_flush(M, Q ? baseq : basep, stg, Q ? lenq : lenp, nt, lane);
     }
-    if (st) flush(Q ? baseq : basep, Q ? lenq : lenp);
-  }
+  };
+  if (lenp <= kFLCap && lenq <= kFLCap) columns(std::true_type{});
+  else columns(std::false_type{});
 }
 
 template <bool STRUCT>
@@ -363,37 +351,7 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 //   * angle rows of a line (all periods): (+1, -1) at the free angle slots;
 //   * ramp rows: one thread per row.
 constexpr int kSJW = 8;  // warps per CTA
-__device__ __forceinline__ void warp_flush(double* __restrict__ A, int64_t base, const double* stg,
-                                           int32_t len, int32_t nt, int lane) {
-  __syncwarp();
-  const int32_t q32 = 32 / len, r32 = 32 - q32 * len;
-  int32_t tq = lane / len, rj = lane - tq * len;
-  for (int32_t e = lane; e < nt * len; e += 32) {
-    A[base + e] = stg[rj * 33 + tq];
-    tq += q32;
-    rj += r32;
-    if (rj >= len) {
-      rj -= len;
-      ++tq;
-    }
-  }
-  __syncwarp();
-}
-
-// span of T rows of `len` constant slots; lane j < len holds slot j's value
-__device__ __forceinline__ void warp_const_rows(double* __restrict__ A, int64_t base, double v,
-                                                int32_t len, int32_t T, int lane) {
-  const int32_t r32 = 32 % len, n = T * len;
-  int32_t rj = lane % len;
-  for (int32_t e0 = 0; e0 < n; e0 += 32) {  // warp-uniform trip count (full-mask shuffle)
-    const double val = __shfl_sync(0xffffffffu, v, rj);
-    if (e0 + lane < n) A[base + e0 + lane] = val;
-    rj += r32;
-    if (rj >= len) rj -= len;
-  }
-}
-
-__global__ void __launch_bounds__(kSJW * 32) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
+__global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
                                                                 const double* __restrict__ x,
                                                                 double* __restrict__ A) {
   __shared__ double stg_all[kSJW * 5 * 33];
@@ -438,11 +396,11 @@ __global__ void __launch_bounds__(kSJW * 32) k_opf_set_jac_fused(OpfKktTab t, in
 #pragma unroll
     for (int fl = 0; fl < 5; ++fl)
       if (pos[fl] >= 0) stg[pos[fl] * 33 + lane] = 0.0 + j_flow_p(s, G, B, fl);
-    warp_flush(A, bp, stg, len, nt, lane);
+    warp_span_flush(A, bp, stg, len, nt, lane);
 #pragma unroll
     for (int fl = 0; fl < 5; ++fl)
       if (pos[fl] >= 0) stg[pos[fl] * 33 + lane] = 0.0 + j_flow_q(s, G, B, fl);
-    warp_flush(A, bq, stg, len, nt, lane);
+    warp_span_flush(A, bq, stg, len, nt, lane);
     return;
   }
   wg -= (int64_t)t.L * tch;
