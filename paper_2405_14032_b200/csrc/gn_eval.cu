@@ -48,7 +48,9 @@ __device__ __forceinline__ void const_out(double* __restrict__ out, int nb,
 }
 
 // ---------------------------------------------------------------- lines
-// Patterns 1, 2 (balance-flow J/H), 7, 8 (flow definitions), 10 (angle).
+// Patterns 1, 2 (balance-flow J/H), 7, 8 (flow definitions), 10 (angle), and
+// 12 (thermal) for rated lines: its rows / records of (line k, period t) are
+// written by the same thread, which already holds p and q.
 template <int MODE>
 __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const double* __restrict__ x,
                                               const double* __restrict__ w,
@@ -61,9 +63,12 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
   const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
   const bool valid = r < nrec;
   double p = 0, q = 0, G = 0, B = 0, vf = 0, vt = 0, thf = 0, tht = 0;
+  int64_t rk = -1;  // record of the line's thermal pattern (12: p^2 + q^2 <= smax^2), if rated
   if (valid) {
     const int32_t l = (int32_t)(r / d.T), t = (int32_t)(r - (int64_t)l * d.T);
     const int32_t f = __ldg(net.lf + l), to = __ldg(net.lt + l);
+    const int32_t k = __ldg(net.l_therm + l);
+    if (k >= 0) rk = (int64_t)k * d.T + t;
     G = __ldg(net.lg + l);
     B = __ldg(net.lb + l);
     p = x[d.p0 + r];
@@ -86,6 +91,11 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
       if (!isfinite(gp)) report(st, d.pid[K_FLOW_P], r);
       if (!isfinite(gq)) report(st, d.pid[K_FLOW_Q], r);
       if (!isfinite(ga)) report(st, d.pid[K_ANGLE], r);
+      if (rk >= 0) {  // thermal row of the same (line, period)
+        const double v = g_thermal(p, q);
+        out[d.therm0 + rk] = v;
+        if (!isfinite(v)) report(st, d.pid[K_THERMAL], rk);
+      }
     }
   } else if constexpr (MODE == EV_J) {
     // balance flows: (+1 to-record, -1 from-record); angle: (1, -1)
@@ -111,6 +121,12 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
     }
     stage_out<5>(sm, jp, valid, out + d.jac_off[K_FLOW_P] + 5 * r0, nb);
     stage_out<5>(sm, jq, valid, out + d.jac_off[K_FLOW_Q] + 5 * r0, nb);
+    if (rk >= 0) {  // thermal [p, q]: (2p, 2q)
+      const double j0 = j_thermal(p), j1 = j_thermal(q);
+      out[d.jac_off[K_THERMAL] + 2 * rk] = j0;
+      out[d.jac_off[K_THERMAL] + 2 * rk + 1] = j1;
+      if (!(isfinite(j0) && isfinite(j1))) report(st, d.pid[K_THERMAL], rk);
+    }
   } else {  // EV_H
     const double z2[2] = {0.0, 0.0};
     const double z3[3] = {0.0, 0.0, 0.0};
@@ -140,6 +156,18 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
     }
     stage_out<15>(sm, hp, valid, out + d.hess_off[K_FLOW_P] + 15 * r0, nb);
     stage_out<15>(sm, hq, valid, out + d.hess_off[K_FLOW_Q] + 15 * r0, nb);
+    if (rk >= 0) {  // thermal: (2a, 0, 2a), a = the row weight (zeros when a == 0)
+      const double a = w[d.therm0 + rk];
+      double h0 = 0.0;
+      if (a != 0.0) {
+        h0 = h_thermal_diag(a);
+        if (!(isfinite(h0) && isfinite(p) && isfinite(q))) report(st, d.pid[K_THERMAL], rk);
+      }
+      double* o = out + d.hess_off[K_THERMAL] + 3 * rk;
+      o[0] = h0;
+      o[1] = 0.0;
+      o[2] = h0;
+    }
   }
 }
 
@@ -223,47 +251,6 @@ __global__ void k_sum_partials(const double* __restrict__ part, int n, double* o
 
 // ----------------------------------------------------------------- thermal
 // Pattern 9: p^2 + q^2 over rated lines (opf.hpp:323-332).
-template <int MODE>
-__global__ void __launch_bounds__(kBS) k_thermal(OpfDims d, DevNet net,
-                                                 const double* __restrict__ x,
-                                                 const double* __restrict__ w,
-                                                 double* __restrict__ out,
-                                                 unsigned long long* st) {
-  __shared__ double sm[kBS * 3];
-  const int64_t nrec = (int64_t)d.LT * d.T;
-  const int64_t r0 = (int64_t)blockIdx.x * kBS;
-  const int64_t r = r0 + threadIdx.x;
-  const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
-  const bool valid = r < nrec;
-  double p = 0.0, q = 0.0;
-  if (valid) {
-    const int32_t k = (int32_t)(r / d.T), t = (int32_t)(r - (int64_t)k * d.T);
-    const int32_t l = __ldg(net.th_line + k);
-    p = x[d.p0 + (int64_t)l * d.T + t];
-    q = x[d.q0 + (int64_t)l * d.T + t];
-  }
-  if constexpr (MODE == EV_G) {
-    if (valid) {
-      const double v = g_thermal(p, q);
-      out[d.therm0 + r] = v;
-      if (!isfinite(v)) report(st, d.pid[K_THERMAL], r);
-    }
-  } else if constexpr (MODE == EV_J) {
-    double j[2] = {j_thermal(p), j_thermal(q)};
-    if (valid && !(isfinite(j[0]) && isfinite(j[1]))) report(st, d.pid[K_THERMAL], r);
-    stage_out<2>(sm, j, valid, out + d.jac_off[K_THERMAL] + 2 * r0, nb);
-  } else {
-    const double a = valid ? w[d.therm0 + r] : 0.0;
-    double h[3] = {0.0, 0.0, 0.0};
-    if (a != 0.0) {
-      h[0] = h_thermal_diag(a);
-      h[2] = h_thermal_diag(a);
-      if (valid && !(isfinite(h[0]) && isfinite(p) && isfinite(q)))
-        report(st, d.pid[K_THERMAL], r);
-    }
-    stage_out<3>(sm, h, valid, out + d.hess_off[K_THERMAL] + 3 * r0, nb);
-  }
-}
 
 // -------------------------------------------------------------------- ramp
 // Pattern 11: pg(g,t) - pg(g,t-1), t = 1..T-1 (opf.hpp:343-351).
@@ -344,7 +331,7 @@ static unsigned nblk(int64_t n) { return (unsigned)((n + kBS - 1) / kBS); }
 void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
                  const double* w, double ow, double* out, double* fpart,
                  unsigned long long* st, cudaStream_t s) {
-  const int64_t nl = (int64_t)d.L * d.T, ng = (int64_t)d.G * d.T, nt = (int64_t)d.LT * d.T,
+  const int64_t nl = (int64_t)d.L * d.T, ng = (int64_t)d.G * d.T,
                 nr = d.pid[K_RAMP] >= 0 ? (int64_t)d.GR * d.R : 0,
                 nb = (int64_t)d.N * d.T;
   switch (mode) {
@@ -368,7 +355,6 @@ void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
     case EV_G:
       if (nb) { KTimer kt("k_bus<G>", s); k_bus<<<nblk(nb), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
       if (nl) { KTimer kt("k_line<G>", s); k_line<EV_G><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
-      if (nt) { KTimer kt("k_thermal<G>", s); k_thermal<EV_G><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
       if (nr) { KTimer kt("k_ramp<G>", s); k_ramp<EV_G><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
       break;
     case EV_J:
@@ -383,12 +369,6 @@ void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
         KTimer kt(mode == EV_J ? "k_gen<J>" : "k_gen<H>", s);
         if (mode == EV_J) k_gen<EV_J><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
         else k_gen<EV_H><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
-        count_launch();
-      }
-      if (nt) {
-        KTimer kt(mode == EV_J ? "k_thermal<J>" : "k_thermal<H>", s);
-        if (mode == EV_J) k_thermal<EV_J><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st);
-        else k_thermal<EV_H><<<nblk(nt), kBS, 0, s>>>(d, net, x, w, out, st);
         count_launch();
       }
       if (nr) {
