@@ -21,6 +21,9 @@
 #include <cstdlib>
 
 #include "gn_opf_kkt.cuh"
+
+// (the STRUCT instantiations return before the value code: "loop is not reachable")
+#pragma nv_diag_suppress 128
 #include "gn_opf_math.cuh"
 
 namespace gnb {
