@@ -297,7 +297,7 @@ def run_ours(args, rank, world, local_rank, dist):
     def step(ev=None, serial=False):
         """One unit; serial=True runs the KKT on the callback stream (per-kernel timing)."""
         ks = stream if serial else kstream
-        kkt.set_stream(ks.cuda_stream)
+        kkt.set_stream(ks.cuda_stream)  # no-op (no sync) when unchanged: capturable
 
         def mark(i, st=None):
             if ev is not None:
@@ -368,6 +368,32 @@ def run_ours(args, rank, world, local_rank, dist):
     per_stage = {k: float(np.mean([ev[a].elapsed_time(ev[b]) for ev in events]))
                  for k, (a, b) in spans.items()}
     ms = float(per_step.mean())
+    eager_ms = ms
+    # ---- CUDA graph (one graph per unit of work on device-resident
+    # buffers).  The whole step -- both streams, fork/join events included -- is
+    # captured once and replayed; this is the production launch mode and `value`.
+    graph_mode = args.graph and halo is None
+    if graph_mode:
+        graph = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+        for _ in range(args.warmup):
+            graph.replay()
+        torch.cuda.synchronize()
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        t_clk0 = clocks.mark()
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+                gev[k][0].record(stream)
+                graph.replay()
+                gev[k][1].record(stream)
+        torch.cuda.synchronize()
+        clk = clocks.stop(t_clk0, clocks.mark())
+        assert nlp.status(), "evaluation failed in the graph-timed region"
+        ms = float(np.mean([a.elapsed_time(b) for a, b in gev]))
     if dist:
         import torch.distributed as tdist
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
@@ -511,6 +537,7 @@ def run_ours(args, rank, world, local_rank, dist):
                      "contract: set_jacobian(J) + assemble(H) read the callback outputs")
                     + (f"; {args.streams} streams"),
         "stages_ms": per_stage,
+        "launch": ("cuda_graph (eager step %.4f ms)" % eager_ms) if graph_mode else "eager",
         "setup_s": setup_s,
         "clocks": clk,
         "e2e": e2e,
@@ -621,7 +648,7 @@ def run_reference(args, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=CONFIG)
@@ -633,6 +660,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
     ap.add_argument("--streams", type=int, choices=[1, 2], default=2)
+    ap.add_argument("--graph", type=int, choices=[0, 1], default=1,
+                    help="replay the step as one CUDA graph (single rank / no halo)")
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
     args = ap.parse_args()
 

@@ -130,7 +130,9 @@ int gn_ctx_create_shard(const gn_network* net, int32_t periods_total, int32_t fi
  *         gn_lifted_create)]; ramp_gens[n_ramp_gens] (may be NULL). */
 int gn_ctx_shard_info(gn_ctx* ctx, int64_t* info, int32_t* ramp_gens);
 int gn_ctx_destroy(gn_ctx* ctx);
-/* Use a caller-owned cudaStream_t (as void*) for every launch of this context. */
+/* Use a caller-owned cudaStream_t (as void*) for every launch of this context; NULL
+ * returns to the context's own stream, which lives until gn_ctx_destroy (a KKT
+ * created on it keeps using it).  Work already enqueued is synchronised first. */
 int gn_ctx_set_stream(gn_ctx* ctx, void* cuda_stream);
 int gn_ctx_get_stream(gn_ctx* ctx, void** cuda_stream);
 /* Synchronises the stream, returns (and clears) the latched evaluation status. */
@@ -189,6 +191,7 @@ int gn_kkt_create(int32_t n, int32_t m, int64_t jac_nnz, const int32_t* jac_rows
  * KKT shares the context's stream. */
 int gn_kkt_create_lifted(gn_ctx* ctx, gn_kkt** out, gn_error* err);
 int gn_kkt_destroy(gn_kkt* kkt);
+/* As gn_ctx_set_stream, for the KKT's launches. */
 int gn_kkt_set_stream(gn_kkt* kkt, void* cuda_stream);
 /* dims = [dim, a_nnz, m_nnz, pair_count, jac_nnz, hess_nnz, n_rows, opf_ready,
  *         fused_ready] (opf_ready / fused_ready = 1 when the OPF-specialised /

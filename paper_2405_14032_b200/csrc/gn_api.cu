@@ -210,6 +210,7 @@ static int ctx_create(const gn_network* net, int32_t periods_total, int32_t firs
 
   GN_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   c->own_stream = true;
+  c->owned_stream = c->stream;
   cudaStream_t s = c->stream;
 
   // SoA tables
@@ -305,10 +306,9 @@ int gn_ctx_destroy(gn_ctx* c) {
   if (!c) return GN_OK;
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
-  cudaStream_t s = c->stream;
-  const bool own = c->own_stream;
+  cudaStream_t s = c->owned_stream;  // the caller's stream (set_stream) is never destroyed
   delete c;
-  if (own && s) cudaStreamDestroy(s);
+  if (s) cudaStreamDestroy(s);
   return GN_OK;
 }
 
@@ -316,10 +316,12 @@ int gn_ctx_set_stream(gn_ctx* c, void* stream) {
   if (!c) return GN_ERR_INVALID;
   API_TRY
   set_device(c->device);
+  if ((stream ? static_cast<cudaStream_t>(stream) : c->owned_stream) == c->stream) return GN_OK;
   GN_CK(cudaStreamSynchronize(c->stream));
-  if (c->own_stream) cudaStreamDestroy(c->stream);
-  c->stream = static_cast<cudaStream_t>(stream);
-  c->own_stream = false;
+  // the context's own stream stays alive until gn_ctx_destroy: a KKT created on it
+  // may still reference it
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->owned_stream;
+  c->own_stream = c->stream == c->owned_stream;
   return GN_OK;
   API_CATCH(nullptr)
 }
@@ -529,6 +531,7 @@ int gn_kkt_create(int32_t n, int32_t m, int64_t nj, const int32_t* jr, const int
   K->n = n; K->m = m; K->nj = nj; K->nh = nh;
   GN_CK(cudaStreamCreateWithFlags(&K->stream, cudaStreamNonBlocking));
   K->own_stream = true;
+  K->owned_stream = K->stream;
   DBuf<int32_t> djr, djc, dhr, dhc;
   djr.upload(jr, nj, K->stream); djc.upload(jc, nj, K->stream);
   dhr.upload(hr, nh, K->stream); dhc.upload(hc, nh, K->stream);
@@ -579,11 +582,10 @@ int gn_kkt_destroy(gn_kkt* K) {
   if (!K) return GN_OK;
   cudaSetDevice(K->device);
   if (K->stream) cudaStreamSynchronize(K->stream);
-  cudaStream_t s = K->stream;
-  const bool own = K->own_stream;
+  cudaStream_t s = K->owned_stream;
   gnb::opf_kkt_free(K);
   delete K;
-  if (own && s) cudaStreamDestroy(s);
+  if (s) cudaStreamDestroy(s);
   return GN_OK;
 }
 
@@ -591,10 +593,10 @@ int gn_kkt_set_stream(gn_kkt* K, void* stream) {
   if (!K) return GN_ERR_INVALID;
   API_TRY
   set_device(K->device);
+  if ((stream ? static_cast<cudaStream_t>(stream) : K->owned_stream) == K->stream) return GN_OK;
   GN_CK(cudaStreamSynchronize(K->stream));
-  if (K->own_stream) cudaStreamDestroy(K->stream);
-  K->stream = static_cast<cudaStream_t>(stream);
-  K->own_stream = false;
+  K->stream = stream ? static_cast<cudaStream_t>(stream) : K->owned_stream;
+  K->own_stream = K->stream == K->owned_stream;
   return GN_OK;
   API_CATCH(nullptr)
 }

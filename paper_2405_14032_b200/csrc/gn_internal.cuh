@@ -137,6 +137,7 @@ struct gn_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t owned_stream = nullptr;  // created here; destroyed with the object
   gnb::OpfDims d{};
   // host copies of the network (bounds, starts)
   std::vector<double> bus_vmin, bus_vmax, vm_start, va_start;

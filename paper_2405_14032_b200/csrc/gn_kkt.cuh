@@ -25,6 +25,7 @@ struct gn_kkt {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t owned_stream = nullptr;  // created here; destroyed with the object
   gn_ctx* ctx = nullptr;  // set for gn_kkt_create_lifted
   int32_t n = 0, m = 0;
   int64_t nj = 0, nh = 0, npair = 0;

@@ -314,3 +314,26 @@ def test_fused_kkt_equals_contract_path_edge_network(gpu, T):
     sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, T + 2)
     _fused_check(nlp, K, x, w, 0.7, sx, ss)
     _fused_check(nlp, K, x, w, 0.0, sx, ss)  # restoration-style obj_weight 0
+
+
+def test_stream_switching_any_order(gpu):
+    """set_stream on the context, then on a KKT created before it (which still
+    referenced the context's own stream), then back to the own streams."""
+    import torch
+    from paper_2405_14032_b200.opf import load_profile
+    raw = synthetic_case(60, 100, 15, 50, seed=9)
+    net = raw.network()
+    nlp = OpfNlp(net, 3, load_profile(net.n_load, 3))
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    st = torch.cuda.Stream()
+    nlp.set_stream(st.cuda_stream)
+    K.set_stream(st.cuda_stream)
+    xl, xu, xs, _, _ = nlp.bounds()
+    ok, g1 = nlp.eval_g(xs)
+    assert ok
+    nlp.set_stream(0)
+    K.set_stream(0)
+    ok, g2 = nlp.eval_g(xs)
+    assert ok and np.array_equal(g1, g2)
+    K.close()
