@@ -416,6 +416,23 @@ def run_ours(args, rank, world, local_rank, dist):
     unit_bytes = alg_bytes(s, kkt)
     unit_gbs = unit_bytes / (ms * 1e-3) / 1e9
 
+    # line-search trial point: f and g only, one call (gn_eval_fg)
+    tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(10)]
+    for a_, b_ in tev:
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            a_.record(stream)
+            nlp.eval_device("fg", dx, (f, g), sync=False)
+            b_.record(stream)
+    torch.cuda.synchronize()
+    assert nlp.status()
+    trial_ms = float(np.median([a_.elapsed_time(b_) for a_, b_ in tev]))
+    trial_bytes = 8 * (s.n_vars + s.n_cons + 1)  # x read once, g and f written once
+    trial = {"ms": trial_ms, "alg_bytes": trial_bytes,
+             "gbs": trial_bytes / (trial_ms * 1e-3) / 1e9,
+             "frac": trial_bytes / (trial_ms * 1e-3) / 1e9 / peak}
+
     # ---------------------------------------------------------- e2e (host data)
     # (1) e2e: a device-resident IPM's iteration seen from the host.  Every step
     # copies its inputs (x, w, Sigma_x, Sigma_s) from pinned host memory, runs the
@@ -537,6 +554,7 @@ def run_ours(args, rank, world, local_rank, dist):
                      "contract: set_jacobian(J) + assemble(H) read the callback outputs")
                     + (f"; {args.streams} streams"),
         "stages_ms": per_stage,
+        "line_search_trial": trial,
         "launch": ("cuda_graph (eager step %.4f ms)" % eager_ms) if graph_mode else "eager",
         "setup_s": setup_s,
         "clocks": clk,

@@ -162,6 +162,11 @@ int gn_eval_jac(gn_ctx* ctx, const double* x, double* out, int mem, gn_error* er
 int gn_eval_hess(gn_ctx* ctx, const double* x, const double* row_weights,
                  double obj_weight, double* out, int mem, gn_error* err);
 
+/* Line-search trial point (solver.hpp:267-304 evaluates f and g at each trial):
+ * eval_f and eval_g in one call, no derivative work, one status (the
+ * lexicographically first failing (pattern, record) over both). */
+int gn_eval_fg(gn_ctx* ctx, const double* x, double* f, double* g, int mem, gn_error* err);
+
 /* ---------------------------------------------------------------- lifted */
 /* LiftedProblem constructor filter (lifted.hpp:25-100): free map, slack
  * boxes (relative relaxation), J/H picks.  Built on the device. */

@@ -79,6 +79,7 @@ _SIGS = {
     "gn_eval_jac": (C.c_int, [vp, f64p, f64p, C.c_int, C.POINTER(GnError)]),
     "gn_eval_hess": (C.c_int, [vp, f64p, f64p, C.c_double, f64p, C.c_int,
                                C.POINTER(GnError)]),
+    "gn_eval_fg": (C.c_int, [vp, f64p, f64p, f64p, C.c_int, C.POINTER(GnError)]),
     "gn_lifted_create": (C.c_int, [vp, C.c_double, C.POINTER(GnError)]),
     "gn_lifted_structure": (C.c_int, [vp, i32p, i32p, i32p, i32p, i32p, i32p, i32p, f64p,
                                       f64p, C.c_int]),

@@ -437,6 +437,37 @@ int gn_eval_hess(gn_ctx* c, const double* x, const double* w, double ow, double*
   return eval(c, gnb::EV_H, x, w, ow, out, mem, err);
 }
 
+// Line-search trial point (solver.hpp:267-304): the objective and
+// the constraint values only -- no derivative kernels -- under one status word.
+int gn_eval_fg(gn_ctx* c, const double* x, double* f, double* g, int mem, gn_error* err) {
+  if (!c) return fail(err, GN_ERR_INVALID, "null context");
+  if (!x || !f || !g) return fail(err, GN_ERR_INVALID, "null array");
+  API_TRY
+  set_device(c->device);
+  const auto& d = c->d;
+  cudaStream_t s = c->stream;
+  const double* dx = x;
+  double *df = f, *dg = g;
+  if (!is_device(mem)) {
+    c->sx.upload(x, d.n, s);
+    dx = c->sx.p;
+    if (c->sout.n < static_cast<size_t>(d.m) + 1) c->sout.alloc(static_cast<size_t>(d.m) + 1);
+    dg = c->sout.p;
+    df = c->sout.p + d.m;
+  }
+  if (!is_async(mem))
+    GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof(unsigned long long), s));
+  gnb::launch_eval(gnb::EV_F, d, c->net(), dx, nullptr, 0.0, df, c->fpart.p, c->status.p, s);
+  gnb::launch_eval(gnb::EV_G, d, c->net(), dx, nullptr, 0.0, dg, c->fpart.p, c->status.p, s);
+  if (is_async(mem)) return ok(err);
+  if (!is_device(mem)) {
+    GN_CK(cudaMemcpyAsync(g, dg, sizeof(double) * d.m, cudaMemcpyDeviceToHost, s));
+    GN_CK(cudaMemcpyAsync(f, df, sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  return take_status(c, err);
+  API_CATCH(err)
+}
+
 // ------------------------------------------------------------------- lifted
 int gn_lifted_create(gn_ctx* c, double relax, gn_error* err) {
   if (!c) return fail(err, GN_ERR_INVALID, "null context");

@@ -186,6 +186,15 @@ class OpfNlp:
     def eval_jac(self, x, out=None):
         return self._eval_vec(self.lib.gn_eval_jac, x, self.sizes.jac_nnz, out=out)
 
+    def eval_fg(self, x, g_out=None):
+        """Line-search trial point: (ok, f, g) from one call, no derivative work."""
+        g_out = np.empty(self.n_cons()) if g_out is None else g_out
+        f = np.empty(1)
+        err = GnError()
+        ok = self._record(self.lib.gn_eval_fg(self.h, _f64(x), _f64(f), _f64(g_out), GN_MEM_HOST,
+                                              C.byref(err)), err)
+        return ok, float(f[0]), g_out
+
     def eval_hess(self, x, row_weights, obj_weight: float, out=None):
         out = np.empty(self.sizes.hess_nnz) if out is None else out
         err = GnError()
@@ -207,6 +216,8 @@ class OpfNlp:
             rc = L.gn_eval_g(self.h, _f64(x), _f64(out), mem, C.byref(err))
         elif which == "jac":
             rc = L.gn_eval_jac(self.h, _f64(x), _f64(out), mem, C.byref(err))
+        elif which == "fg":  # out = (f, g) device buffers
+            rc = L.gn_eval_fg(self.h, _f64(x), _f64(out[0]), _f64(out[1]), mem, C.byref(err))
         elif which == "hess":
             rc = L.gn_eval_hess(self.h, _f64(x), _f64(w), float(ow), _f64(out), mem,
                                 C.byref(err))

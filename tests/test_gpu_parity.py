@@ -337,3 +337,25 @@ def test_stream_switching_any_order(gpu):
     ok, g2 = nlp.eval_g(xs)
     assert ok and np.array_equal(g1, g2)
     K.close()
+
+
+def test_line_search_trial_fg(gpu):
+    """gn_eval_fg: f and g of a trial point in one call, bit-identical
+    to eval_f + eval_g; a failure reports the first failing (pattern, record) of
+    the pair, as the reference's eval_f-then-eval_g does."""
+    nlp, z, meta, net = _nlp("synth_T3")
+    ok, f, g = nlp.eval_fg(z["x"])
+    okf, fr = nlp.eval_f(z["x"])
+    okg, gr = nlp.eval_g(z["x"])
+    assert ok and okf and okg
+    assert f == fr and np.array_equal(g, gr)
+    orc = B.OracleModel(net, meta["periods"], z["scale"])
+    n = meta["sizes"][0]
+    for idx in (n // 2, 5):  # a flow (g fails), a generator (f fails first)
+        xb = z["x"].copy()
+        xb[idx] = np.nan
+        ok, _, _ = nlp.eval_fg(xb)
+        oko, _, failf = orc.eval_f(xb)
+        okg, _, failg = orc.eval_g(xb)
+        assert ok == (oko and okg)
+        assert nlp.last_error == (failf if not oko else failg)
