@@ -237,6 +237,64 @@ int gn_compress_to_csc(int32_t nrows, int32_t ncols, int64_t nnz, const int32_t*
                        const int32_t* cols, int32_t* colptr, int32_t* rowidx,
                        int32_t* slot_map, int32_t* nnz_out, gn_error* err);
 
+/* ------------------------------------------ device-resident IPM vector ops
+ * (SURVEY §8(f)1-2): the per-iteration vector work of ipm::IpmSolver on the
+ * lifted problem of a gn_kkt_create_lifted() KKT, so that x, s, y, z and the
+ * residuals stay in HBM.  Every vector argument is a device pointer (mem =
+ * GN_MEM_DEVICE or GN_MEM_DEVICE_ASYNC; GN_MEM_HOST is GN_ERR_UNSUPPORTED);
+ * scalar results are written to device doubles.  Sizes: n = n_free (lifted
+ * variables), m = n_cons.  Element-wise results and the sparse products are
+ * bit-identical to the reference (same operation order, -fmad=false); whole-
+ * vector sums use a fixed reduction tree (deterministic, equal to the
+ * reference's sequential sums to rounding). */
+typedef struct gn_ipm gn_ipm;
+typedef struct { const double *x, *s, *y, *zlx, *zux, *zls, *zus; } gn_iterate;  /* Iterate (iterate.hpp:16-19) */
+typedef struct { double *px, *ps, *py, *pzlx, *pzux, *pzls, *pzus; } gn_residuals; /* Residuals (:31-34) */
+typedef struct { double *dx, *ds, *dy, *dzlx, *dzux, *dzls, *dzus; } gn_direction; /* Direction (:23-26) */
+
+/* Bounds of the lifted problem: x_lower/x_upper[n], s_lower/s_upper[m] (+-inf = absent). */
+int gn_ipm_create(gn_kkt* kkt, const double* x_lower, const double* x_upper,
+                  const double* s_lower, const double* s_upper, int mem, gn_ipm** out,
+                  gn_error* err);
+int gn_ipm_destroy(gn_ipm* ipm);
+/* jac_transpose_multiply / jac_multiply (iterate.hpp:42-62) on the lifted J COO values. */
+int gn_ipm_jac_transpose_multiply(gn_ipm* ipm, const double* jac_vals, const double* y,
+                                  double* out_n, int mem);
+int gn_ipm_jac_multiply(gn_ipm* ipm, const double* jac_vals, const double* x, double* out_m,
+                        int mem);
+/* compute_residuals (iterate.hpp:64-97). */
+int gn_ipm_residuals(gn_ipm* ipm, const gn_iterate* it, const double* grad, const double* g,
+                     const double* jac_vals, double mu, const gn_residuals* r, int mem);
+/* bound_condensation (iterate.hpp:99-145): sigma_x[n], sigma_s[m], qx[n], qs[m]. */
+int gn_ipm_bound_condensation(gn_ipm* ipm, const gn_iterate* it, const gn_residuals* r,
+                              double* sigma_x, double* sigma_s, double* qx, double* qs, int mem);
+/* fraction_to_boundary (iterate.hpp:147-198): out2 = {primal, dual}. */
+int gn_ipm_fraction_to_boundary(gn_ipm* ipm, const gn_iterate* it, const gn_direction* d,
+                                double tau, double* out2, int mem);
+/* barrier_value (iterate.hpp:200-218); f is a host double, out a device double. */
+int gn_ipm_barrier_value(gn_ipm* ipm, double f, const double* x, const double* s, double mu,
+                         double* out, int mem);
+/* barrier_slope (iterate.hpp:220-236). */
+int gn_ipm_barrier_slope(gn_ipm* ipm, const double* grad, const gn_iterate* it,
+                         const gn_direction* d, double mu, double* out, int mem);
+/* constraint_violation (iterate.hpp:238-244). */
+int gn_ipm_constraint_violation(gn_ipm* ipm, const double* g, const double* s, double* out,
+                                int mem);
+/* kkt_error (iterate.hpp:246-298): out3 = {stat, feas, comp}. */
+int gn_ipm_kkt_error(gn_ipm* ipm, const gn_iterate* it, const gn_residuals* r, double mu,
+                     double* out3, int mem);
+/* recover_bound_steps (condensed.hpp:187-212): reads d->dx, d->ds, writes d->dz*. */
+int gn_ipm_recover_bound_steps(gn_ipm* ipm, const gn_iterate* it, const gn_residuals* r,
+                               const gn_direction* d, int mem);
+/* CondensedKkt::solve around the LDL^T (condensed.hpp:150-172), with the sigma_s,
+ * delta_w, delta_c of the last assemble: rhs[n] = -(qx + A^T (c.qs + d.qy)) before
+ * the factor solve; ds, dy from the solved dx after it. */
+int gn_kkt_solve_rhs(gn_ipm* ipm, const double* qx, const double* qs, const double* qy,
+                     const double* sigma_s, double delta_w, double delta_c, double* rhs, int mem);
+int gn_kkt_solve_finish(gn_ipm* ipm, const double* dx, const double* qs, const double* qy,
+                        const double* sigma_s, double delta_w, double delta_c, double* ds,
+                        double* dy, int mem);
+
 #ifdef __cplusplus
 }
 #endif

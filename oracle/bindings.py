@@ -83,6 +83,14 @@ def ref_available() -> bool:
     return REF_LIB.exists()
 
 
+f64pp = C.POINTER(C.POINTER(C.c_double))
+
+
+def _pp(arrays):
+    """double*[k] over float64 numpy arrays (kept alive by the caller)."""
+    return (C.POINTER(C.c_double) * len(arrays))(*[_f(a) for a in arrays])
+
+
 def ref_lib():
     global _ref
     if _ref is None:
@@ -120,6 +128,19 @@ def ref_lib():
             "gnr_compress_to_csc": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, i32p, i32p,
                                               i32p, i32p, i32p]),
             "gnr_solve": (None, [vp, C.c_double, C.c_int, f64p]),
+            "gnr_lifted_bounds": (None, [vp, f64p, f64p, f64p, f64p]),
+            "gnr_ipm_jac_t": (None, [vp, f64p, f64p, f64p]),
+            "gnr_ipm_jac": (None, [vp, f64p, f64p, f64p]),
+            "gnr_ipm_residuals": (None, [vp, f64pp, f64pp, f64p, f64p, f64p, C.c_double, f64pp]),
+            "gnr_ipm_condense": (None, [vp, f64pp, f64pp, f64pp, f64p, f64p, f64p, f64p]),
+            "gnr_ipm_ftb": (None, [vp, f64pp, f64pp, f64pp, C.c_double, f64p]),
+            "gnr_ipm_barrier": (C.c_double, [vp, f64pp, C.c_double, f64p, f64p, C.c_double]),
+            "gnr_ipm_slope": (C.c_double, [vp, f64pp, f64p, f64pp, f64pp, C.c_double]),
+            "gnr_ipm_violation": (C.c_double, [vp, f64p, f64p]),
+            "gnr_ipm_kkt_error": (None, [vp, f64pp, f64pp, f64pp, C.c_double, f64p]),
+            "gnr_ipm_recover": (None, [vp, f64pp, f64pp, f64pp, f64pp, f64pp]),
+            "gnr_kkt_solve_parts": (None, [vp, f64p, f64p, f64p, f64p, C.c_double, C.c_double,
+                                           f64p, f64p, f64p, f64p]),
         }
         for k, (r, a) in sig.items():
             getattr(L, k).restype = r
@@ -402,6 +423,72 @@ class RefModel(_ModelBase):
         m = np.empty(self.kkt_sizes[2])
         self.L.gnr_kkt_values(self.h, _f(a), _f(m))
         return a, m
+
+    # ---- ipm/iterate.hpp vector ops on the lifted problem (arrays in the
+    # Iterate / Residuals / Direction field order x s y zlx zux zls zus)
+    def lifted_bounds(self):
+        n, m = self.lifted_sizes[0], self.lifted_sizes[1]
+        b = [np.empty(n), np.empty(n), np.empty(m), np.empty(m)]
+        self.L.gnr_lifted_bounds(self.h, *[_f(a) for a in b])
+        return b
+
+    def ipm_jac_t(self, jv, y):
+        out = np.empty(self.lifted_sizes[0])
+        self.L.gnr_ipm_jac_t(self.h, _f(jv), _f(y), _f(out))
+        return out
+
+    def ipm_jac(self, jv, x):
+        out = np.empty(self.lifted_sizes[1])
+        self.L.gnr_ipm_jac(self.h, _f(jv), _f(x), _f(out))
+        return out
+
+    def _nm(self):
+        n, m = self.lifted_sizes[0], self.lifted_sizes[1]
+        return [n, m, m, n, n, m, m]
+
+    def ipm_residuals(self, bounds, it, grad, g, jv, mu):
+        out = [np.empty(k) for k in self._nm()]
+        self.L.gnr_ipm_residuals(self.h, _pp(bounds), _pp(it), _f(grad), _f(g), _f(jv), mu,
+                                 _pp(out))
+        return out
+
+    def ipm_condense(self, bounds, it, r):
+        n, m = self.lifted_sizes[0], self.lifted_sizes[1]
+        o = [np.empty(n), np.empty(m), np.empty(n), np.empty(m)]
+        self.L.gnr_ipm_condense(self.h, _pp(bounds), _pp(it), _pp(r), *[_f(a) for a in o])
+        return o
+
+    def ipm_ftb(self, bounds, it, d, tau):
+        out = np.empty(2)
+        self.L.gnr_ipm_ftb(self.h, _pp(bounds), _pp(it), _pp(d), tau, _f(out))
+        return out
+
+    def ipm_barrier(self, bounds, f, x, s, mu):
+        return self.L.gnr_ipm_barrier(self.h, _pp(bounds), f, _f(x), _f(s), mu)
+
+    def ipm_slope(self, bounds, grad, it, d, mu):
+        return self.L.gnr_ipm_slope(self.h, _pp(bounds), _f(grad), _pp(it), _pp(d), mu)
+
+    def ipm_violation(self, g, s):
+        return self.L.gnr_ipm_violation(self.h, _f(g), _f(s))
+
+    def ipm_kkt_error(self, bounds, it, r, mu):
+        out = np.empty(3)
+        self.L.gnr_ipm_kkt_error(self.h, _pp(bounds), _pp(it), _pp(r), mu, _f(out))
+        return out
+
+    def ipm_recover(self, bounds, it, r, d):
+        n, m = self.lifted_sizes[0], self.lifted_sizes[1]
+        o = [np.empty(n), np.empty(n), np.empty(m), np.empty(m)]
+        self.L.gnr_ipm_recover(self.h, _pp(bounds), _pp(it), _pp(r), _pp(d), _pp(o))
+        return o
+
+    def kkt_solve_parts(self, qx, qs, qy, ss, dw, dc, dx):
+        n, m = self.lifted_sizes[0], self.lifted_sizes[1]
+        rhs, ds, dy = np.empty(n), np.empty(m), np.empty(m)
+        self.L.gnr_kkt_solve_parts(self.h, _f(qx), _f(qs), _f(qy), _f(ss), dw, dc, _f(dx),
+                                   _f(rhs), _f(ds), _f(dy))
+        return rhs, ds, dy
 
     def solve(self, tol=1e-4, max_iter=500):
         out = np.zeros(4)

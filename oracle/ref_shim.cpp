@@ -13,6 +13,9 @@
 //   CondensedKkt              ipm/condensed.hpp:29-135
 //   compress_to_csc           sparse/matrix.hpp:45
 //   solve_nlp                 ipm/solver.hpp:469
+//   iterate.hpp vector ops    ipm/iterate.hpp:42-298 (residuals, condensation,
+//                             fraction to boundary, barrier, kkt_error), and
+//                             recover_bound_steps, condensed.hpp:187-212
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -352,6 +355,185 @@ void gnr_solve(void* h, double tol, int max_iter, double* out) {
   out[1] = r.objective;
   out[2] = static_cast<double>(static_cast<int>(r.status));
   out[3] = r.restorations;
+}
+
+// ---------------------------------------------------------------- IPM vector ops
+// Lifted bounds of the model's LiftedProblem: xl, xu [n], sl, su [m].
+void gnr_lifted_bounds(void* h, double* xl, double* xu, double* sl, double* su) {
+  auto& L = *static_cast<RefModel*>(h)->lifted;
+  std::memcpy(xl, L.x_lower().data(), L.x_lower().size() * sizeof(double));
+  std::memcpy(xu, L.x_upper().data(), L.x_upper().size() * sizeof(double));
+  std::memcpy(sl, L.s_lower().data(), L.s_lower().size() * sizeof(double));
+  std::memcpy(su, L.s_upper().data(), L.s_upper().size() * sizeof(double));
+}
+
+}  // extern "C"
+
+namespace {
+struct IpmView {
+  size_t n, m;
+  std::span<const double> xl, xu, sl, su;
+};
+IpmView view(void* h, const double* const* b) {
+  auto& L = *static_cast<RefModel*>(h)->lifted;
+  const size_t n = static_cast<size_t>(L.n()), m = static_cast<size_t>(L.m());
+  return {n, m, {b[0], n}, {b[1], n}, {b[2], m}, {b[3], m}};
+}
+// arrays: x s y zlx zux zls zus (iterate) / the same order for residuals and directions
+ipm::Iterate make_it(const IpmView& v, const double* const* a) {
+  ipm::Iterate it;
+  it.x.assign(a[0], a[0] + v.n);
+  it.s.assign(a[1], a[1] + v.m);
+  it.y.assign(a[2], a[2] + v.m);
+  it.zlx.assign(a[3], a[3] + v.n);
+  it.zux.assign(a[4], a[4] + v.n);
+  it.zls.assign(a[5], a[5] + v.m);
+  it.zus.assign(a[6], a[6] + v.m);
+  return it;
+}
+ipm::Residuals make_res(const IpmView& v, const double* const* a) {
+  ipm::Residuals r;
+  r.px.assign(a[0], a[0] + v.n);
+  r.ps.assign(a[1], a[1] + v.m);
+  r.py.assign(a[2], a[2] + v.m);
+  r.pzlx.assign(a[3], a[3] + v.n);
+  r.pzux.assign(a[4], a[4] + v.n);
+  r.pzls.assign(a[5], a[5] + v.m);
+  r.pzus.assign(a[6], a[6] + v.m);
+  return r;
+}
+ipm::Direction make_dir(const IpmView& v, const double* const* a) {
+  ipm::Direction d;
+  d.dx.assign(a[0], a[0] + v.n);
+  d.ds.assign(a[1], a[1] + v.m);
+  d.dy.assign(a[2], a[2] + v.m);
+  d.dzlx.assign(a[3], a[3] + v.n);
+  d.dzux.assign(a[4], a[4] + v.n);
+  d.dzls.assign(a[5], a[5] + v.m);
+  d.dzus.assign(a[6], a[6] + v.m);
+  return d;
+}
+void put7(const std::vector<double>* v[7], double* const* out) {
+  for (int k = 0; k < 7; ++k) std::memcpy(out[k], v[k]->data(), v[k]->size() * sizeof(double));
+}
+}  // namespace
+
+extern "C" {
+
+void gnr_ipm_jac_t(void* h, const double* jv, const double* y, double* out) {
+  auto& L = *static_cast<RefModel*>(h)->lifted;
+  const size_t nj = static_cast<size_t>(L.jac_nnz());
+  ipm::jac_transpose_multiply(L.jac_rows(), L.jac_cols(), {jv, nj},
+                              {y, static_cast<size_t>(L.m())}, {out, static_cast<size_t>(L.n())});
+}
+
+void gnr_ipm_jac(void* h, const double* jv, const double* x, double* out) {
+  auto& L = *static_cast<RefModel*>(h)->lifted;
+  const size_t nj = static_cast<size_t>(L.jac_nnz());
+  ipm::jac_multiply(L.jac_rows(), L.jac_cols(), {jv, nj}, {x, static_cast<size_t>(L.n())},
+                    {out, static_cast<size_t>(L.m())});
+}
+
+void gnr_ipm_residuals(void* h, const double* const* bounds, const double* const* it_a,
+                       const double* grad, const double* g, const double* jv, double mu,
+                       double* const* out) {
+  auto& L = *static_cast<RefModel*>(h)->lifted;
+  const IpmView v = view(h, bounds);
+  const ipm::Iterate it = make_it(v, it_a);
+  ipm::Residuals r;
+  ipm::compute_residuals(it, {grad, v.n}, {g, v.m}, L.jac_rows(), L.jac_cols(),
+                         {jv, static_cast<size_t>(L.jac_nnz())}, v.xl, v.xu, v.sl, v.su, mu, r);
+  const std::vector<double>* o[7] = {&r.px, &r.ps, &r.py, &r.pzlx, &r.pzux, &r.pzls, &r.pzus};
+  put7(o, out);
+}
+
+void gnr_ipm_condense(void* h, const double* const* bounds, const double* const* it_a,
+                      const double* const* r_a, double* sx, double* ss, double* qx, double* qs) {
+  const IpmView v = view(h, bounds);
+  const ipm::Iterate it = make_it(v, it_a);
+  const ipm::Residuals r = make_res(v, r_a);
+  std::vector<double> a, b, c, d;
+  ipm::bound_condensation(it, r, v.xl, v.xu, v.sl, v.su, a, b, c, d);
+  std::memcpy(sx, a.data(), v.n * sizeof(double));
+  std::memcpy(ss, b.data(), v.m * sizeof(double));
+  std::memcpy(qx, c.data(), v.n * sizeof(double));
+  std::memcpy(qs, d.data(), v.m * sizeof(double));
+}
+
+void gnr_ipm_ftb(void* h, const double* const* bounds, const double* const* it_a,
+                 const double* const* d_a, double tau, double* out2) {
+  const IpmView v = view(h, bounds);
+  const ipm::StepSizes a = ipm::fraction_to_boundary(make_it(v, it_a), make_dir(v, d_a), v.xl,
+                                                     v.xu, v.sl, v.su, tau);
+  out2[0] = a.primal;
+  out2[1] = a.dual;
+}
+
+double gnr_ipm_barrier(void* h, const double* const* bounds, double f, const double* x,
+                       const double* sv, double mu) {
+  const IpmView v = view(h, bounds);
+  return ipm::barrier_value(f, {x, v.n}, {sv, v.m}, v.xl, v.xu, v.sl, v.su, mu);
+}
+
+double gnr_ipm_slope(void* h, const double* const* bounds, const double* grad,
+                     const double* const* it_a, const double* const* d_a, double mu) {
+  const IpmView v = view(h, bounds);
+  return ipm::barrier_slope({grad, v.n}, make_it(v, it_a), make_dir(v, d_a), v.xl, v.xu, v.sl,
+                            v.su, mu);
+}
+
+double gnr_ipm_violation(void* h, const double* g, const double* sv) {
+  const size_t m = static_cast<size_t>(static_cast<RefModel*>(h)->lifted->m());
+  return ipm::constraint_violation({g, m}, {sv, m});
+}
+
+void gnr_ipm_kkt_error(void* h, const double* const* bounds, const double* const* it_a,
+                       const double* const* r_a, double mu, double* out3) {
+  const IpmView v = view(h, bounds);
+  const ipm::KktError e = ipm::kkt_error(make_it(v, it_a), make_res(v, r_a), mu, v.xl, v.xu,
+                                         v.sl, v.su);
+  out3[0] = e.stat;
+  out3[1] = e.feas;
+  out3[2] = e.comp;
+}
+
+// d_a: dx, ds in; dzlx dzux dzls dzus out (d_out[0..3])
+void gnr_ipm_recover(void* h, const double* const* bounds, const double* const* it_a,
+                     const double* const* r_a, const double* const* d_a, double* const* d_out) {
+  const IpmView v = view(h, bounds);
+  ipm::Direction d = make_dir(v, d_a);
+  ipm::recover_bound_steps(make_it(v, it_a), make_res(v, r_a), v.xl, v.xu, v.sl, v.su, d);
+  std::memcpy(d_out[0], d.dzlx.data(), v.n * sizeof(double));
+  std::memcpy(d_out[1], d.dzux.data(), v.n * sizeof(double));
+  std::memcpy(d_out[2], d.dzls.data(), v.m * sizeof(double));
+  std::memcpy(d_out[3], d.dzus.data(), v.m * sizeof(double));
+}
+
+// The vector parts of CondensedKkt::solve (condensed.hpp:150-172) around the factor
+// solve, on the model's reference KKT: its own A (jacobian_csr / jacobian_values) and
+// its csr_matvec / csr_matvec_transpose.  The c / d / sd formulas are the ones
+// assemble() stores (condensed.hpp:112-116).  rhs[n] before, ds/dy[m] from dx after.
+void gnr_kkt_solve_parts(void* h, const double* qx, const double* qs, const double* qy,
+                         const double* ss, double dw, double dc, const double* dx, double* rhs,
+                         double* ds, double* dy) {
+  auto* mdl = static_cast<RefModel*>(h);
+  const auto& a = mdl->kkt->jacobian_csr();
+  const auto av = mdl->kkt->jacobian_values();
+  const size_t n = static_cast<size_t>(mdl->lifted->n()), m = static_cast<size_t>(a.nrows);
+  std::vector<double> tm(m), c(m), sd(m);
+  for (size_t i = 0; i < m; ++i) {
+    sd[i] = ss[i] + dw;
+    c[i] = 1.0 / (1.0 + dc * sd[i]);
+    tm[i] = c[i] * qs[i] + (sd[i] * c[i]) * qy[i];
+  }
+  std::vector<double> r(n);
+  sparse::csr_matvec_transpose(a, av, tm, r);
+  for (size_t i = 0; i < n; ++i) rhs[i] = -(qx[i] + r[i]);
+  sparse::csr_matvec(a, av, {dx, n}, tm);
+  for (size_t i = 0; i < m; ++i) {
+    ds[i] = c[i] * (tm[i] + qy[i] - dc * qs[i]);
+    dy[i] = -qs[i] - sd[i] * ds[i];
+  }
 }
 
 }  // extern "C"

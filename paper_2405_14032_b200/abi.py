@@ -50,6 +50,19 @@ class GnSizes(C.Structure):
         "n_free", "jac_nnz_lifted", "hess_nnz_lifted")]
 
 
+class GnIterate(C.Structure):
+    """gn_iterate: device pointers of an ipm::Iterate (iterate.hpp:16-19)."""
+    _fields_ = [(k, vp) for k in ("x", "s", "y", "zlx", "zux", "zls", "zus")]
+
+
+class GnResiduals(C.Structure):
+    _fields_ = [(k, vp) for k in ("px", "ps", "py", "pzlx", "pzux", "pzls", "pzus")]
+
+
+class GnDirection(C.Structure):
+    _fields_ = [(k, vp) for k in ("dx", "ds", "dy", "dzlx", "dzux", "dzls", "dzus")]
+
+
 _SIGS = {
     "gn_abi_version": (C.c_int, []),
     "gn_launch_count": (C.c_int64, []),
@@ -80,6 +93,27 @@ _SIGS = {
     "gn_eval_hess": (C.c_int, [vp, f64p, f64p, C.c_double, f64p, C.c_int,
                                C.POINTER(GnError)]),
     "gn_eval_fg": (C.c_int, [vp, f64p, f64p, f64p, C.c_int, C.POINTER(GnError)]),
+    "gn_ipm_create": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(vp), C.POINTER(GnError)]),
+    "gn_ipm_destroy": (C.c_int, [vp]),
+    "gn_ipm_jac_transpose_multiply": (C.c_int, [vp, vp, vp, vp, C.c_int]),
+    "gn_ipm_jac_multiply": (C.c_int, [vp, vp, vp, vp, C.c_int]),
+    "gn_ipm_residuals": (C.c_int, [vp, C.POINTER(GnIterate), vp, vp, vp, C.c_double,
+                                   C.POINTER(GnResiduals), C.c_int]),
+    "gn_ipm_bound_condensation": (C.c_int, [vp, C.POINTER(GnIterate), C.POINTER(GnResiduals),
+                                            vp, vp, vp, vp, C.c_int]),
+    "gn_ipm_fraction_to_boundary": (C.c_int, [vp, C.POINTER(GnIterate), C.POINTER(GnDirection),
+                                              C.c_double, vp, C.c_int]),
+    "gn_ipm_barrier_value": (C.c_int, [vp, C.c_double, vp, vp, C.c_double, vp, C.c_int]),
+    "gn_ipm_barrier_slope": (C.c_int, [vp, vp, C.POINTER(GnIterate), C.POINTER(GnDirection),
+                                       C.c_double, vp, C.c_int]),
+    "gn_ipm_constraint_violation": (C.c_int, [vp, vp, vp, vp, C.c_int]),
+    "gn_ipm_kkt_error": (C.c_int, [vp, C.POINTER(GnIterate), C.POINTER(GnResiduals), C.c_double,
+                                   vp, C.c_int]),
+    "gn_ipm_recover_bound_steps": (C.c_int, [vp, C.POINTER(GnIterate), C.POINTER(GnResiduals),
+                                             C.POINTER(GnDirection), C.c_int]),
+    "gn_kkt_solve_rhs": (C.c_int, [vp, vp, vp, vp, vp, C.c_double, C.c_double, vp, C.c_int]),
+    "gn_kkt_solve_finish": (C.c_int, [vp, vp, vp, vp, vp, C.c_double, C.c_double, vp, vp,
+                                      C.c_int]),
     "gn_lifted_create": (C.c_int, [vp, C.c_double, C.POINTER(GnError)]),
     "gn_lifted_structure": (C.c_int, [vp, i32p, i32p, i32p, i32p, i32p, i32p, i32p, f64p,
                                       f64p, C.c_int]),

@@ -8,6 +8,7 @@
 #include <limits>
 #include <random>
 
+#include "gn_ipm.cuh"
 #include "gn_kkt.cuh"
 
 using gnb::DBuf;
@@ -785,6 +786,170 @@ int gn_compress_to_csc(int32_t nrows, int32_t ncols, int64_t nnz, const int32_t*
   if (nnz_out) *nnz_out = out.nnz;
   return ok(err);
   API_CATCH(err)
+}
+
+}  // extern "C"
+
+// ------------------------------------------------- device-resident IPM vector ops
+namespace {
+int ipm_mode(int mem) { return is_device(mem) ? GN_OK : GN_ERR_UNSUPPORTED; }
+int ipm_done(gn_ipm* P, int mem) {
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(P->K->stream));
+  return GN_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int gn_ipm_create(gn_kkt* K, const double* xl, const double* xu, const double* sl,
+                  const double* su, int mem, gn_ipm** out, gn_error* err) {
+  if (!K || !out) return fail(err, GN_ERR_INVALID, "null argument");
+  if (!K->ctx) return fail(err, GN_ERR_INVALID, "gn_ipm_create needs a gn_kkt_create_lifted KKT");
+  if ((K->n && (!xl || !xu)) || (K->m && (!sl || !su))) return fail(err, GN_ERR_INVALID, "null bounds");
+  API_TRY
+  set_device(K->device);
+  *out = gnb::ipm_create(K, xl, xu, sl, su, is_device(mem));
+  return ok(err);
+  API_CATCH(err)
+}
+
+int gn_ipm_destroy(gn_ipm* P) {
+  if (!P) return GN_OK;
+  cudaSetDevice(P->device);
+  cudaStreamSynchronize(P->K->stream);
+  delete P;
+  return GN_OK;
+}
+
+int gn_ipm_jac_transpose_multiply(gn_ipm* P, const double* jv, const double* y, double* out,
+                                  int mem) {
+  if (!P || !jv || !y || !out) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_jac_t(P, jv, y, out, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_jac_multiply(gn_ipm* P, const double* jv, const double* x, double* out, int mem) {
+  if (!P || !jv || !x || !out) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_jac(P, jv, x, out, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_residuals(gn_ipm* P, const gn_iterate* it, const double* grad, const double* g,
+                     const double* jv, double mu, const gn_residuals* r, int mem) {
+  if (!P || !it || !grad || !g || !jv || !r) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_residuals(P, *it, grad, g, jv, mu, *r, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_bound_condensation(gn_ipm* P, const gn_iterate* it, const gn_residuals* r,
+                              double* sx, double* ss, double* qx, double* qs, int mem) {
+  if (!P || !it || !r || !sx || !ss || !qx || !qs) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_condense(P, *it, *r, sx, ss, qx, qs, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_fraction_to_boundary(gn_ipm* P, const gn_iterate* it, const gn_direction* d,
+                                double tau, double* out2, int mem) {
+  if (!P || !it || !d || !out2) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_ftb(P, *it, *d, tau, out2, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_barrier_value(gn_ipm* P, double f, const double* x, const double* s, double mu,
+                         double* out, int mem) {
+  if (!P || !x || !s || !out) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_barrier(P, f, x, s, mu, out, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_barrier_slope(gn_ipm* P, const double* grad, const gn_iterate* it,
+                         const gn_direction* d, double mu, double* out, int mem) {
+  if (!P || !grad || !it || !d || !out) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_slope(P, grad, *it, *d, mu, out, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_constraint_violation(gn_ipm* P, const double* g, const double* s, double* out,
+                                int mem) {
+  if (!P || !g || !s || !out) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_violation(P, g, s, out, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_kkt_error(gn_ipm* P, const gn_iterate* it, const gn_residuals* r, double mu,
+                     double* out3, int mem) {
+  if (!P || !it || !r || !out3) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_kkt_error(P, *it, *r, mu, out3, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_ipm_recover_bound_steps(gn_ipm* P, const gn_iterate* it, const gn_residuals* r,
+                               const gn_direction* d, int mem) {
+  if (!P || !it || !r || !d) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::ipm_recover(P, *it, *r, *d, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_solve_rhs(gn_ipm* P, const double* qx, const double* qs, const double* qy,
+                     const double* ss, double dw, double dc, double* rhs, int mem) {
+  if (!P || !qx || !qs || !qy || !ss || !rhs) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::kkt_solve_rhs(P, qx, qs, qy, ss, dw, dc, rhs, P->scratch.p, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_solve_finish(gn_ipm* P, const double* dx, const double* qs, const double* qy,
+                        const double* ss, double dw, double dc, double* ds, double* dy, int mem) {
+  if (!P || !dx || !qs || !qy || !ss || !ds || !dy) return GN_ERR_INVALID;
+  if (ipm_mode(mem)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(P->device);
+  gnb::kkt_solve_finish(P, dx, qs, qy, ss, dw, dc, ds, dy, P->K->stream);
+  return ipm_done(P, mem);
+  API_CATCH(nullptr)
 }
 
 }  // extern "C"

@@ -371,3 +371,106 @@ def compress_to_csc(nrows, ncols, rows, cols):
 
 __all__ = ["OpfNlp", "CondensedKkt", "GridError", "load_profile", "compress_to_csc",
            "GN_MEM_HOST", "GN_MEM_DEVICE", "GN_MEM_DEVICE_ASYNC", "GN_IN_FULL"]
+
+
+class Ipm:
+    """Device-resident IPM vector operations (gn_ipm_*) on the lifted
+    problem of `kkt` (a CondensedKkt(nlp=...)).  Vectors are CUDA tensors (float64);
+    iterates / residuals / directions are sequences in the field order
+    x s y zlx zux zls zus.  Scalars come back as Python floats unless `sync=False`."""
+
+    def __init__(self, kkt: CondensedKkt, x_lower, x_upper, s_lower, s_upper):
+        import torch
+        self.lib = abi.lib()
+        self.kkt = kkt
+        dev = torch.device("cuda", torch.cuda.current_device())
+        t = lambda a: (a if hasattr(a, "data_ptr") else  # noqa: E731
+                       torch.from_numpy(np.ascontiguousarray(a, np.float64))).to(dev)
+        self._b = [t(x_lower), t(x_upper), t(s_lower), t(s_upper)]
+        h = C.c_void_p()
+        err = GnError()
+        _check(self.lib.gn_ipm_create(kkt.h, *[b.data_ptr() for b in self._b], GN_MEM_DEVICE,
+                                      C.byref(h), C.byref(err)), err, "gn_ipm_create")
+        self.h = h
+        self._out = torch.zeros(4, dtype=torch.float64, device=dev)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.gn_ipm_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _s(cls, arrays):
+        return cls(*[a.data_ptr() if a is not None else None for a in arrays])
+
+    def _mem(self, sync):
+        return GN_MEM_DEVICE if sync else GN_MEM_DEVICE_ASYNC
+
+    def _scalar(self, k, sync):
+        return [float(v) for v in self._out[:k].cpu()] if sync else self._out[:k]
+
+    def jac_transpose_multiply(self, jv, y, out, sync=True):
+        _check(self.lib.gn_ipm_jac_transpose_multiply(self.h, jv.data_ptr(), y.data_ptr(),
+                                                      out.data_ptr(), self._mem(sync)))
+
+    def jac_multiply(self, jv, x, out, sync=True):
+        _check(self.lib.gn_ipm_jac_multiply(self.h, jv.data_ptr(), x.data_ptr(), out.data_ptr(),
+                                            self._mem(sync)))
+
+    def residuals(self, it, grad, g, jv, mu, r, sync=True):
+        _check(self.lib.gn_ipm_residuals(self.h, C.byref(self._s(abi.GnIterate, it)),
+                                         grad.data_ptr(), g.data_ptr(), jv.data_ptr(), mu,
+                                         C.byref(self._s(abi.GnResiduals, r)), self._mem(sync)))
+
+    def bound_condensation(self, it, r, sx, ss, qx, qs, sync=True):
+        _check(self.lib.gn_ipm_bound_condensation(
+            self.h, C.byref(self._s(abi.GnIterate, it)), C.byref(self._s(abi.GnResiduals, r)),
+            sx.data_ptr(), ss.data_ptr(), qx.data_ptr(), qs.data_ptr(), self._mem(sync)))
+
+    def fraction_to_boundary(self, it, d, tau, sync=True):
+        _check(self.lib.gn_ipm_fraction_to_boundary(
+            self.h, C.byref(self._s(abi.GnIterate, it)), C.byref(self._s(abi.GnDirection, d)),
+            tau, self._out.data_ptr(), self._mem(sync)))
+        return self._scalar(2, sync)
+
+    def barrier_value(self, f, x, s, mu, sync=True):
+        _check(self.lib.gn_ipm_barrier_value(self.h, f, x.data_ptr(), s.data_ptr(), mu,
+                                             self._out.data_ptr(), self._mem(sync)))
+        return self._scalar(1, sync)
+
+    def barrier_slope(self, grad, it, d, mu, sync=True):
+        _check(self.lib.gn_ipm_barrier_slope(
+            self.h, grad.data_ptr(), C.byref(self._s(abi.GnIterate, it)),
+            C.byref(self._s(abi.GnDirection, d)), mu, self._out.data_ptr(), self._mem(sync)))
+        return self._scalar(1, sync)
+
+    def constraint_violation(self, g, s, sync=True):
+        _check(self.lib.gn_ipm_constraint_violation(self.h, g.data_ptr(), s.data_ptr(),
+                                                    self._out.data_ptr(), self._mem(sync)))
+        return self._scalar(1, sync)
+
+    def kkt_error(self, it, r, mu, sync=True):
+        _check(self.lib.gn_ipm_kkt_error(self.h, C.byref(self._s(abi.GnIterate, it)),
+                                         C.byref(self._s(abi.GnResiduals, r)), mu,
+                                         self._out.data_ptr(), self._mem(sync)))
+        return self._scalar(3, sync)
+
+    def recover_bound_steps(self, it, r, d, sync=True):
+        _check(self.lib.gn_ipm_recover_bound_steps(
+            self.h, C.byref(self._s(abi.GnIterate, it)), C.byref(self._s(abi.GnResiduals, r)),
+            C.byref(self._s(abi.GnDirection, d)), self._mem(sync)))
+
+    def solve_rhs(self, qx, qs, qy, ss, dw, dc, rhs, sync=True):
+        _check(self.lib.gn_kkt_solve_rhs(self.h, qx.data_ptr(), qs.data_ptr(), qy.data_ptr(),
+                                         ss.data_ptr(), dw, dc, rhs.data_ptr(), self._mem(sync)))
+
+    def solve_finish(self, dx, qs, qy, ss, dw, dc, ds, dy, sync=True):
+        _check(self.lib.gn_kkt_solve_finish(self.h, dx.data_ptr(), qs.data_ptr(), qy.data_ptr(),
+                                            ss.data_ptr(), dw, dc, ds.data_ptr(), dy.data_ptr(),
+                                            self._mem(sync)))
