@@ -205,6 +205,93 @@ def kernel_bytes(s, kkt, nlp, net, T):
     return {k: 8.0 * v for k, v in b.items()}
 
 
+def ipm_vector_ops(nlp, kkt, J, grad, g, dsx, dss, flush, stream, peak, reps=5):
+    """One IPM iteration's vector work on the device: residuals (with
+    J^T y), kkt_error, bound condensation, the condensed solve's rhs and ds/dy around the
+    (host, out-of-scope) factor solve, bound-step recovery, fraction to boundary, barrier
+    value and slope -- everything an IpmSolver iteration does besides the callbacks, the
+    KKT assembly and the LDL^T.  Synthetic interior iterate; L2 flushed before each rep."""
+    import torch
+    from paper_2405_14032_b200.opf import Ipm
+    s = nlp.sizes
+    n, m, nj = s.n_free, s.n_cons, s.jac_nnz_lifted
+    st = nlp.lifted_structure()
+    f2f = st["free_to_full"]
+    xl_f, xu_f, xs_f, _, _ = nlp.bounds()
+    xl, xu, sl, su = xl_f[f2f], xu_f[f2f], st["s_lower"], st["s_upper"]
+    dev = grad.device
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float64)).to(dev)  # noqa: E731
+    ipm = Ipm(kkt, xl, xu, sl, su)
+    rng = np.random.default_rng(3)
+
+    def interior(lo, hi, k):
+        base = np.where(np.isfinite(lo), lo, np.where(np.isfinite(hi), hi - 2.0, 0.0))
+        width = np.where(np.isfinite(lo) & np.isfinite(hi), hi - lo, 2.0)
+        return base + (0.1 + 0.8 * rng.random(k)) * width
+    it = [t(interior(xl, xu, n)), t(interior(sl, su, m)), t(rng.uniform(-1, 1, m))]
+    it += [t(np.where(np.isfinite(b), rng.uniform(0.01, 2, k), 0.0))
+           for b, k in ((xl, n), (xu, n), (sl, m), (su, m))]
+    del xl_f, xu_f, xs_f
+    jl = torch.empty(nj, dtype=torch.float64, device=dev)
+    from paper_2405_14032_b200.opf import _f64
+    nlp.lib.gn_lifted_gather_jac(nlp.h, _f64(J), _f64(jl), abi_dev_async())
+    e = lambda k: torch.empty(k, dtype=torch.float64, device=dev)  # noqa: E731
+    r = [e(k) for k in (n, m, m, n, n, m, m)]
+    d = [e(k) for k in (n, m, m, n, n, m, m)]
+    sx_, ss_, qx, qs, rhs = e(n), e(m), e(n), e(m), e(n)
+    gl = grad[torch.from_numpy(f2f.astype(np.int64)).to(dev)]  # lifted gradient
+    kkt.set_jacobian(jl, mem=abi_dev_async())
+
+    def iteration():
+        ipm.residuals(it, gl, g, jl, 0.1, r, sync=False)
+        ipm.kkt_error(it, r, 0.1, sync=False)
+        ipm.bound_condensation(it, r, sx_, ss_, qx, qs, sync=False)
+        ipm.solve_rhs(qx, qs, r[2], ss_, 1e-4, 0.0, rhs, sync=False)
+        d[0].copy_(rhs)  # stands in for the host LDL^T solve (out of scope)
+        ipm.solve_finish(d[0], qs, r[2], ss_, 1e-4, 0.0, d[1], d[2], sync=False)
+        ipm.recover_bound_steps(it, r, d, sync=False)
+        ipm.fraction_to_boundary(it, d, 0.99, sync=False)
+        ipm.barrier_value(1.0, it[0], it[1], 0.1, sync=False)
+        ipm.barrier_slope(gl, it, d, 0.1, sync=False)
+
+    with torch.cuda.stream(stream):
+        iteration()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(reps)]
+    for a_, b_ in evs:
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            a_.record(stream)
+            iteration()
+            b_.record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.median([a_.elapsed_time(b_) for a_, b_ in evs]))
+    annz = kkt.a_nnz
+    vec = {  # algorithmic reads + writes per op, in doubles (index maps excluded)
+        "residuals": nj + (4 * n + 5 * m) + (n + m) + 2 * (n + m) + (3 * n + 4 * m),
+        "kkt_error": (3 * n + 4 * m) + (n + 2 * m) + 2 * (n + m),
+        "bound_condensation": (3 * n + 3 * m) + (3 * n + 3 * m) + 2 * (n + m) + 2 * (n + m),
+        "solve_rhs": 3 * m + n + annz + n + 2 * m,
+        "rhs_copy": 2 * n,
+        "solve_finish": annz + n + 3 * m + 2 * m,
+        "recover_bound_steps": 10 * (n + m),  # w, d, z, pz, bounds in; dz out
+        "fraction_to_boundary": 8 * (n + m),  # w, d, z, dz, bounds
+        "barrier_value": (n + m) + 2 * (n + m),
+        "barrier_slope": n + 2 * (n + m) + 2 * (n + m),
+    }
+    alg = 8.0 * sum(vec.values())
+    ipm.close()
+    return {"ms": ms, "alg_bytes": alg, "gbs": alg / (ms * 1e-3) / 1e9,
+            "frac": alg / (ms * 1e-3) / 1e9 / peak, "n": n, "m": m,
+            "ops": list(vec.keys())}
+
+
+def abi_dev_async():
+    from paper_2405_14032_b200.abi import GN_MEM_DEVICE_ASYNC
+    return GN_MEM_DEVICE_ASYNC
+
+
 def profile_kernels(L, step, steps, stream, flush):
     """Per-kernel CUDA-event times (library KTimer, events on each kernel's launch
     stream) over `steps` extra steps run serially on one stream, L2 flushed
@@ -433,6 +520,9 @@ def run_ours(args, rank, world, local_rank, dist):
              "gbs": trial_bytes / (trial_ms * 1e-3) / 1e9,
              "frac": trial_bytes / (trial_ms * 1e-3) / 1e9 / peak}
 
+    ipm_ops = None if args.no_ipm_ops else ipm_vector_ops(nlp, kkt, J, grad, g, dsx, dss, flush,
+                                                          stream, peak)
+
     # ---------------------------------------------------------- e2e (host data)
     # (1) e2e: a device-resident IPM's iteration seen from the host.  Every step
     # copies its inputs (x, w, Sigma_x, Sigma_s) from pinned host memory, runs the
@@ -555,6 +645,7 @@ def run_ours(args, rank, world, local_rank, dist):
                     + (f"; {args.streams} streams"),
         "stages_ms": per_stage,
         "line_search_trial": trial,
+        "ipm_vector_ops": ipm_ops,
         "launch": ("cuda_graph (eager step %.4f ms)" % eager_ms) if graph_mode else "eager",
         "setup_s": setup_s,
         "clocks": clk,
@@ -678,6 +769,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
     ap.add_argument("--streams", type=int, choices=[1, 2], default=2)
+    ap.add_argument("--no-ipm-ops", action="store_true",
+                    help="skip the device-resident IPM vector-op measurement")
     ap.add_argument("--graph", type=int, choices=[0, 1], default=1,
                     help="replay the step as one CUDA graph (single rank / no halo)")
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
