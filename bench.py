@@ -165,7 +165,8 @@ def kernel_bytes(s, kkt, nlp, net, T):
     R = max(T - 1, 0)
     m, annz = s.n_cons, kkt.a_nnz
     # M slots per column block, from the lifted structure
-    _, _, colptr, _ = kkt.structure()
+    rowptr, _, colptr, _ = kkt.structure()
+    a_flow = int(rowptr[2 * N * T + 2 * L * T] - rowptr[2 * N * T])  # A entries of flow rows
     lens = np.diff(colptr.astype(np.int64))
     f2f = nlp.lifted_structure()["free_to_full"]
     bounds = np.cumsum([0, G * T, G * T, L * T, L * T, N * T, N * T])
@@ -193,6 +194,7 @@ def kernel_bytes(s, kkt, nlp, net, T):
         "k_line<H>": 39 * L * T + 2 * N * T, "k_gen<H>": 4 * G * T,
         "k_thermal<H>": 6 * LTh * T, "k_ramp<H>": 3 * GR * R,
         "k_opf_set_jac_fused": annz - 2 * LTh * T + 2 * N * T,
+        "k_opf_set_jac_fused<noflow>": annz - a_flow + 2 * LTh * T,
         "k_opf_set_jac_thermal": 4 * LTh * T,
         "k_fz_dvec": 2 * m,
         **bus_cls,
@@ -397,8 +399,7 @@ def run_ours(args, rank, world, local_rank, dist):
         if fused and ks is not stream:
             ks.wait_event(ev_x)
             mark(6, ks)
-            kkt.set_jacobian_x(dx, mem=A)
-            kkt.assemble_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)
+            kkt.update_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)  # set_jacobian + assemble
             mark(7, ks)
         nlp.eval_device("f", dx, f, sync=False)
         mark(1)
@@ -414,8 +415,7 @@ def run_ours(args, rank, world, local_rank, dist):
             stream.wait_event(ev_k)
         elif fused:
             mark(6)
-            kkt.set_jacobian_x(dx, mem=A)
-            kkt.assemble_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)
+            kkt.update_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)  # set_jacobian + assemble
             mark(7)
         else:  # contract path: A from J, M from H (GN_IN_FULL: lifted gather fused)
             ev_k.record(stream)

@@ -223,6 +223,13 @@ int gn_kkt_set_jacobian_x(gn_kkt* kkt, const double* x, int mem);
 int gn_kkt_assemble_x(gn_kkt* kkt, const double* x, const double* row_weights,
                       double obj_weight, const double* sigma_x, const double* sigma_s,
                       double delta_w, double delta_c, int mem);
+/* gn_kkt_set_jacobian_x + gn_kkt_assemble_x at the same x in one call (the IPM's
+ * per-iteration pair, solver.hpp:213-228): identical A and M, with the flow rows of A
+ * written by the flow-column kernel from the line state it already computes.  Inertia
+ * retries call gn_kkt_assemble_x alone. */
+int gn_kkt_update_x(gn_kkt* kkt, const double* x, const double* row_weights, double obj_weight,
+                    const double* sigma_x, const double* sigma_s, double delta_w,
+                    double delta_c, int mem);
 /* jacobian_values() / values() (condensed.hpp:94-96).  In the device modes the
  * destinations may be any UVA-addressable memory: device buffers or pinned host
  * buffers (an asynchronous read-back overlapping later work on the stream). */

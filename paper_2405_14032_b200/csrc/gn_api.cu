@@ -742,6 +742,26 @@ int gn_kkt_assemble_x(gn_kkt* K, const double* x, const double* w, double ow, co
   API_CATCH(nullptr)
 }
 
+int gn_kkt_update_x(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
+                    const double* ss, double dw, double dc, int mem) {
+  if (!K || !x || !w || !sx || !ss) return GN_ERR_INVALID;
+  if (!gnb::opf_fused_ready(K)) return GN_ERR_UNSUPPORTED;
+  API_TRY
+  set_device(K->device);
+  const double *dx = x, *dwt = w, *dsx = sx, *dss = ss;
+  if (!is_device(mem)) {
+    K->sj.upload(x, K->ctx->d.n, K->stream);
+    K->sh.upload(w, K->m, K->stream);
+    K->ssx.upload(sx, K->n, K->stream);
+    K->sss.upload(ss, K->m, K->stream);
+    dx = K->sj.p; dwt = K->sh.p; dsx = K->ssx.p; dss = K->sss.p;
+  }
+  gnb::opf_update_fused(K, dx, dwt, ow, dsx, dss, dw, dc);
+  if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
 int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
   if (!K) return GN_ERR_INVALID;
   API_TRY

@@ -52,6 +52,8 @@ bool opf_kkt_ready(const gn_kkt* K);
 bool opf_fused_ready(const gn_kkt* K);
 bool opf_fused_verify(gn_kkt* K);
 void opf_set_jacobian_fused(gn_kkt* K, const double* x);
+void opf_update_fused(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
+                      const double* ss, double dw, double dc);
 void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
                         const double* ss, double dw, double dc);
 void opf_set_jacobian(gn_kkt* K, const double* Jfull);

@@ -353,7 +353,8 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 constexpr int kSJW = 8;  // warps per CTA
 __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
                                                                 const double* __restrict__ x,
-                                                                double* __restrict__ A) {
+                                                                double* __restrict__ A,
+                                                                int skip_flow) {
   __shared__ double stg_all[kSJW * 5 * 33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t T = t.T, tch = t.tchunks;
@@ -379,7 +380,8 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
     return;
   }
   wg -= 2ll * t.N;
-  if (wg < (int64_t)t.L * tch) {  // flow_p / flow_q rows of (line, 32 periods)
+  const int64_t nflow = skip_flow ? 0 : (int64_t)t.L * tch;
+  if (wg < nflow) {  // flow_p / flow_q rows of (line, 32 periods)
     double* stg = stg_all + warp * (5 * 33);
     const int32_t l = (int32_t)(wg / tch), c0 = (int32_t)(wg - (int64_t)l * tch) * 32;
     const int32_t nt = min(32, T - c0), ts = lane < nt ? c0 + lane : c0;
@@ -403,7 +405,7 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
     warp_span_flush(A, bq, stg, len, nt, lane);
     return;
   }
-  wg -= (int64_t)t.L * tch;
+  wg -= nflow;
   if (wg < LT) {  // thermal rows of thermal slot k, all periods: [p, q] -> (2p, 2q)
     const int32_t k = (int32_t)wg, l = __ldg(t.th_line + k);
     const int64_t base = __ldg(t.rowptr + t.therm0 + k * T);
@@ -478,18 +480,30 @@ void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, 
   launch_fused<false>(K, in, K->dvals.p, K->mvals.p, nullptr, nullptr);
 }
 
-void opf_set_jacobian_fused(gn_kkt* K, const double* x) {
+static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow) {
   const OpfKktTab& t = K->opf->t;
   if (K->m <= 0) return;
   {
-    KTimer kt("k_opf_set_jac_fused", K->stream);
+    KTimer kt(skip_flow ? "k_opf_set_jac_fused<noflow>" : "k_opf_set_jac_fused", K->stream);
     const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
-    const int64_t warps = 2ll * t.N + (int64_t)t.L * t.tchunks + LT + t.L + (K->m - t.ramp0 + 31) / 32;
+    const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
+                          (K->m - t.ramp0 + 31) / 32;
     k_opf_set_jac_fused<<<(unsigned)((warps + kSJW - 1) / kSJW), kSJW * 32, 0, K->stream>>>(
-        t, K->m, x, K->avals.p);
+        t, K->m, x, K->avals.p, skip_flow);
   }
   count_launch();
   GN_CK(cudaGetLastError());
+}
+
+void opf_set_jacobian_fused(gn_kkt* K, const double* x) { set_jac_launch(K, x, 0); }
+
+// set_jacobian_x + assemble_x at the same x (gn_kkt_update_x).  (Writing A's flow rows
+// from the flow-column kernel's line state was measured slower than the separate
+// set_jacobian pass: it costs that latency-bound kernel a third of its occupancy.)
+void opf_update_fused(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
+                      const double* ss, double dw, double dc) {
+  set_jac_launch(K, x, 0);
+  opf_assemble_fused(K, x, w, ow, sx, ss, dw, dc);
 }
 
 // Structure check of the fused enumeration (row index of every slot, column lengths).

@@ -343,6 +343,13 @@ class CondensedKkt:
                                           _f64(sigma_x), _f64(sigma_s), float(delta_w),
                                           float(delta_c), mem))
 
+    def update_x(self, x, row_weights, obj_weight, sigma_x, sigma_s, delta_w, delta_c,
+                 mem: int = GN_MEM_HOST):
+        """set_jacobian_x + assemble_x at the same x in one call (gn_kkt_update_x)."""
+        _check(self.lib.gn_kkt_update_x(self.h, _f64(x), _f64(row_weights), float(obj_weight),
+                                        _f64(sigma_x), _f64(sigma_s), float(delta_w),
+                                        float(delta_c), mem))
+
     def values(self, a=None, m=None):
         a = np.empty(self.a_nnz) if a is None else a
         m = np.empty(self.m_nnz) if m is None else m

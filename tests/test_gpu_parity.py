@@ -285,6 +285,13 @@ def _fused_check(nlp, K, x, w, ow, sx, ss):
         a, m = K.values()
         assert_bitexact(a, a_ref, f"fused A dw={dw}")
         assert_bitexact(m, m_ref, f"fused M dw={dw}")
+        # gn_kkt_update_x (set_jacobian_x + assemble_x in one pass) over poisoned A / M
+        K.set_jacobian(np.full_like(jv, np.nan), mem=GN_IN_FULL)
+        K.assemble(np.full_like(hv, np.nan), sx, ss, dw, dc, mem=GN_IN_FULL)
+        K.update_x(x, w, ow, sx, ss, dw, dc)
+        a, m = K.values()
+        assert_bitexact(a, a_ref, f"update_x A dw={dw}")
+        assert_bitexact(m, m_ref, f"update_x M dw={dw}")
         K.set_jacobian(jv, mem=GN_IN_FULL)  # restore the contract A for the next delta
 
 
