@@ -187,12 +187,12 @@ def kernel_bytes(s, kkt, nlp, net, T):
     b = {
         "k_gen<F>": G * T, "k_gen<GRAD>": 2 * G * T,
         "k_bus<G>": 2 * N * T + 2 * L * T + 2 * G * T + 2 * D * T,
-        "k_line<G>": 5 * L * T + 2 * N * T, "k_thermal<G>": 3 * LTh * T,
+        "k_line<G>": 5 * L * T + 2 * N * T + 3 * LTh * T,  # thermal rows folded in
         "k_ramp<G>": GR * R + G * T,
-        "k_line<J>": 16 * L * T + 2 * N * T, "k_gen<J>": 2 * G * T,
-        "k_thermal<J>": 4 * LTh * T, "k_ramp<J>": 2 * GR * R,
-        "k_line<H>": 39 * L * T + 2 * N * T, "k_gen<H>": 4 * G * T,
-        "k_thermal<H>": 6 * LTh * T, "k_ramp<H>": 3 * GR * R,
+        "k_line<J>": 16 * L * T + 2 * N * T + 4 * LTh * T, "k_gen<J>": 2 * G * T,
+        "k_ramp<J>": 2 * GR * R,
+        "k_line<H>": 39 * L * T + 2 * N * T + 6 * LTh * T, "k_gen<H>": 4 * G * T,
+        "k_ramp<H>": 3 * GR * R,
         "k_opf_set_jac_fused": annz - 2 * LTh * T + 2 * N * T,
         "k_opf_set_jac_fused<noflow>": annz - a_flow + 2 * LTh * T,
         "k_opf_set_jac_thermal": 4 * LTh * T,
