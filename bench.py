@@ -378,7 +378,10 @@ def run_ours(args, rank, world, local_rank, dist):
     # and Sigma, f/grad/g/J/H and the fused A/M are independent (the fused KKT
     # recomputes its J/H terms), so a device-resident IPM overlaps them; the
     # contract pipeline must wait for J and H.
-    kstream = torch.cuda.Stream(device=dev) if args.streams == 2 else stream
+    # the KKT stream gets the higher priority: its latency-bound kernels are placed
+    # first and the bandwidth-bound callback kernels fill the SMs around them
+    prio = int(os.environ.get("GN_KKT_PRIORITY", "-1"))
+    kstream = torch.cuda.Stream(device=dev, priority=prio) if args.streams == 2 else stream
     kkt.set_stream(kstream.cuda_stream)
     ev_x = torch.cuda.Event()
     ev_k = torch.cuda.Event()
