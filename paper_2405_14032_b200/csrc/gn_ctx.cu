@@ -49,6 +49,7 @@ KTimer::~KTimer() {
 }
 
 void profile_enable(bool on) { g_prof = on; }
+bool profiling() { return g_prof; }
 void profile_reset() {
   for (auto& r : g_recs)
     for (auto& e : r.pending) {

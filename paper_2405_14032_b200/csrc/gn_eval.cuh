@@ -18,6 +18,7 @@ void host_bounds(const gn_ctx* c, double* xl, double* xu, double* xs, double* rl
 int32_t exclusive_scan(const int32_t* flag, int32_t* pos, int64_t n, cudaStream_t s);
 int64_t launch_count();
 void profile_enable(bool on);
+bool profiling();
 void profile_reset();
 int profile_count();
 const char* profile_get(int i, double* ms, int64_t* launches);

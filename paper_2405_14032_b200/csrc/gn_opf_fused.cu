@@ -442,15 +442,46 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
 }
 
 // ------------------------------------------------------------------ host
+// The column kernels write disjoint parts of M.  In value mode they are forked over
+// the KKT stream and two auxiliary streams (fork/join by events: capturable in a CUDA
+// graph), so the short, low-occupancy degree-class launches overlap the flow-column
+// kernel instead of each paying its own tail.  Per-kernel profiling runs them serially.
 template <bool STRUCT>
 static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, int32_t* rows,
                          int32_t* bad) {
-  const OpfKktTab& t = K->opf->t;
+  OpfKkt* X = K->opf;
+  const OpfKktTab& t = X->t;
   cudaStream_t s = K->stream;
-  for (int k = 0; k < kBusClasses; ++k)
-    launch_fz_bus(t, K->opf->bus_cls[k].p, K->opf->n_bus_cls[k],
-                  k < kBusRegMax ? k + 1 : (k == kBusRegMax ? 8 : K->opf->maxdeg_rest), k, in, dv,
-                  M, rows, bad, s);
+  const bool fork = !STRUCT && !profiling();
+  cudaStream_t lane[3] = {s, s, s};
+  if (fork) {
+    int prio = 0;
+    GN_CK(cudaStreamGetPriority(s, &prio));
+    if (!X->aux[0] || prio != X->aux_prio) {
+      for (auto& a : X->aux) {
+        if (a) GN_CK(cudaStreamDestroy(a));
+        GN_CK(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, prio));
+      }
+      if (!X->ev_fork) {
+        GN_CK(cudaEventCreateWithFlags(&X->ev_fork, cudaEventDisableTiming));
+        for (auto& e : X->ev_join) GN_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      }
+      X->aux_prio = prio;
+    }
+    GN_CK(cudaEventRecord(X->ev_fork, s));
+    for (int a = 0; a < 2; ++a) {
+      GN_CK(cudaStreamWaitEvent(X->aux[a], X->ev_fork, 0));
+      lane[a + 1] = X->aux[a];
+    }
+  }
+  // degree classes 1..6, le8, rest: alternate the two auxiliary lanes, largest first
+  static const int order[kBusClasses] = {2, 3, 1, 4, 5, 6, 7, 0};
+  for (int i = 0; i < kBusClasses; ++i) {
+    const int k = order[i];
+    launch_fz_bus(t, X->bus_cls[k].p, X->n_bus_cls[k],
+                  k < kBusRegMax ? k + 1 : (k == kBusRegMax ? 8 : X->maxdeg_rest), k, in, dv, M,
+                  rows, bad, lane[1 + (i & 1)]);
+  }
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
     KTimer kt("k_fz_line", s);
@@ -463,6 +494,12 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
     KTimer kt("k_fz_gen", s);
     k_fz_gen<STRUCT><<<(unsigned)((ng + 255) / 256), 256, 0, s>>>(t, in, dv, M, rows, bad);
     count_launch();
+  }
+  if (fork) {
+    for (int a = 0; a < 2; ++a) {
+      GN_CK(cudaEventRecord(X->ev_join[a], X->aux[a]));
+      GN_CK(cudaStreamWaitEvent(s, X->ev_join[a], 0));
+    }
   }
   GN_CK(cudaGetLastError());
 }

@@ -73,6 +73,15 @@ bool fz_bus_fits(int32_t maxdeg);  // one warp's shared memory fits (else: no fu
 
 struct OpfKkt {
   bool ready = false;
+  // fork/join of the column kernels over auxiliary streams (same priority as the KKT's)
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  int aux_prio = 0;
+  ~OpfKkt() {
+    for (auto& a : aux) if (a) cudaStreamDestroy(a);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    for (auto& e : ev_join) if (e) cudaEventDestroy(e);
+  }
   OpfKktTab t{};
   DBuf<int32_t> lent, items, lf, lt, l_therm, lidx_to, lidx_from, gbus, ppos, qpos, g_ramp, ngp,
       ngq, bl_ptr, bl, bg_ptr, bg, nb_ptr, nb, lnb_ptr, lnb, nb_inc;
