@@ -140,10 +140,21 @@ __device__ void fz_gen_cols(const Ctx& c, int32_t gsel, double* M, int32_t* rows
 }
 
 // d_r for every row (condensed.hpp:111-117), once per assemble call.
+// Four rows per thread with 16-byte loads / stores (when sigma_s is 16-byte aligned; the
+// d buffer is ours and always is): a pure stream, so wide accesses and more bytes in
+// flight per thread are what move it toward the copy bandwidth.
 __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __restrict__ ss, double dw,
                                                  double dc, double* __restrict__ dv) {
-  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < m) dv[r] = dvec(ss[r], dw, dc);
+  const int64_t r0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (r0 >= m) return;
+  if (r0 + 4 <= m && (reinterpret_cast<uintptr_t>(ss) & 15) == 0) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(ss + r0));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(ss + r0 + 2));
+    reinterpret_cast<double2*>(dv + r0)[0] = make_double2(dvec(a.x, dw, dc), dvec(a.y, dw, dc));
+    reinterpret_cast<double2*>(dv + r0)[1] = make_double2(dvec(b.x, dw, dc), dvec(b.y, dw, dc));
+  } else {
+    for (int64_t r = r0; r < r0 + 4 && r < m; ++r) dv[r] = dvec(ss[r], dw, dc);
+  }
 }
 
 // p(l) and q(l) columns of line l, one warp per (l, 32 consecutive periods),
@@ -511,7 +522,7 @@ void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, 
   FIn in{x, w, ow, sx, ss, dw, dc};
   if (K->m > 0) {
     KTimer kt("k_fz_dvec", K->stream);
-    k_fz_dvec<<<(unsigned)((K->m + 255) / 256), 256, 0, K->stream>>>(K->m, ss, dw, dc, K->dvals.p);
+    k_fz_dvec<<<(unsigned)((K->m + 1023) / 1024), 256, 0, K->stream>>>(K->m, ss, dw, dc, K->dvals.p);
     count_launch();
   }
   launch_fused<false>(K, in, K->dvals.p, K->mvals.p, nullptr, nullptr);
