@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   const int64_t w = (int64_t)blockIdx.x * nw + warp;
   const int64_t n64 = w / t.tchunks;
   if (n64 >= n_buses) return;  // warp-uniform
-  const int4 bd0 = __ldg(buses + 2 * n64), bd1 = __ldg(buses + 2 * n64 + 1);
+  const int4 bd0 = __ldg(buses + kBusDesc * n64), bd1 = __ldg(buses + kBusDesc * n64 + 1);
+  const int4 bd2 = __ldg(buses + kBusDesc * n64 + 2);
   const int32_t n = bd0.x, b0 = bd0.y, deg = bd0.z & 255, T = t.T;
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
   // per (line, lane): 6 state values + the 5 row inputs it contributes with
@@ -145,8 +146,8 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
     return k < 0 ? -1 : k * T + tt;
   };
   const int32_t cv = bd1.x < 0 ? -1 : bd1.x * T + tt, ct = bd1.y < 0 ? -1 : bd1.y * T + tt;
-  const int64_t posv = cv >= 0 ? (int64_t)__ldg(t.colptr + cv) : 0;
-  const int64_t post = ct >= 0 ? (int64_t)__ldg(t.colptr + ct) : 0;
+  const int64_t posv = cv >= 0 ? (int64_t)bd2.x + (int64_t)tt * bd2.y : 0;
+  const int64_t post = ct >= 0 ? (int64_t)bd2.z + (int64_t)tt * bd2.w : 0;
   int jv = 0, jt = 0;
   const int32_t p0 = bd0.w, p1 = p0 + (bd0.z >> 8);
 #define PASS(expr)                                 \
@@ -284,7 +285,8 @@ __global__ void __launch_bounds__(kBW3 * 32) k_fz_busr(OpfKktTab t, const int4* 
   const int32_t T = t.T;
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
   if (tt >= T) return;
-  const int4 bd0 = __ldg(buses + 2 * n64), bd1 = __ldg(buses + 2 * n64 + 1);
+  const int4 bd0 = __ldg(buses + kBusDesc * n64), bd1 = __ldg(buses + kBusDesc * n64 + 1);
+  const int4 bd2 = __ldg(buses + kBusDesc * n64 + 2);
   const int32_t n = bd0.x, b0 = bd0.y, boff = bd0.w;
   const int32_t cv = bd1.x < 0 ? -1 : bd1.x * T + tt, ct = bd1.y < 0 ? -1 : bd1.y * T + tt;
   int2 e[DEG];
@@ -294,8 +296,8 @@ __global__ void __launch_bounds__(kBW3 * 32) k_fz_busr(OpfKktTab t, const int4* 
     e[i] = __ldg(t.blx + b0 + i);
     pp[i] = __ldg(t.bpos + b0 + i);
   }
-  const int64_t posv = cv >= 0 ? (int64_t)__ldg(t.colptr + cv) : 0;
-  const int64_t post = ct >= 0 ? (int64_t)__ldg(t.colptr + ct) : 0;
+  const int64_t posv = cv >= 0 ? (int64_t)bd2.x + (int64_t)tt * bd2.y : 0;
+  const int64_t post = ct >= 0 ? (int64_t)bd2.z + (int64_t)tt * bd2.w : 0;
   if constexpr (STRUCT) {
     const int32_t off_v = 2 * t.G + 2 * t.L, off_th = off_v + t.N;
     auto col = [&](int32_t off, int32_t ent) {

@@ -768,6 +768,19 @@ bool opf_kkt_prepare(gn_kkt* K) {
     // program: (v(o), v(n)) | (th(o), v(n)) << 8 | (th(o), th(n)) << 16, 0xff = absent.
     std::vector<int32_t> bpos(bl.size(), 0xffffff);
     std::vector<int4> cls[kBusClasses];
+    // M column starts/lengths of v(n), th(n): a column's slots are the same for every
+    // period, so column (k, t) starts at colptr[k*T] + t * len(k) -- held in the bus
+    // descriptor, no colptr lookup on the kernels' critical path
+    std::vector<int32_t> cp(static_cast<size_t>(K->n) + 1);
+    GN_CK(cudaMemcpyAsync(cp.data(), K->M.ptr.p, sizeof(int32_t) * cp.size(), cudaMemcpyDeviceToHost, s));
+    GN_CK(cudaStreamSynchronize(s));
+    auto colspan = [&](int32_t k, int32_t& base, int32_t& len) {
+      base = len = 0;
+      if (k < 0) return;
+      const int64_t c = static_cast<int64_t>(k) * d.T;
+      base = cp[c];
+      len = cp[c + 1] - cp[c];
+    };
     for (int32_t n = 0; n < N; ++n) {
       const int32_t deg = bl_ptr[n + 1] - bl_ptr[n];
       const int32_t np = bprog_ptr[n + 1] - bprog_ptr[n];
@@ -796,16 +809,22 @@ bool opf_kkt_prepare(gn_kkt* K) {
             make_int4(n, bl_ptr[n], deg | (np << 8), bprog_ptr[n]));
       }
       auto& v = simple ? cls[deg - 1] : cls[deg <= 8 ? kBusClasses - 2 : kBusClasses - 1];
-      v.push_back(make_int4(lent[offs[C_V] + n], lent[offs[C_TH] + n], 0, 0));
+      const int32_t kv = lent[offs[C_V] + n], kt = lent[offs[C_TH] + n];
+      int32_t bv, lv, bt, lt;
+      colspan(kv, bv, lv);
+      colspan(kt, bt, lt);
+      v.push_back(make_int4(kv, kt, 0, 0));
+      v.push_back(make_int4(bv, lv, bt, lt));
     }
     up(X->bpos, bpos, s);
     for (int k = 0; k < kBusClasses; ++k) {
       up(X->bus_cls[k], cls[k], s);
-      if (cls[k].empty()) X->bus_cls[k].alloc(2);
-      X->n_bus_cls[k] = static_cast<int32_t>(cls[k].size() / 2);
+      if (cls[k].empty()) X->bus_cls[k].alloc(kBusDesc);
+      X->n_bus_cls[k] = static_cast<int32_t>(cls[k].size() / kBusDesc);
     }
     int32_t md = 0;
-    for (size_t i = 0; i < cls[kBusClasses - 1].size(); i += 2) md = std::max(md, cls[kBusClasses - 1][i].z & 255);
+    for (size_t i = 0; i < cls[kBusClasses - 1].size(); i += kBusDesc)
+      md = std::max(md, cls[kBusClasses - 1][i].z & 255);
     X->maxdeg_rest = md;
   }
   t.lent = X->lent.p; t.items = X->items.p; t.lf = X->lf.p; t.lt = X->lt.p; t.l_therm = X->l_therm.p;
