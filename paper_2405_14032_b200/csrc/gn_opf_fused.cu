@@ -238,7 +238,8 @@ __global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, const double
     wth = w[t.therm0 + k * T + ts];
     dth = dv[t.therm0 + k * T + ts];
   }
-  const int64_t basep = __ldg(t.colptr + d1.z * T + c0), baseq = __ldg(t.colptr + d1.w * T + c0);
+  const int2 cb = __ldg(t.lcb + l);
+  const int64_t basep = cb.x + (int64_t)c0 * lenp, baseq = cb.y + (int64_t)c0 * lenq;
   const LineState s = line_state(G, B, vf, vt, thf, tht);
   const double jtp = j_thermal(xp), jtq = j_thermal(xq);
   // ---- values, slot by slot; column p, then column q.  Staged (the common case:
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
     const int32_t nf = __ldg((Q ? t.ngq : t.ngp) + b);
     const int32_t b0 = __ldg(t.bl_ptr + b), len = nf + __ldg(t.bl_ptr + b + 1) - b0;
     if (len == 0) return;
-    const int64_t base = __ldg(t.rowptr + (Q ? t.bal_q0 : t.bal_p0) + b * T);
+    const int64_t base = __ldg(t.rbase + (Q ? t.N : 0) + b);
     if (len > 32) {  // (very high degree: slot by slot)
       for (int32_t e = lane; e < T * len; e += 32) {
         const int32_t j = e % len;
@@ -401,8 +402,8 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
     const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
     const LineState s = line_state(G, B, x[t.v0 + f * T + ts], x[t.v0 + to * T + ts],
                                    x[t.th0 + f * T + ts], x[t.th0 + to * T + ts]);
-    const int64_t bp = __ldg(t.rowptr + t.flow_p0 + l * T + c0);
-    const int64_t bq = __ldg(t.rowptr + t.flow_q0 + l * T + c0);
+    const int64_t bp = __ldg(t.rbase + 2 * t.N + l) + (int64_t)c0 * len;
+    const int64_t bq = __ldg(t.rbase + 2 * t.N + t.L + l) + (int64_t)c0 * len;
     int pos[5];
 #pragma unroll
     for (int fl = 0; fl < 5; ++fl) pos[fl] = __ldg(t.fpos + 5 * l + fl);
@@ -419,7 +420,7 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
   wg -= nflow;
   if (wg < LT) {  // thermal rows of thermal slot k, all periods: [p, q] -> (2p, 2q)
     const int32_t k = (int32_t)wg, l = __ldg(t.th_line + k);
-    const int64_t base = __ldg(t.rowptr + t.therm0 + k * T);
+    const int64_t base = __ldg(t.rbase + 2 * t.N + 2 * t.L + k);
     for (int32_t e = lane; e < 2 * T; e += 32) {
       const int32_t tt = e >> 1;
       A[base + e] = 0.0 + j_thermal(x[((e & 1) ? t.q0 : t.p0) + l * T + tt]);
@@ -432,7 +433,7 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
     const int pf = __ldg(t.apos + 2 * l), pt = __ldg(t.apos + 2 * l + 1);
     const int32_t len = (pf >= 0) + (pt >= 0);
     if (len == 0) return;
-    const int64_t base = __ldg(t.rowptr + t.ang0 + l * T);
+    const int64_t base = __ldg(t.rbase + 2 * t.N + 2 * t.L + LT + l);
     const double v = lane == pf ? 0.0 + 1.0 : 0.0 + (-1.0);
     warp_const_rows(A, base, v, len, T, lane);
     return;

@@ -774,6 +774,31 @@ bool opf_kkt_prepare(gn_kkt* K) {
     std::vector<int32_t> cp(static_cast<size_t>(K->n) + 1);
     GN_CK(cudaMemcpyAsync(cp.data(), K->M.ptr.p, sizeof(int32_t) * cp.size(), cudaMemcpyDeviceToHost, s));
     GN_CK(cudaStreamSynchronize(s));
+    {  // row / column starts at t = 0 of the fused kernels' entities (same reason)
+      std::vector<int32_t> rp(static_cast<size_t>(K->m) + 1);
+      GN_CK(cudaMemcpyAsync(rp.data(), K->A.ptr.p, sizeof(int32_t) * rp.size(),
+                            cudaMemcpyDeviceToHost, s));
+      GN_CK(cudaStreamSynchronize(s));
+      const int64_t TT = d.T;
+      std::vector<int32_t> rbase(2 * static_cast<size_t>(N) + 3 * static_cast<size_t>(L) + d.LT);
+      for (int32_t b = 0; b < N; ++b) {
+        rbase[b] = rp[d.bal_p0 + b * TT];
+        rbase[N + b] = rp[d.bal_q0 + b * TT];
+      }
+      for (int32_t l = 0; l < L; ++l) {
+        rbase[2 * N + l] = rp[d.flow_p0 + l * TT];
+        rbase[2 * N + L + l] = rp[d.flow_q0 + l * TT];
+        rbase[2 * N + 2 * L + d.LT + l] = rp[d.ang0 + l * TT];
+      }
+      for (int32_t k = 0; k < d.LT; ++k) rbase[2 * N + 2 * L + k] = rp[d.therm0 + k * TT];
+      std::vector<int2> lcb(L);
+      for (int32_t l = 0; l < L; ++l) {
+        const int32_t kp = lent[offs[C_P] + l], kq = lent[offs[C_Q] + l];
+        lcb[l] = make_int2(kp >= 0 ? cp[kp * TT] : 0, kq >= 0 ? cp[kq * TT] : 0);
+      }
+      up(X->rbase, rbase, s);
+      up(X->lcb, lcb, s);
+    }
     auto colspan = [&](int32_t k, int32_t& base, int32_t& len) {
       base = len = 0;
       if (k < 0) return;
@@ -834,6 +859,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
   t.bg_ptr = X->bg_ptr.p; t.bg = X->bg.p; t.nb_ptr = X->nb_ptr.p; t.nb = X->nb.p; t.nb_inc = X->nb_inc.p;
   t.lnb_ptr = X->lnb_ptr.p; t.lnb = X->lnb.p; t.lnbx = X->lnbx.p;
   t.blx = X->blx.p; t.blgb = X->blgb.p; t.bpos = X->bpos.p;
+  t.rbase = X->rbase.p; t.lcb = X->lcb.p;
   t.ldesc0 = X->ldesc0.p; t.ldesc1 = X->ldesc1.p;
   t.bprog_ptr = X->bprog_ptr.p; t.bprog = X->bprog.p;
   t.rowptr = K->A.ptr.p; t.colptr = K->M.ptr.p;

@@ -44,6 +44,9 @@ struct OpfKktTab {
   const int2* blx;                      // [bl] (l << 1 | is_from, other bus) per incident line
   const double2* blgb;                  // [bl] (G, B) per incident line
   const int32_t* bpos;                  // [bl] neighbour-slot offsets (register bus classes)
+  const int32_t* rbase;                 // A row start at t = 0: bal_p[N] bal_q[N] flow_p[L]
+                                        // flow_q[L] thermal[LT] angle[L] (row (e, t) = + t*len)
+  const int2* lcb;                      // [L] M column start at t = 0 of p(l), q(l)
   const int32_t* bprog_ptr;             // [N+1] per-bus slot programs of the v(n)/th(n) columns
   const unsigned long long* bprog;      // (row entity << 35 | type << 32 | lane mask)
 };
@@ -97,7 +100,8 @@ struct OpfKkt {
   DBuf<unsigned long long> bprog;
   DBuf<int4> bus_cls[kBusClasses];  // bus descriptors by degree class (bus-column kernel)
   DBuf<int2> blx;
-  DBuf<int32_t> bpos;
+  DBuf<int32_t> bpos, rbase;
+  DBuf<int2> lcb;
   int32_t maxdeg_rest = 0;
   DBuf<double2> blgb;
   int32_t n_bus_cls[kBusClasses] = {};
