@@ -74,3 +74,23 @@ def test_synthetic_topology_properties():
 def test_matpower_emission_parses_bit_identically():
     raw = synthetic_case(60, 100, 15, 50, seed=9, parallel_lines=3, shared_gens=2)
     assert raw.network().equal(B.ref_parse_matpower(raw.to_matpower()))
+
+
+def test_plain_c_consumer_compiles_links_and_runs(tmp_path):
+    """The ABI as a C host binding sees it: tests/c/abi_smoke.c against the header and
+    the in-tree library, gcc -std=c11 -pedantic, run without a GPU."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    root = Path(__file__).resolve().parents[1]
+    exe = tmp_path / "abi_smoke"
+    libdir = abi.LIB_PATH.parent
+    subprocess.run([gcc, "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror",
+                    str(root / "tests" / "c" / "abi_smoke.c"), "-I", str(root / "include"),
+                    "-L", str(libdir), "-lgridnlp_b200", f"-Wl,-rpath,{libdir}", "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, (out.returncode, out.stdout, out.stderr)
+    assert out.stdout.startswith("abi 1 devices")
