@@ -329,7 +329,7 @@ def run_ours(args, rank, world, local_rank, dist):
     t0 = time.time()
     # period shard [first, first + periods) of the T_total horizon (world == 1: the whole horizon)
     nlp = OpfNlp(net, args.periods, scale, device=local_rank, shard=(T_total, first))
-    stream = torch.cuda.Stream(device=dev)
+    stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("GN_CB_PRIORITY", "0")))
     nlp.set_stream(stream.cuda_stream)
     nlp.lift(1e-4)
     kkt = CondensedKkt(nlp=nlp)
