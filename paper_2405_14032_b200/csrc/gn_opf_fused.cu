@@ -454,6 +454,28 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
 }
 
 // ------------------------------------------------------------------ host
+// Auxiliary streams of the fork/join below (created on first use, same priority as the
+// KKT stream); false when kernels must run serially (per-kernel profiling).
+static bool ensure_aux(gn_kkt* K) {
+  if (profiling()) return false;
+  OpfKkt* X = K->opf;
+  int prio = 0;
+  GN_CK(cudaStreamGetPriority(K->stream, &prio));
+  if (!X->aux[0] || prio != X->aux_prio) {
+    for (auto& a : X->aux) {
+      if (a) GN_CK(cudaStreamDestroy(a));
+      GN_CK(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, prio));
+    }
+    if (!X->ev_fork) {
+      GN_CK(cudaEventCreateWithFlags(&X->ev_fork, cudaEventDisableTiming));
+      GN_CK(cudaEventCreateWithFlags(&X->ev_fork2, cudaEventDisableTiming));
+      for (auto& e : X->ev_join) GN_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    X->aux_prio = prio;
+  }
+  return true;
+}
+
 // The column kernels write disjoint parts of M.  In value mode they are forked over
 // the KKT stream and two auxiliary streams (fork/join by events: capturable in a CUDA
 // graph), so the short, low-occupancy degree-class launches overlap the flow-column
@@ -464,22 +486,9 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   OpfKkt* X = K->opf;
   const OpfKktTab& t = X->t;
   cudaStream_t s = K->stream;
-  const bool fork = !STRUCT && !profiling();
+  const bool fork = !STRUCT && ensure_aux(K);
   cudaStream_t lane[3] = {s, s, s};
   if (fork) {
-    int prio = 0;
-    GN_CK(cudaStreamGetPriority(s, &prio));
-    if (!X->aux[0] || prio != X->aux_prio) {
-      for (auto& a : X->aux) {
-        if (a) GN_CK(cudaStreamDestroy(a));
-        GN_CK(cudaStreamCreateWithPriority(&a, cudaStreamNonBlocking, prio));
-      }
-      if (!X->ev_fork) {
-        GN_CK(cudaEventCreateWithFlags(&X->ev_fork, cudaEventDisableTiming));
-        for (auto& e : X->ev_join) GN_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      }
-      X->aux_prio = prio;
-    }
     GN_CK(cudaEventRecord(X->ev_fork, s));
     for (int a = 0; a < 2; ++a) {
       GN_CK(cudaStreamWaitEvent(X->aux[a], X->ev_fork, 0));
@@ -529,30 +538,42 @@ void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, 
   launch_fused<false>(K, in, K->dvals.p, K->mvals.p, nullptr, nullptr);
 }
 
-static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow) {
+static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream_t st) {
   const OpfKktTab& t = K->opf->t;
   if (K->m <= 0) return;
   {
-    KTimer kt(skip_flow ? "k_opf_set_jac_fused<noflow>" : "k_opf_set_jac_fused", K->stream);
+    KTimer kt(skip_flow ? "k_opf_set_jac_fused<noflow>" : "k_opf_set_jac_fused", st);
     const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
     const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
                           (K->m - t.ramp0 + 31) / 32;
-    k_opf_set_jac_fused<<<(unsigned)((warps + kSJW - 1) / kSJW), kSJW * 32, 0, K->stream>>>(
+    k_opf_set_jac_fused<<<(unsigned)((warps + kSJW - 1) / kSJW), kSJW * 32, 0, st>>>(
         t, K->m, x, K->avals.p, skip_flow);
   }
   count_launch();
   GN_CK(cudaGetLastError());
 }
 
-void opf_set_jacobian_fused(gn_kkt* K, const double* x) { set_jac_launch(K, x, 0); }
+void opf_set_jacobian_fused(gn_kkt* K, const double* x) { set_jac_launch(K, x, 0, K->stream); }
 
 // set_jacobian_x + assemble_x at the same x (gn_kkt_update_x).  (Writing A's flow rows
 // from the flow-column kernel's line state was measured slower than the separate
 // set_jacobian pass: it costs that latency-bound kernel a third of its occupancy.)
 void opf_update_fused(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
                       const double* ss, double dw, double dc) {
-  set_jac_launch(K, x, 0);
-  opf_assemble_fused(K, x, w, ow, sx, ss, dw, dc);
+  // A (set_jacobian) and M (assemble) are independent given x: A is built on a third
+  // auxiliary stream beside the M kernels, so the two latency-bound phases overlap
+  OpfKkt* X = K->opf;
+  if (ensure_aux(K)) {
+    GN_CK(cudaEventRecord(X->ev_fork2, K->stream));
+    GN_CK(cudaStreamWaitEvent(X->aux[2], X->ev_fork2, 0));
+    set_jac_launch(K, x, 0, X->aux[2]);
+    GN_CK(cudaEventRecord(X->ev_join[2], X->aux[2]));
+    opf_assemble_fused(K, x, w, ow, sx, ss, dw, dc);
+    GN_CK(cudaStreamWaitEvent(K->stream, X->ev_join[2], 0));
+  } else {
+    set_jac_launch(K, x, 0, K->stream);
+    opf_assemble_fused(K, x, w, ow, sx, ss, dw, dc);
+  }
 }
 
 // Structure check of the fused enumeration (row index of every slot, column lengths).

@@ -81,12 +81,13 @@ bool fz_bus_fits(int32_t maxdeg);  // one warp's shared memory fits (else: no fu
 struct OpfKkt {
   bool ready = false;
   // fork/join of the column kernels over auxiliary streams (same priority as the KKT's)
-  cudaStream_t aux[2] = {nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_join[2] = {nullptr, nullptr};
+  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
   int aux_prio = 0;
   ~OpfKkt() {
     for (auto& a : aux) if (a) cudaStreamDestroy(a);
     if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_fork2) cudaEventDestroy(ev_fork2);
     for (auto& e : ev_join) if (e) cudaEventDestroy(e);
   }
   OpfKktTab t{};
