@@ -98,20 +98,25 @@ class Clocks:
     def mark(self):
         return time.perf_counter()
 
+    def close(self):
+        if self.nv is not None and not self._stop.is_set():
+            self._stop.set()
+            self.t.join(timeout=5)
+
     def stop(self, t0, t1):
         """Samples taken inside [t0, t1] (at least the 3 nearest when the timed
-        region is shorter than the NVML sampling period)."""
+        region is shorter than the NVML sampling period).  The sampler keeps running:
+        several timed windows can be read; close() ends it."""
         if self.nv is None:
             return None
-        self._stop.set()
-        self.t.join(timeout=5)
-        if not self.samples:
+        samples = list(self.samples)
+        if not samples:
             return None
-        inside = [x for x in self.samples if t0 <= x[0] <= t1]
+        inside = [x for x in samples if t0 <= x[0] <= t1]
         widened = len(inside) < 3
         if widened:
             mid = 0.5 * (t0 + t1)
-            inside = sorted(self.samples, key=lambda x: abs(x[0] - mid))[:3]
+            inside = sorted(samples, key=lambda x: abs(x[0] - mid))[:3]
         reasons = sorted({n for x in inside for n in x[2]})
         return {"sm_mhz": float(np.median([x[1] for x in inside])),
                 "sm_max_mhz": float(self.max_mhz), "reasons": reasons, "samples": len(inside),
@@ -482,8 +487,10 @@ def run_ours(args, rank, world, local_rank, dist):
                 gev[k][1].record(stream)
         torch.cuda.synchronize()
         clk = clocks.stop(t_clk0, clocks.mark())
+        clocks.close()
         assert nlp.status(), "evaluation failed in the graph-timed region"
         ms = float(np.mean([a.elapsed_time(b) for a, b in gev]))
+    clocks.close()
     if dist:
         import torch.distributed as tdist
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
