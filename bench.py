@@ -515,7 +515,7 @@ def run_ours(args, rank, world, local_rank, dist):
 
     # line-search trial point: f and g only, one call (gn_eval_fg)
     tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(10)]
+           for _ in range(0 if args.no_trial else 10)]
     for a_, b_ in tev:
         with torch.cuda.stream(stream):
             flush.zero_()
@@ -524,7 +524,7 @@ def run_ours(args, rank, world, local_rank, dist):
             b_.record(stream)
     torch.cuda.synchronize()
     assert nlp.status()
-    trial_ms = float(np.median([a_.elapsed_time(b_) for a_, b_ in tev]))
+    trial_ms = float(np.median([a_.elapsed_time(b_) for a_, b_ in tev])) if tev else float("nan")
     trial_bytes = 8 * (s.n_vars + s.n_cons + 1)  # x read once, g and f written once
     trial = {"ms": trial_ms, "alg_bytes": trial_bytes,
              "gbs": trial_bytes / (trial_ms * 1e-3) / 1e9,
@@ -779,6 +779,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
     ap.add_argument("--streams", type=int, choices=[1, 2], default=2)
+    ap.add_argument("--no-trial", action="store_true",
+                    help="skip the line-search trial (gn_eval_fg) measurement")
     ap.add_argument("--no-ipm-ops", action="store_true",
                     help="skip the device-resident IPM vector-op measurement")
     ap.add_argument("--graph", type=int, choices=[0, 1], default=1,
