@@ -43,6 +43,10 @@ def pretty(name: str) -> str:
     for k in ("k_line", "k_gen", "k_thermal", "k_ramp"):
         if n.startswith(k + "<") and n[len(k) + 1:-1] in MODES:
             return f"{k}<{MODES[n[len(k) + 1:-1]]}>"
+    import re
+    mm = re.fullmatch(r"k_fz_busr<(\d+), 0>", n)
+    if mm:
+        return f"k_fz_busr<d{mm.group(1)}>"
     for k in ("k_fz_bus3", "k_fz_line", "k_fz_gen", "k_opf_assemble"):
         if n == k + "<0>":
             return k
