@@ -258,7 +258,7 @@ __device__ void col_v(const OpfKktTab& t, const In& in, int32_t n, int32_t tt, O
     }
     if (!self_done && n < nb) {  // the (th(n), v(n)) slot: every incident line
       self_done = true;
-      if (freev(t, C_TH, n)) {
+      if (b1 > b0 && freev(t, C_TH, n)) {  // (an isolated bus has no such entry)
         double acc = 0.0;
         if constexpr (!STRUCT) {
           for (int32_t u = b0; u < b1; ++u) {
@@ -667,7 +667,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
           const int32_t ob = k < groups.size() ? groups[k].first : 0x7fffffff;
           if (!self && n < ob) {
             self = true;
-            if (tfree_n) slot(all, 2, n);
+            if (tfree_n && deg > 0) slot(all, 2, n);  // no (th(n), v(n)) without lines
           }
           if (k < groups.size() && !fixed[offs[C_TH] + ob]) slot(groups[k].second, 3, ob);
         }

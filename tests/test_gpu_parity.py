@@ -366,3 +366,52 @@ def test_line_search_trial_fg(gpu):
         okg, _, failg = orc.eval_g(xb)
         assert ok == (oko and okg)
         assert nlp.last_error == (failf if not oko else failg)
+
+
+def test_fused_kkt_isolated_and_high_degree_buses(gpu):
+    """Buses outside the register-resident classes: an isolated bus (no lines; its
+    v/th columns hold only dw + Sx) and a hub of degree 9 (slot-program class), next
+    to parallel lines; fused == contract bit for bit, and the contract path == oracle."""
+    from paper_2405_14032_b200.network import RawCase
+    from paper_2405_14032_b200.opf import load_profile
+    raw = synthetic_case(80, 130, 20, 60, seed=23, parallel_lines=3, shared_gens=2)
+    bus, gen, br, gc = raw.bus.copy(), raw.gen.copy(), raw.branch.copy(), raw.gencost.copy()
+    nb = int(bus[:, 0].max())
+    iso = bus[5].copy()
+    iso[0], iso[1] = nb + 1, 1  # a PQ bus with the load of bus 6 and no branch
+    bus = np.vstack([bus, iso])
+    g = gen[0].copy()
+    g[0] = nb + 1
+    gen = np.vstack([gen, g])
+    gc = np.vstack([gc, gc[0]])
+    hub = int(bus[10, 0])
+    extra = []
+    for k in range(7):  # degree 2 + 7 chords = 9 at the hub
+        row = br[0].copy()
+        row[0], row[1] = hub, int(bus[(20 + 7 * k) % 80, 0])
+        extra.append(row)
+    br = np.vstack([br] + extra)
+    raw2 = RawCase(raw.base_mva, bus, gen, br, gc)
+    net = raw2.network()
+    T = 5
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale)
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, 31)
+    w = row_weights(nlp.sizes.n_cons, 32, zero_every=6)
+    sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, 33)
+    _fused_check(nlp, K, x, w, 0.9, sx, ss)
+    orc = B.OracleModel(net, T, scale)
+    lo = orc.lift(1e-4)
+    Ko = orc.kkt()
+    ok, jv, _ = orc.eval_jac(x)
+    ok2, hv, _ = orc.eval_hess(x, w, 0.9)
+    Ko.set_jacobian(jv[lo["jac_pick"]])
+    Ko.assemble(hv[lo["hess_pick"]], sx, ss, *DELTAS[1])
+    K.update_x(x, w, 0.9, sx, ss, *DELTAS[1])
+    a, m = K.values()
+    a_o, m_o = Ko.values()
+    assert_close(m, m_o, what="fused M vs oracle (sin/cos ulps)")
+    assert_close(a, a_o, what="fused A vs oracle")
