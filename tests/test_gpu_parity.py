@@ -415,3 +415,50 @@ def test_fused_kkt_isolated_and_high_degree_buses(gpu):
     a_o, m_o = Ko.values()
     assert_close(m, m_o, what="fused M vs oracle (sin/cos ulps)")
     assert_close(a, a_o, what="fused A vs oracle")
+
+
+def test_degree_above_32_falls_back_loudly(gpu):
+    """A bus with more than 32 lines exceeds the fused kernels' one-line-per-lane
+    layout: the fused path reports GN_ERR_UNSUPPORTED (never a silent wrong answer)
+    and the contract KKT still matches the oracle."""
+    from paper_2405_14032_b200.network import RawCase
+    from paper_2405_14032_b200.opf import load_profile
+    raw = synthetic_case(120, 200, 25, 90, seed=29)
+    br = raw.branch.copy()
+    hub = int(raw.bus[3, 0])
+    extra = []
+    for k in range(34):
+        row = br[0].copy()
+        row[0], row[1] = hub, int(raw.bus[(10 + 3 * k) % 120, 0])
+        if row[1] != hub:
+            extra.append(row)
+    raw2 = RawCase(raw.base_mva, raw.bus, raw.gen, np.vstack([br] + extra), raw.gencost)
+    net = raw2.network()
+    T = 3
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale)
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    assert K.fused_ready == 0
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, 41)
+    w = row_weights(nlp.sizes.n_cons, 42)
+    sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, 43)
+    with pytest.raises(GridError) as e:
+        K.update_x(x, w, 1.0, sx, ss, *DELTAS[1])
+    assert e.value.code == 4  # GN_ERR_UNSUPPORTED
+    ok, jv = nlp.eval_jac(x)
+    ok2, hv = nlp.eval_hess(x, w, 1.0)
+    K.set_jacobian(jv, mem=GN_IN_FULL)
+    K.assemble(hv, sx, ss, *DELTAS[1], mem=GN_IN_FULL)
+    a, m = K.values()
+    orc = B.OracleModel(net, T, scale)
+    lo = orc.lift(1e-4)
+    Ko = orc.kkt()
+    ok, jo, _ = orc.eval_jac(x)
+    ok2, ho, _ = orc.eval_hess(x, w, 1.0)
+    Ko.set_jacobian(jo[lo["jac_pick"]])
+    Ko.assemble(ho[lo["hess_pick"]], sx, ss, *DELTAS[1])
+    a_o, m_o = Ko.values()
+    assert_close(m, m_o, what="M (fallback) vs oracle")
+    assert_close(a, a_o, what="A (fallback) vs oracle")
