@@ -462,3 +462,38 @@ def test_degree_above_32_falls_back_loudly(gpu):
     a_o, m_o = Ko.values()
     assert_close(m, m_o, what="M (fallback) vs oracle")
     assert_close(a, a_o, what="A (fallback) vs oracle")
+
+
+@pytest.mark.parametrize("T", [1, 3])
+def test_no_thermal_no_ramp_patterns(gpu, T):
+    """Empty pattern blocks: every line unrated (no thermal rows, LT = 0) and no ramping
+    generator (GR = 0) -- the pattern ids shift; callbacks, failure ids
+    and the fused KKT must follow."""
+    from paper_2405_14032_b200.opf import load_profile
+    raw = synthetic_case(70, 110, 15, 50, seed=37, parallel_lines=2)
+    net = raw.network()
+    net.line_smax[:] = np.inf
+    net.gen_ramp[:] = np.inf
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale)
+    orc = B.OracleModel(net, T, scale)
+    assert [nlp.sizes.n_vars, nlp.sizes.n_cons, nlp.sizes.jac_nnz, nlp.sizes.hess_nnz] == \
+        orc.sizes[:4]
+    assert nlp.sizes.n_thermal == 0 and nlp.sizes.n_ramp_gens == 0
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, 51)
+    w = row_weights(nlp.sizes.n_cons, 52, zero_every=4)
+    for name, args in [("eval_g", (x,)), ("eval_jac", (x,)), ("eval_hess", (x, w, 0.6))]:
+        ok, v = getattr(nlp, name)(*args)
+        oko, vo, _ = getattr(orc, name)(*args)
+        assert ok and oko
+        assert_close(v, vo, what=name)
+    xb = x.copy()
+    xb[len(x) // 2] = np.nan  # a flow variable: the failing pattern id shifts with LT = 0
+    ok, _ = nlp.eval_g(xb)
+    oko, _, fail = orc.eval_g(xb)
+    assert not ok and not oko and nlp.last_error == fail
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, 53)
+    _fused_check(nlp, K, x, w, 0.6, sx, ss)
