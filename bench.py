@@ -322,6 +322,11 @@ def profile_kernels(L, step, steps, stream, flush):
 
 
 def run_ours(args, rank, world, local_rank, dist):
+    if args.streams == 2:
+        # the KKT kernels launch at most 2 CTAs per SM (grid-stride), leaving room for the
+        # callback stream's bandwidth-bound kernels to run beside them (measured best of
+        # 1, 2, 3, 4, 8 and uncapped; read once by the library, so set before any launch)
+        os.environ.setdefault("GRIDNLP_B200_GRID_CAP", "2")
     import torch
     from paper_2405_14032_b200 import abi
     from paper_2405_14032_b200.abi import GN_IN_FULL, GN_MEM_DEVICE_ASYNC, GN_MEM_HOST
@@ -656,7 +661,8 @@ def run_ours(args, rank, world, local_rank, dist):
         "stages_ms": per_stage,
         "line_search_trial": trial,
         "ipm_vector_ops": ipm_ops,
-        "launch": ("cuda_graph (eager step %.4f ms)" % eager_ms) if graph_mode else "eager",
+        "launch": (("cuda_graph (eager step %.4f ms)" % eager_ms) if graph_mode else "eager")
+        + "; KKT grid cap %s CTA/SM" % os.environ.get("GRIDNLP_B200_GRID_CAP", "0"),
         "setup_s": setup_s,
         "clocks": clk,
         "e2e": e2e,

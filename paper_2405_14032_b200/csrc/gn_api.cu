@@ -303,13 +303,22 @@ int gn_ctx_shard_info(gn_ctx* c, int64_t* info, int32_t* ramp_gens) {
   return GN_OK;
 }
 
-int gn_ctx_destroy(gn_ctx* c) {
-  if (!c) return GN_OK;
+// Objects built on another (a KKT on a context, an IPM on a KKT) hold a reference: a
+// destroy call on an object still referenced only marks it closed, and the last
+// dependent's destroy frees it -- destroy calls may come in any order (e.g. from a
+// garbage collector) without a dependent ever touching a freed stream or table.
+static void ctx_free(gn_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaStream_t s = c->owned_stream;  // the caller's stream (set_stream) is never destroyed
   delete c;
   if (s) cudaStreamDestroy(s);
+}
+
+int gn_ctx_destroy(gn_ctx* c) {
+  if (!c) return GN_OK;
+  c->closed = true;
+  if (c->refs == 0) ctx_free(c);
   return GN_OK;
 }
 
@@ -591,6 +600,7 @@ int gn_kkt_create_lifted(gn_ctx* c, gn_kkt** out, gn_error* err) {
   K = new gn_kkt();
   K->device = c->device;
   K->ctx = c;
+  ++c->refs;
   K->stream = c->stream;
   K->own_stream = false;
   K->n = c->n_free; K->m = c->d.m; K->nj = c->nj_l; K->nh = c->nh_l;
@@ -610,14 +620,21 @@ int gn_kkt_create_lifted(gn_ctx* c, gn_kkt** out, gn_error* err) {
   }
 }
 
-int gn_kkt_destroy(gn_kkt* K) {
-  if (!K) return GN_OK;
+static void kkt_free(gn_kkt* K) {
   cudaSetDevice(K->device);
   if (K->stream) cudaStreamSynchronize(K->stream);
   cudaStream_t s = K->owned_stream;
+  gn_ctx* c = K->ctx;
   gnb::opf_kkt_free(K);
   delete K;
   if (s) cudaStreamDestroy(s);
+  if (c && --c->refs == 0 && c->closed) ctx_free(c);
+}
+
+int gn_kkt_destroy(gn_kkt* K) {
+  if (!K) return GN_OK;
+  K->closed = true;
+  if (K->refs == 0) kkt_free(K);
   return GN_OK;
 }
 
@@ -829,6 +846,7 @@ int gn_ipm_create(gn_kkt* K, const double* xl, const double* xu, const double* s
   API_TRY
   set_device(K->device);
   *out = gnb::ipm_create(K, xl, xu, sl, su, is_device(mem));
+  ++K->refs;
   return ok(err);
   API_CATCH(err)
 }
@@ -837,7 +855,9 @@ int gn_ipm_destroy(gn_ipm* P) {
   if (!P) return GN_OK;
   cudaSetDevice(P->device);
   cudaStreamSynchronize(P->K->stream);
+  gn_kkt* K = P->K;
   delete P;
+  if (--K->refs == 0 && K->closed) kkt_free(K);
   return GN_OK;
 }
 

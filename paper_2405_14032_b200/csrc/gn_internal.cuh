@@ -138,6 +138,8 @@ struct gn_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t owned_stream = nullptr;  // created here; destroyed with the object
+  int refs = 0;         // live objects built on this one (KKTs / IPMs)
+  bool closed = false;  // destroy requested; freed when refs drops to 0
   gnb::OpfDims d{};
   // host copies of the network (bounds, starts)
   std::vector<double> bus_vmin, bus_vmax, vm_start, va_start;

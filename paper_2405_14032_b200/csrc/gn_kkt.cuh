@@ -26,6 +26,8 @@ struct gn_kkt {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   cudaStream_t owned_stream = nullptr;  // created here; destroyed with the object
+  int refs = 0;         // live objects built on this one (KKTs / IPMs)
+  bool closed = false;  // destroy requested; freed when refs drops to 0
   gn_ctx* ctx = nullptr;  // set for gn_kkt_create_lifted
   int32_t n = 0, m = 0;
   int64_t nj = 0, nh = 0, npair = 0;

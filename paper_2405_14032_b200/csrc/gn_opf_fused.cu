@@ -25,6 +25,7 @@
 namespace gnb {
 
 
+
 template <bool STRUCT>
 struct FOut {
   double* M;
@@ -174,17 +175,18 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
 constexpr int kFLW = 8;     // warps per CTA
 constexpr int kFLCap = 16;  // staged slots per column (longer columns are written in place)
 template <bool STRUCT>
-__global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, const double* __restrict__ x,
-                                                      const double* __restrict__ w,
-                                                      const double* __restrict__ sx, double dw,
-                                                      const double* __restrict__ dv,
-                                                      double* __restrict__ M,
-                                                      int32_t* __restrict__ rows,
-                                                      int32_t* __restrict__ bad) {
+__device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
+                                             const double* __restrict__ x,
+                                             const double* __restrict__ w,
+                                             const double* __restrict__ sx, double dw,
+                                             const double* __restrict__ dv,
+                                             double* __restrict__ M,
+                                             int32_t* __restrict__ rows,
+                                             int32_t* __restrict__ bad) {
   __shared__ double stg_all[STRUCT ? 1 : kFLW * kFLCap * 33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t T = t.T;
-  const int64_t wg = (int64_t)blockIdx.x * kFLW + warp;
+  const int64_t wg = vblock * kFLW + warp;
   const int32_t l = (int32_t)(wg / t.tchunks);
   if (l >= t.L) return;  // warp-uniform
   const int32_t c0 = (int32_t)(wg - (int64_t)l * t.tchunks) * 32;
@@ -294,6 +296,32 @@ __global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, const double
   else columns(std::false_type{});
 }
 
+// Grid-stride wrapper: `nvb` virtual CTAs on at most gridDim.x resident CTAs (the grid can be
+// capped so that the latency-bound KKT kernels leave SM room for the callback stream).
+template <bool STRUCT>
+__global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, int64_t nvb,
+                                                      const double* __restrict__ x,
+                                                      const double* __restrict__ w,
+                                                      const double* __restrict__ sx, double dw,
+                                                      const double* __restrict__ dv,
+                                                      double* __restrict__ M,
+                                                      int32_t* __restrict__ rows,
+                                                      int32_t* __restrict__ bad) {
+  fz_line_body<STRUCT>(blockIdx.x, t, x, w, sx, dw, dv, M, rows, bad);
+}
+template <bool STRUCT>
+__global__ void __launch_bounds__(kFLW * 32, 3) k_fz_line_gs(OpfKktTab t, int64_t nvb,
+                                                         const double* __restrict__ x,
+                                                         const double* __restrict__ w,
+                                                         const double* __restrict__ sx, double dw,
+                                                         const double* __restrict__ dv,
+                                                         double* __restrict__ M,
+                                                         int32_t* __restrict__ rows,
+                                                         int32_t* __restrict__ bad) {
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x)
+    fz_line_body<STRUCT>(vb, t, x, w, sx, dw, dv, M, rows, bad);
+}
+
 template <bool STRUCT>
 __global__ void __launch_bounds__(256) k_fz_gen(OpfKktTab t, FIn in, const double* __restrict__ dv,
                                                 double* __restrict__ M, int32_t* __restrict__ rows,
@@ -363,15 +391,14 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 //   * angle rows of a line (all periods): (+1, -1) at the free angle slots;
 //   * ramp rows: one thread per row.
 constexpr int kSJW = 8;  // warps per CTA
-__global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t, int32_t m,
-                                                                const double* __restrict__ x,
-                                                                double* __restrict__ A,
-                                                                int skip_flow) {
+__device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t, int32_t m,
+                                             const double* __restrict__ x,
+                                             double* __restrict__ A, int skip_flow) {
   __shared__ double stg_all[kSJW * 5 * 33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t T = t.T, tch = t.tchunks;
   const int32_t LT = (t.ang0 - t.therm0) / (T > 0 ? T : 1);
-  int64_t wg = (int64_t)blockIdx.x * kSJW + warp;
+  int64_t wg = vblock * kSJW + warp;
   if (wg < 2ll * t.N) {  // balance rows of bus b, all periods
     const bool Q = wg >= t.N;
     const int32_t b = (int32_t)(wg - (Q ? t.N : 0));
@@ -453,6 +480,21 @@ __global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t,
   }
 }
 
+__global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t, int64_t nvb,
+                                                                int32_t m,
+                                                                const double* __restrict__ x,
+                                                                double* __restrict__ A,
+                                                                int skip_flow) {
+  set_jac_body(blockIdx.x, t, m, x, A, skip_flow);
+}
+__global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused_gs(OpfKktTab t, int64_t nvb,
+                                                                   int32_t m,
+                                                                   const double* __restrict__ x,
+                                                                   double* __restrict__ A,
+                                                                   int skip_flow) {
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) set_jac_body(vb, t, m, x, A, skip_flow);
+}
+
 // ------------------------------------------------------------------ host
 // Auxiliary streams of the fork/join below (created on first use, same priority as the
 // KKT stream); false when kernels must run serially (per-kernel profiling).
@@ -507,8 +549,12 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   if (nl > 0) {
     KTimer kt("k_fz_line", s);
     const int64_t warps = (int64_t)t.L * t.tchunks;
-    k_fz_line<STRUCT><<<(unsigned)((warps + kFLW - 1) / kFLW), kFLW * 32, 0, s>>>(
-        t, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
+    const int64_t nvb = (warps + kFLW - 1) / kFLW;
+    const unsigned g = grid_cap(nvb);
+    if (g < nvb)  // capped grid: the grid-stride variant
+      k_fz_line_gs<STRUCT><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
+    else
+      k_fz_line<STRUCT><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
     count_launch();
   }
   if (ng > 0) {
@@ -546,8 +592,12 @@ static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream
     const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
     const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
                           (K->m - t.ramp0 + 31) / 32;
-    k_opf_set_jac_fused<<<(unsigned)((warps + kSJW - 1) / kSJW), kSJW * 32, 0, st>>>(
-        t, K->m, x, K->avals.p, skip_flow);
+    const int64_t nvb = (warps + kSJW - 1) / kSJW;
+    const unsigned g = grid_cap(nvb);
+    if (g < nvb)
+      k_opf_set_jac_fused_gs<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
+    else
+      k_opf_set_jac_fused<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
   }
   count_launch();
   GN_CK(cudaGetLastError());

@@ -272,14 +272,13 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
 // pass-major sweep, each neighbour slot is its line's terms in pass order, and
 // every value goes to its precomputed offset in the column (bpos, boff).
 template <int DEG, bool STRUCT>
-__global__ void __launch_bounds__(kBW3 * 32) k_fz_busr(OpfKktTab t, const int4* __restrict__ buses,
-                                                    int32_t n_buses, FIn in,
-                                                    const double* __restrict__ dv,
-                                                    double* __restrict__ M,
-                                                    int32_t* __restrict__ rows,
-                                                    int32_t* __restrict__ bad) {
+__device__ __forceinline__ void busr_body(int64_t vblock, const OpfKktTab& t,
+                                          const int4* __restrict__ buses, int32_t n_buses,
+                                          const FIn& in, const double* __restrict__ dv,
+                                          double* __restrict__ M, int32_t* __restrict__ rows,
+                                          int32_t* __restrict__ bad) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kBW3 + warp;
+  const int64_t w = vblock * kBW3 + warp;
   const int64_t n64 = w / t.tchunks;
   if (n64 >= n_buses) return;
   const int32_t T = t.T;
@@ -434,18 +433,36 @@ __global__ void __launch_bounds__(kBW3 * 32) k_fz_busr(OpfKktTab t, const int4* 
   }
 }
 
+template <int DEG, bool STRUCT>
+__global__ void __launch_bounds__(kBW3 * 32) k_fz_busr(OpfKktTab t, int64_t nvb,
+                                                    const int4* __restrict__ buses,
+                                                    int32_t n_buses, FIn in,
+                                                    const double* __restrict__ dv,
+                                                    double* __restrict__ M,
+                                                    int32_t* __restrict__ rows,
+                                                    int32_t* __restrict__ bad) {
+  if (nvb <= gridDim.x) {  // (uncapped grid: one virtual CTA per CTA)
+    busr_body<DEG, STRUCT>(blockIdx.x, t, buses, n_buses, in, dv, M, rows, bad);
+    return;
+  }
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x)
+    busr_body<DEG, STRUCT>(vb, t, buses, n_buses, in, dv, M, rows, bad);
+}
+
 template <int DEG>
 static void launch_busr(const OpfKktTab& t, const int4* buses, int32_t n_buses, const FIn& in,
                         const double* dv, double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
   static const char* names[] = {"", "k_fz_busr<d1>", "k_fz_busr<d2>", "k_fz_busr<d3>",
                                 "k_fz_busr<d4>", "k_fz_busr<d5>", "k_fz_busr<d6>"};
   const int64_t warps = (int64_t)n_buses * t.tchunks;
-  const unsigned blocks = (unsigned)((warps + kBW3 - 1) / kBW3);
+  const int64_t nvb = (warps + kBW3 - 1) / kBW3;
   KTimer kt(names[DEG], s);
   if (rows)
-    k_fz_busr<DEG, true><<<blocks, kBW3 * 32, 0, s>>>(t, buses, n_buses, in, dv, M, rows, bad);
+    k_fz_busr<DEG, true><<<grid_cap(nvb), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+                                                             rows, bad);
   else
-    k_fz_busr<DEG, false><<<blocks, kBW3 * 32, 0, s>>>(t, buses, n_buses, in, dv, M, rows, bad);
+    k_fz_busr<DEG, false><<<grid_cap(nvb), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+                                                              rows, bad);
   count_launch();
 }
 

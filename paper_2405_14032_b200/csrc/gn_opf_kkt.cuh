@@ -1,7 +1,21 @@
 #pragma once
 #include "gn_kkt.cuh"
 
+#include <algorithm>
+#include <cstdlib>
+
 namespace gnb {
+
+// CTAs actually launched for `nvb` virtual CTAs: GRIDNLP_B200_GRID_CAP = resident CTAs per SM
+// to allow (0 or unset: one CTA per virtual CTA, the plain grid).
+inline unsigned grid_cap(int64_t nvb) {
+  static const int cap = [] {
+    const char* e = std::getenv("GRIDNLP_B200_GRID_CAP");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (cap <= 0) return (unsigned)nvb;
+  return (unsigned)std::min<int64_t>(nvb, (int64_t)cap * 148);
+}
 
 // Column / row blocks of the lifted OPF variables, in variable order.
 enum ColType { C_PG = 0, C_QG, C_P, C_Q, C_V, C_TH, C_TYPES };

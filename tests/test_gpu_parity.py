@@ -497,3 +497,32 @@ def test_no_thermal_no_ramp_patterns(gpu, T):
     K = CondensedKkt(nlp=nlp)
     sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, 53)
     _fused_check(nlp, K, x, w, 0.6, sx, ss)
+
+
+@pytest.mark.parametrize("order", [(0, 1, 2), (2, 1, 0), (1, 0, 2), (0, 2, 1)])
+def test_destroy_order_any(gpu, order):
+    """Context, KKT and IPM objects may be destroyed in any order (a garbage collector
+    finalising a reference cycle does): a destroyed object that others were built on
+    stays alive until the last of them goes, and the survivors keep working."""
+    import torch
+    from paper_2405_14032_b200.opf import Ipm, load_profile
+    raw = synthetic_case(40, 60, 8, 30, seed=3)
+    net = raw.network()
+    nlp = OpfNlp(net, 3, load_profile(net.n_load, 3))
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    st = nlp.lifted_structure()
+    xl, xu, xs, _, _ = nlp.bounds()
+    f2f = st["free_to_full"]
+    ipm = Ipm(K, xl[f2f], xu[f2f], st["s_lower"], st["s_upper"])
+    objs = [nlp, K, ipm]
+    x = interior_point(xl, xu, xs, 5)
+    for i in order:
+        objs[i].close()
+        if not isinstance(objs[1], CondensedKkt) or objs[1].h is None:
+            continue
+        if objs[1].fused_ready and objs[1].h is not None:  # the KKT still works
+            w = row_weights(nlp.sizes.n_cons, 6)
+            sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, 7)
+            objs[1].update_x(x, w, 1.0, sx, ss, *DELTAS[0])
+    torch.cuda.synchronize()
