@@ -29,6 +29,8 @@
 namespace gnb {
 
 constexpr int kBW3 = 4;  // warps per CTA
+// resident CTAs per SM the register allocation of k_fz_busr<DEG> must allow
+constexpr int kBusrMinBlocks[7] = {1, 8, 5, 4, 3, 2, 2};
 constexpr int kSV = 11;
 constexpr int kBusSmemMax = 200 * 1024;  // dynamic shared memory cap of the bus kernel  // shared doubles per (line, lane): Cs Sn cs sn vf vt w7 w8 d7 d8 d10
 
@@ -434,7 +436,7 @@ __device__ __forceinline__ void busr_body(int64_t vblock, const OpfKktTab& t,
 }
 
 template <int DEG, bool STRUCT>
-__global__ void __launch_bounds__(kBW3 * 32) k_fz_busr(OpfKktTab t, int64_t nvb,
+__global__ void __launch_bounds__(kBW3 * 32, kBusrMinBlocks[DEG]) k_fz_busr(OpfKktTab t, int64_t nvb,
                                                     const int4* __restrict__ buses,
                                                     int32_t n_buses, FIn in,
                                                     const double* __restrict__ dv,
