@@ -582,7 +582,10 @@ bool opf_kkt_prepare(gn_kkt* K) {
       if (ty == C_PG || ty == C_QG) key = c->gen_bus[e];
       else if (ty == C_P || ty == C_Q) key = std::min(c->line_from[e], c->line_to[e]);
       else key = e;
-      order.push_back({((int64_t)key * C_TYPES + ty) * (1ll << 31) + e, (ty << 28) | e});
+      // grouped by column type first (neighbouring warps run the same code path: the
+      // kernel's per-type paths no longer thrash the instruction cache), then by
+      // network locality (key bus) within a type
+      order.push_back({((int64_t)ty * (1ll << 31) + key) * (1ll << 31) + e, (ty << 28) | e});
     }
   std::sort(order.begin(), order.end());
   std::vector<int32_t> items;
