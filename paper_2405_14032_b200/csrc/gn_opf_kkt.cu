@@ -18,6 +18,8 @@
 #include <algorithm>
 #include <numeric>
 
+#include <type_traits>
+
 #include "gn_opf_kkt.cuh"
 
 namespace gnb {
@@ -444,32 +446,52 @@ __device__ void col_gen(const OpfKktTab& t, const In& in, int32_t g, int32_t tt,
 
 // One warp per (entity, 32 consecutive periods): control flow and the per-entity
 // table reads are warp-uniform; sigma, rowptr and the M columns of the warp are
-// contiguous.  Work items are ordered by network locality (key bus) so that all
-// consumers of a line's H records / A rows run close together and hit in L2.
-template <bool STRUCT>
-__global__ void __launch_bounds__(kMB) k_opf_assemble(OpfKktTab t, In in, double* __restrict__ M,
+// contiguous.  Work items are grouped by column type, then ordered by network
+// locality (key bus) so that all consumers of a line's H records / A rows of one
+// type run close together and hit in L2.
+// One launch per column type (the items are grouped by type): each kernel carries only its
+// own code path, so the instruction cache holds it and its registers are its own.
+template <bool STRUCT, int TYPE>
+__global__ void __launch_bounds__(kMB) k_opf_assemble(OpfKktTab t, In in, int32_t item0,
+                                                      int32_t n_items, double* __restrict__ M,
                                                       int32_t* __restrict__ rows,
                                                       int32_t* __restrict__ bad) {
   const int64_t w = ((int64_t)blockIdx.x * kMB + threadIdx.x) >> 5;
   const int32_t lane = threadIdx.x & 31;
-  const int64_t item = w / t.tchunks;
-  if (item >= t.n_items) return;
-  const int32_t tt = (int32_t)(w - item * t.tchunks) * 32 + lane;
+  const int64_t it = w / t.tchunks;
+  if (it >= n_items) return;
+  const int32_t tt = (int32_t)(w - it * t.tchunks) * 32 + lane;
   if (tt >= t.T) return;
-  const int32_t code = __ldg(t.items + item);
-  const int type = code >> 28;
-  const int32_t e = code & 0x0fffffff;
-  const int32_t c = lv(t, type, e, tt);
+  const int32_t e = __ldg(t.items + item0 + it) & 0x0fffffff;
+  const int32_t c = lv(t, TYPE, e, tt);
   Out<STRUCT> o{M, rows, __ldg(t.colptr + c)};
-  switch (type) {
-    case C_PG: col_gen<STRUCT, false>(t, in, e, tt, o); break;
-    case C_QG: col_gen<STRUCT, true>(t, in, e, tt, o); break;
-    case C_P: col_flow<STRUCT, false>(t, in, e, tt, o); break;
-    case C_Q: col_flow<STRUCT, true>(t, in, e, tt, o); break;
-    case C_V: col_v<STRUCT>(t, in, e, tt, o); break;
-    default: col_th<STRUCT>(t, in, e, tt, o); break;
-  }
+  if constexpr (TYPE == C_PG) col_gen<STRUCT, false>(t, in, e, tt, o);
+  else if constexpr (TYPE == C_QG) col_gen<STRUCT, true>(t, in, e, tt, o);
+  else if constexpr (TYPE == C_P) col_flow<STRUCT, false>(t, in, e, tt, o);
+  else if constexpr (TYPE == C_Q) col_flow<STRUCT, true>(t, in, e, tt, o);
+  else if constexpr (TYPE == C_V) col_v<STRUCT>(t, in, e, tt, o);
+  else col_th<STRUCT>(t, in, e, tt, o);
   if (STRUCT && o.base + o.j != __ldg(t.colptr + c + 1)) atomicOr(bad, 1);
+}
+
+template <bool STRUCT>
+static void launch_assemble(const OpfKktTab& t, const int32_t* type_lo, const In& in, double* M,
+                            int32_t* rows, int32_t* bad, cudaStream_t s) {
+  auto go = [&](auto type_tag) {
+    constexpr int TY = decltype(type_tag)::value;
+    const int32_t n = type_lo[TY + 1] - type_lo[TY];
+    if (n <= 0) return;
+    const int64_t warps = (int64_t)n * t.tchunks;
+    const unsigned blocks = (unsigned)((warps * 32 + kMB - 1) / kMB);
+    k_opf_assemble<STRUCT, TY><<<blocks, kMB, 0, s>>>(t, in, type_lo[TY], n, M, rows, bad);
+    count_launch();
+  };
+  go(std::integral_constant<int, C_PG>{});
+  go(std::integral_constant<int, C_QG>{});
+  go(std::integral_constant<int, C_P>{});
+  go(std::integral_constant<int, C_Q>{});
+  go(std::integral_constant<int, C_V>{});
+  go(std::integral_constant<int, C_TH>{});
 }
 
 static int64_t assemble_blocks(const OpfKktTab& t) {
@@ -585,13 +607,16 @@ bool opf_kkt_prepare(gn_kkt* K) {
       // grouped by column type first (neighbouring warps run the same code path: the
       // kernel's per-type paths no longer thrash the instruction cache), then by
       // network locality (key bus) within a type
-      order.push_back({((int64_t)ty * (1ll << 31) + key) * (1ll << 31) + e, (ty << 28) | e});
+      order.push_back({((int64_t)ty << 59) | ((int64_t)key << 28) | e, (ty << 28) | e});
     }
   std::sort(order.begin(), order.end());
   std::vector<int32_t> items;
   items.reserve(order.size());
   for (auto& pr : order) items.push_back(pr.second);
   t.n_items = static_cast<int32_t>(items.size());
+  for (int ty = 0; ty <= C_TYPES; ++ty) X->type_lo[ty] = 0;
+  for (auto& pr : order) ++X->type_lo[(pr.second >> 28) + 1];
+  for (int ty = 0; ty < C_TYPES; ++ty) X->type_lo[ty + 1] += X->type_lo[ty];
   t.tchunks = (d.T + 31) / 32;
   auto vfree = [&](int32_t n) { return !fixed[offs[C_V] + n]; };
   auto tfree = [&](int32_t n) { return !fixed[offs[C_TH] + n]; };
@@ -879,8 +904,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
     bad.alloc(1);
     GN_CK(cudaMemsetAsync(bad.p, 0, 4, s));
     In in{};
-    k_opf_assemble<true><<<(unsigned)blocks, kMB, 0, s>>>(t, in, nullptr, rows.p, bad.p);
-    count_launch();
+    launch_assemble<true>(t, X->type_lo, in, nullptr, rows.p, bad.p, s);
     GN_CK(cudaGetLastError());
     int32_t hb = 0;
     GN_CK(cudaMemcpyAsync(&hb, bad.p, 4, cudaMemcpyDeviceToHost, s));
@@ -924,8 +948,7 @@ void opf_assemble(gn_kkt* K, const double* Hfull, const double* sx, const double
   if (blocks <= 0) return;
   In in{Hfull, K->avals.p, sx, ss, dw, dc};
   KTimer kt("k_opf_assemble", K->stream);
-  k_opf_assemble<false><<<(unsigned)blocks, kMB, 0, K->stream>>>(t, in, K->mvals.p, nullptr, nullptr);
-  count_launch();
+  launch_assemble<false>(t, K->opf->type_lo, in, K->mvals.p, nullptr, nullptr, K->stream);
   GN_CK(cudaGetLastError());
 }
 

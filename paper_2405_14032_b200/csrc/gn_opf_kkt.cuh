@@ -94,6 +94,7 @@ bool fz_bus_fits(int32_t maxdeg);  // one warp's shared memory fits (else: no fu
 
 struct OpfKkt {
   bool ready = false;
+  int32_t type_lo[C_TYPES + 1] = {};  // items of column type ty: [type_lo[ty], type_lo[ty+1])
   // fork/join of the column kernels over auxiliary streams (same priority as the KKT's)
   cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
