@@ -631,6 +631,9 @@ def run_ours(args, rank, world, local_rank, dist):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference(raw, args, budget_s=args.cpu_budget)
+    dropin = None
+    if rank == 0 and world == 1 and not args.no_dropin:
+        dropin = dropin_ipm()
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -668,6 +671,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "e2e": e2e,
         "e2e_contract": e2e_contract,
         "cpu_baseline": cpu,
+        "dropin_ipm": dropin,
     }
     if args.traffic_json and Path(args.traffic_json).exists():
         tr = json.loads(Path(args.traffic_json).read_text())
@@ -749,6 +753,41 @@ def cpu_reference(raw, args, budget_s=15.0, periods=None, steps=None, warmup=0):
                       f"(single-threaded by design); median of {len(times)} units"}
 
 
+def dropin_ipm(periods=24):
+    """The UNMODIFIED reference interior-point solver end to end, twice on the same problem
+    (synthetic case118-size x `periods`): with the reference's own callbacks and
+    CondensedKkt (oracle/_ref, gnr_solve), and through the drop-in seams on the B200 path
+    (oracle/_ref/ipm_dropin cuda: CudaOpfNlp + the shadowing CondensedKkt).  The sparse
+    LDL^T stays on the host in both (out of scope), so this bounds the end-to-end gain of
+    the drop-in at this size; wall seconds of solve_nlp, problem construction excluded."""
+    import subprocess
+    import tempfile
+    from oracle import bindings as B
+    from paper_2405_14032_b200.network import config_case
+    from paper_2405_14032_b200.opf import load_profile
+    if not (B.ref_available() and B.DROPIN.exists()):
+        return None
+    raw = config_case("case118")
+    net = raw.network()
+    scale = load_profile(net.n_load, periods)
+    ref = B.RefModel(raw.to_matpower(), periods, scale).solve(1e-4)
+    with tempfile.TemporaryDirectory() as d:
+        path = Path(d) / "net.bin"
+        B.write_network_bin(path, net, periods, scale)
+        out = subprocess.run([str(B.DROPIN), str(path), "cuda", "1e-4", "2"], capture_output=True,
+                             text=True, timeout=600)
+    if out.returncode != 0:
+        return {"error": out.stderr.strip()[-300:]}
+    ours = json.loads(out.stdout.strip().splitlines()[-1])
+    return {"case": f"synthetic case118 x {periods} periods", "tol": 1e-4,
+            "reference": {"iterations": ref["iterations"], "objective": ref["objective"],
+                          "seconds": ref["seconds"]},
+            "b200_dropin": {"iterations": ours["iterations"], "objective": ours["objective"],
+                            "seconds": ours["warm_seconds"]},
+            "objective_rel_diff": abs(ours["objective"] - ref["objective"]) / abs(ref["objective"]),
+            "speedup": ref["seconds"] / ours["warm_seconds"]}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -785,6 +824,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
     ap.add_argument("--streams", type=int, choices=[1, 2], default=2)
+    ap.add_argument("--no-dropin", action="store_true",
+                    help="skip the whole-solve drop-in comparison (reference IPM, both paths)")
     ap.add_argument("--no-trial", action="store_true",
                     help="skip the line-search trial (gn_eval_fg) measurement")
     ap.add_argument("--no-ipm-ops", action="store_true",

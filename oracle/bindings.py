@@ -491,10 +491,10 @@ class RefModel(_ModelBase):
         return rhs, ds, dy
 
     def solve(self, tol=1e-4, max_iter=500):
-        out = np.zeros(4)
+        out = np.zeros(5)
         self.L.gnr_solve(self.h, tol, max_iter, _f(out))
         return dict(iterations=int(out[0]), objective=float(out[1]), status=int(out[2]),
-                    restorations=int(out[3]))
+                    restorations=int(out[3]), seconds=float(out[4]))
 
 
 def ref_load_profile(matpower_text: str, T: int, resolution=60.0, seed=1, amplitude=0.2,
@@ -512,3 +512,28 @@ def ref_load_profile(matpower_text: str, T: int, resolution=60.0, seed=1, amplit
         return out[: T * d[3]].reshape(T, d[3])
     finally:
         L.gnr_net_free(h)
+
+
+DROPIN = HERE / "_ref" / "ipm_dropin"
+
+
+def write_network_bin(path, net, T, scale):
+    """The binary network file of oracle/ipm_dropin.cpp (its load())."""
+    with open(path, "wb") as f:
+        np.array([net.n_bus, net.n_line, net.n_gen, net.n_load, net.reference_bus, T],
+                 np.int32).tofile(f)
+        np.array([net.base_mva], np.float64).tofile(f)
+        for k in ("bus_vmin", "bus_vmax", "vm_start", "va_start"):
+            getattr(net, k).tofile(f)
+        net.line_from.tofile(f)
+        net.line_to.tofile(f)
+        for k in ("line_g", "line_b", "line_smax", "line_amin", "line_amax"):
+            getattr(net, k).tofile(f)
+        net.gen_bus.tofile(f)
+        for k in ("gen_pmin", "gen_pmax", "gen_qmin", "gen_qmax", "gen_ramp", "gen_c2", "gen_c1",
+                  "gen_c0", "gen_pstart", "gen_qstart", "gen_qstart"):
+            getattr(net, k).tofile(f)
+        net.load_bus.tofile(f)
+        net.load_p.tofile(f)
+        net.load_q.tofile(f)
+        np.ascontiguousarray(scale, np.float64).tofile(f)

@@ -11,6 +11,8 @@
 //
 // Input: a binary network file written by tests/test_dropin.py (SoA arrays
 // in the order of gn_network, then the T x n_load demand table).
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <fstream>
@@ -100,7 +102,7 @@ power::MultiPeriodCase load(const char* path) {
 
 int main(int argc, char** argv) {
   if (argc < 3) {
-    std::fprintf(stderr, "usage: ipm_dropin <network.bin> cuda|ref [tol]\n");
+    std::fprintf(stderr, "usage: ipm_dropin <network.bin> cuda|ref [tol] [repeat]\n");
     return 2;
   }
   try {
@@ -109,18 +111,32 @@ int main(int argc, char** argv) {
     ipm::SolverConfig cfg;
     cfg.tol = argc > 3 ? std::atof(argv[3]) : 1e-4;
     ipm::SolveResult r;
+    // seconds = solve_nlp only (the problem object is built first, as gnr_solve does);
+    // with `repeat` > 1 the solve runs again on the same problem object and
+    // warm_seconds times the last one (one-time CUDA module loading etc. excluded)
+    const int repeat = argc > 4 ? std::max(1, std::atoi(argv[4])) : 1;
+    double secs = 0.0, warm = 0.0;
+    auto timed = [&](auto& nlp) {
+      for (int k = 0; k < repeat; ++k) {
+        const auto t0 = std::chrono::steady_clock::now();
+        r = ipm::solve_nlp(nlp, cfg);
+        const double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        if (k == 0) secs = s;
+        warm = s;
+      }
+    };
     if (which == "cuda") {
       gridnlp_b200::CudaOpfNlp nlp(mpc);
-      r = ipm::solve_nlp(nlp, cfg);
+      timed(nlp);
     } else {
       power::BuiltOpf built = power::build_multiperiod_opf(mpc);
       ipm::PatternNlp nlp(built.model);
-      r = ipm::solve_nlp(nlp, cfg);
+      timed(nlp);
     }
     std::printf("{\"nlp\": \"%s\", \"iterations\": %d, \"objective\": %.17g, \"status\": \"%s\", "
-                "\"restorations\": %d}\n",
+                "\"restorations\": %d, \"seconds\": %.6f, \"warm_seconds\": %.6f}\n",
                 which.c_str(), r.iterations, r.objective, ipm::to_string(r.status),
-                r.restorations);
+                r.restorations, secs, warm);
     return 0;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());

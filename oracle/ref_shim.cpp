@@ -16,6 +16,7 @@
 //   iterate.hpp vector ops    ipm/iterate.hpp:42-298 (residuals, condensation,
 //                             fraction to boundary, barrier, kkt_error), and
 //                             recover_bound_steps, condensed.hpp:187-212
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -344,13 +345,15 @@ int gnr_compress_to_csc(int32_t nrows, int32_t ncols, int64_t nnz, const int32_t
 
 // ---------------------------------------------------------------- end to end
 // solve_nlp on the reference model (solver.hpp:469).  out: [iterations,
-// objective, status, restorations]
+// objective, status, restorations, wall seconds of solve_nlp]
 void gnr_solve(void* h, double tol, int max_iter, double* out) {
   auto* m = static_cast<RefModel*>(h);
   ipm::SolverConfig cfg;
   cfg.tol = tol;
   cfg.max_iter = max_iter;
+  const auto t0 = std::chrono::steady_clock::now();
   ipm::SolveResult r = ipm::solve_nlp(*m->nlp, cfg);
+  out[4] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   out[0] = r.iterations;
   out[1] = r.objective;
   out[2] = static_cast<double>(static_cast<int>(r.status));

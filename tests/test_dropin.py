@@ -19,25 +19,7 @@ ROOT = Path(__file__).resolve().parents[1]
 DROPIN = ROOT / "oracle" / "_ref" / "ipm_dropin"
 
 
-def write_bin(path, net, T, scale):
-    with open(path, "wb") as f:
-        np.array([net.n_bus, net.n_line, net.n_gen, net.n_load, net.reference_bus, T],
-                 np.int32).tofile(f)
-        np.array([net.base_mva], np.float64).tofile(f)
-        for k in ("bus_vmin", "bus_vmax", "vm_start", "va_start"):
-            getattr(net, k).tofile(f)
-        net.line_from.tofile(f)
-        net.line_to.tofile(f)
-        for k in ("line_g", "line_b", "line_smax", "line_amin", "line_amax"):
-            getattr(net, k).tofile(f)
-        net.gen_bus.tofile(f)
-        for k in ("gen_pmin", "gen_pmax", "gen_qmin", "gen_qmax", "gen_ramp", "gen_c2", "gen_c1",
-                  "gen_c0", "gen_pstart", "gen_qstart", "gen_qstart"):
-            getattr(net, k).tofile(f)
-        net.load_bus.tofile(f)
-        net.load_p.tofile(f)
-        net.load_q.tofile(f)
-        np.ascontiguousarray(scale, np.float64).tofile(f)
+from oracle.bindings import write_network_bin as write_bin  # noqa: E402
 
 
 @pytest.mark.parametrize("key", ["case9_T1", "case30_T30_r30", "case118_T24"])
