@@ -7,6 +7,8 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cmath>
 #include <limits>
 
@@ -25,11 +27,13 @@ struct ProfRec {
   double ms = 0.0;
   int64_t launches = 0;
 };
-static bool g_prof = false;
+static std::atomic<bool> g_prof{false};
 static std::vector<ProfRec> g_recs;
+static std::mutex g_prof_mu;  // the registry is shared by every context / thread
 
 KTimer::KTimer(const char* name, cudaStream_t stream) {
   if (!g_prof) return;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   for (size_t i = 0; i < g_recs.size(); ++i)
     if (g_recs[i].name == name) idx = static_cast<int>(i);
   if (idx < 0) {
@@ -45,12 +49,14 @@ KTimer::~KTimer() {
   cudaEvent_t b;
   cudaEventCreate(&b);
   cudaEventRecord(b, s);
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   g_recs[idx].pending.push_back({a, b});
 }
 
 void profile_enable(bool on) { g_prof = on; }
 bool profiling() { return g_prof; }
 void profile_reset() {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   for (auto& r : g_recs)
     for (auto& e : r.pending) {
       cudaEventDestroy(e.first);
@@ -59,6 +65,7 @@ void profile_reset() {
   g_recs.clear();
 }
 int profile_count() {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   for (auto& r : g_recs) {
     for (auto& e : r.pending) {
       float ms = 0.f;
@@ -74,6 +81,7 @@ int profile_count() {
   return static_cast<int>(g_recs.size());
 }
 const char* profile_get(int i, double* ms, int64_t* launches) {
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   if (i < 0 || i >= static_cast<int>(g_recs.size())) return nullptr;
   *ms = g_recs[i].ms;
   *launches = g_recs[i].launches;

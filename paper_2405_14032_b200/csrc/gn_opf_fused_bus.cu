@@ -19,6 +19,8 @@
 // Hessian slots that are structurally zero are added as +0.0, a no-op on an
 // accumulator that starts at +0.0 (it never becomes -0.0).
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "gn_opf_kkt.cuh"
 
@@ -460,10 +462,10 @@ static void launch_busr(const OpfKktTab& t, const int4* buses, int32_t n_buses, 
   const int64_t nvb = (warps + kBW3 - 1) / kBW3;
   KTimer kt(names[DEG], s);
   if (rows)
-    k_fz_busr<DEG, true><<<grid_cap(nvb), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+    k_fz_busr<DEG, true><<<grid_cap(nvb, CAP_BUS), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
                                                              rows, bad);
   else
-    k_fz_busr<DEG, false><<<grid_cap(nvb), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+    k_fz_busr<DEG, false><<<grid_cap(nvb, CAP_BUS), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
                                                               rows, bad);
   count_launch();
 }
@@ -494,11 +496,20 @@ void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32
   const size_t smem = (size_t)nw * md * (kSV * 32 * sizeof(double) + 24);
   if (smem > kBusSmemMax) throw Error(GN_ERR_UNSUPPORTED, "bus degree too large for the fused kernel");
   const unsigned blocks = (unsigned)((warps + nw - 1) / nw);
-  static bool attr = false;
-  if (!attr) {
-    GN_CK(cudaFuncSetAttribute(k_fz_bus3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBusSmemMax));
-    GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kBusSmemMax));
-    attr = true;
+  {  // the dynamic shared-memory opt-in is per device (contexts on several GPUs)
+    static std::mutex mu;
+    static std::vector<char> done;
+    int dev = 0;
+    GN_CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lock(mu);
+    if (static_cast<size_t>(dev) >= done.size()) done.resize(static_cast<size_t>(dev) + 1, 0);
+    if (!done[dev]) {
+      GN_CK(cudaFuncSetAttribute(k_fz_bus3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kBusSmemMax));
+      GN_CK(cudaFuncSetAttribute(k_fz_bus3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kBusSmemMax));
+      done[dev] = 1;
+    }
   }
   KTimer kt(klass == kBusRegMax ? "k_fz_bus3<le8>" : "k_fz_bus3<rest>", s);
   if (rows)

@@ -6,13 +6,27 @@
 
 namespace gnb {
 
-// CTAs actually launched for `nvb` virtual CTAs: GRIDNLP_B200_GRID_CAP = resident CTAs per SM
-// to allow (0 or unset: one CTA per virtual CTA, the plain grid).
-inline unsigned grid_cap(int64_t nvb) {
-  static const int cap = [] {
-    const char* e = std::getenv("GRIDNLP_B200_GRID_CAP");
-    return e ? std::atoi(e) : 0;
-  }();
+// CTAs actually launched for `nvb` virtual CTAs: GRIDNLP_B200_GRID_CAP[_SETJAC|_LINE|_BUS] =
+// resident CTAs per SM to allow (0 or unset: one CTA per virtual CTA, the plain grid).
+enum CapKernel { CAP_SETJAC = 0, CAP_LINE = 1, CAP_BUS = 2 };
+inline int grid_cap_of(CapKernel which) {
+  struct Caps {  // read once (thread-safe function-local static)
+    int v[3];
+    Caps() {
+      const char* g = std::getenv("GRIDNLP_B200_GRID_CAP");
+      const char* names[3] = {"GRIDNLP_B200_GRID_CAP_SETJAC", "GRIDNLP_B200_GRID_CAP_LINE",
+                              "GRIDNLP_B200_GRID_CAP_BUS"};
+      for (int i = 0; i < 3; ++i) {
+        const char* e = std::getenv(names[i]);
+        v[i] = std::max(0, e ? std::atoi(e) : (g ? std::atoi(g) : 0));
+      }
+    }
+  };
+  static const Caps caps;
+  return caps.v[which];
+}
+inline unsigned grid_cap(int64_t nvb, CapKernel which) {
+  const int cap = grid_cap_of(which);
   if (cap <= 0) return (unsigned)nvb;
   return (unsigned)std::min<int64_t>(nvb, (int64_t)cap * 148);
 }
