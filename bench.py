@@ -306,7 +306,7 @@ def profile_kernels(L, step, steps, stream, flush):
     import torch
     L.gn_profile_reset()
     L.gn_profile_enable(1)
-    for _ in range(steps):
+    for _ in range(steps):  # (the caller runs this with the KKT grid uncapped)
         with torch.cuda.stream(stream):
             flush.zero_()
         step(serial=True)
@@ -322,11 +322,6 @@ def profile_kernels(L, step, steps, stream, flush):
 
 
 def run_ours(args, rank, world, local_rank, dist):
-    if args.streams == 2:
-        # the KKT kernels launch at most 2 CTAs per SM (grid-stride), leaving room for the
-        # callback stream's bandwidth-bound kernels to run beside them (measured best of
-        # 1, 2, 3, 4, 8 and uncapped; read once by the library, so set before any launch)
-        os.environ.setdefault("GRIDNLP_B200_GRID_CAP", "2")
     import torch
     from paper_2405_14032_b200 import abi
     from paper_2405_14032_b200.abi import GN_IN_FULL, GN_MEM_DEVICE_ASYNC, GN_MEM_HOST
@@ -343,6 +338,11 @@ def run_ours(args, rank, world, local_rank, dist):
     nlp.set_stream(stream.cuda_stream)
     nlp.lift(1e-4)
     kkt = CondensedKkt(nlp=nlp)
+    # with two streams the KKT kernels launch at most 2 CTAs per SM (grid-stride), leaving
+    # room for the callback stream's bandwidth-bound kernels beside them (swept: 1, 2, 3, 4,
+    # 8 and uncapped, per kernel and uniform; uniform 2 is best)
+    grid_cap = args.grid_cap if args.grid_cap >= 0 else (2 if args.streams == 2 else 0)
+    kkt.set_grid_cap(grid_cap)
     setup_s = time.time() - t0
     s = nlp.sizes
     xl, xu, xs, _, _ = nlp.bounds()
@@ -507,7 +507,9 @@ def run_ours(args, rank, world, local_rank, dist):
     # roofline of the dominant kernel: per-kernel CUDA events on the launch stream
     # (library KTimer), measured over extra steps after the timed region
     peak, peak_kind = peaks()
+    kkt.set_grid_cap(0)  # standalone per-kernel times: each kernel alone, full grid
     kprof = profile_kernels(L, step, max(3, min(args.steps, 10)), stream, flush)
+    kkt.set_grid_cap(grid_cap)
     kb = kernel_bytes(s, kkt, nlp, net, args.periods)
     dom = max(kprof, key=lambda k: kprof[k][0] * kprof[k][1])
     dom_ms = kprof[dom][0]
@@ -665,7 +667,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "line_search_trial": trial,
         "ipm_vector_ops": ipm_ops,
         "launch": (("cuda_graph (eager step %.4f ms)" % eager_ms) if graph_mode else "eager")
-        + "; KKT grid cap %s CTA/SM" % os.environ.get("GRIDNLP_B200_GRID_CAP", "0"),
+        + "; KKT grid cap %d CTA/SM" % grid_cap,
         "setup_s": setup_s,
         "clocks": clk,
         "e2e": e2e,
@@ -824,6 +826,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
     ap.add_argument("--streams", type=int, choices=[1, 2], default=2)
+    ap.add_argument("--grid-cap", type=int, default=-1,
+                    help="KKT CTAs per SM (default: 2 with two streams, else uncapped)")
     ap.add_argument("--no-dropin", action="store_true",
                     help="skip the whole-solve drop-in comparison (reference IPM, both paths)")
     ap.add_argument("--no-trial", action="store_true",

@@ -236,6 +236,10 @@ int gn_kkt_update_x(gn_kkt* kkt, const double* x, const double* row_weights, dou
 int gn_kkt_values(gn_kkt* kkt, double* a_vals, double* m_vals, int mem);
 /* Selects the assembly algorithm: 0 = auto, 1 = generic contributor lists,
  * 2 = OPF-specialised (lifted KKTs only). */
+/* Cap the fused/specialised KKT kernels at `ctas_per_sm` resident CTAs per SM (grid-stride;
+ * 0 = uncapped, the default unless GRIDNLP_B200_GRID_CAP is set).  A cap leaves SM room for
+ * kernels of other streams -- e.g. the callbacks evaluated concurrently with the KKT. */
+int gn_kkt_set_grid_cap(gn_kkt* kkt, int ctas_per_sm);
 int gn_kkt_set_algorithm(gn_kkt* kkt, int algo);
 
 /* compress_to_csc (sparse/matrix.hpp:45-81) of a host COO, on the device;

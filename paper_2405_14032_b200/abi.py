@@ -136,6 +136,7 @@ _SIGS = {
     "gn_kkt_update_x": (C.c_int, [vp, f64p, f64p, C.c_double, f64p, f64p, C.c_double,
                                     C.c_double, C.c_int]),
     "gn_kkt_set_algorithm": (C.c_int, [vp, C.c_int]),
+    "gn_kkt_set_grid_cap": (C.c_int, [vp, C.c_int]),
     "gn_compress_to_csc": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, i32p, i32p, i32p, i32p,
                                      i32p, i32p, C.POINTER(GnError)]),
 }

@@ -792,6 +792,12 @@ int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
   API_CATCH(nullptr)
 }
 
+int gn_kkt_set_grid_cap(gn_kkt* K, int ctas_per_sm) {
+  if (!K || ctas_per_sm < 0) return GN_ERR_INVALID;
+  gnb::opf_set_grid_cap(K, ctas_per_sm);
+  return GN_OK;
+}
+
 int gn_kkt_set_algorithm(gn_kkt* K, int algo) {
   if (!K || algo < 0 || algo > 2) return GN_ERR_INVALID;
   if (algo == 2 && !K->ctx) return GN_ERR_INVALID;

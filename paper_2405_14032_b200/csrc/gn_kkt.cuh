@@ -50,6 +50,7 @@ void kkt_assemble(gn_kkt* K, const double* H, const double* sx, const double* ss
                   double dc, bool full);
 bool opf_kkt_prepare(gn_kkt* K);
 void opf_kkt_free(gn_kkt* K);
+void opf_set_grid_cap(gn_kkt* K, int ctas_per_sm);
 bool opf_kkt_ready(const gn_kkt* K);
 bool opf_fused_ready(const gn_kkt* K);
 bool opf_fused_verify(gn_kkt* K);

@@ -550,7 +550,7 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
     KTimer kt("k_fz_line", s);
     const int64_t warps = (int64_t)t.L * t.tchunks;
     const int64_t nvb = (warps + kFLW - 1) / kFLW;
-    const unsigned g = grid_cap(nvb, CAP_LINE);
+    const unsigned g = grid_cap(nvb, t.grid_cap);
     if (g < nvb)  // capped grid: the grid-stride variant
       k_fz_line_gs<STRUCT><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
     else
@@ -593,7 +593,7 @@ static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream
     const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
                           (K->m - t.ramp0 + 31) / 32;
     const int64_t nvb = (warps + kSJW - 1) / kSJW;
-    const unsigned g = grid_cap(nvb, CAP_SETJAC);
+    const unsigned g = grid_cap(nvb, t.grid_cap);
     if (g < nvb)
       k_opf_set_jac_fused_gs<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
     else

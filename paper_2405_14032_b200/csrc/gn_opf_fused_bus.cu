@@ -462,10 +462,10 @@ static void launch_busr(const OpfKktTab& t, const int4* buses, int32_t n_buses, 
   const int64_t nvb = (warps + kBW3 - 1) / kBW3;
   KTimer kt(names[DEG], s);
   if (rows)
-    k_fz_busr<DEG, true><<<grid_cap(nvb, CAP_BUS), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+    k_fz_busr<DEG, true><<<grid_cap(nvb, t.grid_cap), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
                                                              rows, bad);
   else
-    k_fz_busr<DEG, false><<<grid_cap(nvb, CAP_BUS), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+    k_fz_busr<DEG, false><<<grid_cap(nvb, t.grid_cap), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
                                                               rows, bad);
   count_launch();
 }

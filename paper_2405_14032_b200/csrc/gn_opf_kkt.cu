@@ -710,6 +710,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
   }
   t.pg0 = d.pg0; t.qg0 = d.qg0; t.p0 = d.p0; t.q0 = d.q0; t.v0 = d.v0; t.th0 = d.th0;
   t.s_lo = d.s_lo; t.R = d.R; t.prev = d.prev; t.next = d.next;
+  t.grid_cap = grid_cap_default();
   t.lg = c->lg.p; t.lb = c->lb.p; t.c2 = c->c2.p; t.th_line = c->th_line.p;
   // flow-row / angle-row positions
   std::vector<int8_t> fpos(5 * static_cast<size_t>(L)), apos(2 * static_cast<size_t>(L));
@@ -926,6 +927,10 @@ bool opf_kkt_prepare(gn_kkt* K) {
 }
 
 bool opf_kkt_ready(const gn_kkt* K) { return K->opf && K->opf->ready; }
+
+void opf_set_grid_cap(gn_kkt* K, int ctas_per_sm) {
+  if (K->opf) K->opf->t.grid_cap = ctas_per_sm;
+}
 
 void opf_kkt_free(gn_kkt* K) {
   delete K->opf;

@@ -8,25 +8,17 @@ namespace gnb {
 
 // CTAs actually launched for `nvb` virtual CTAs: GRIDNLP_B200_GRID_CAP[_SETJAC|_LINE|_BUS] =
 // resident CTAs per SM to allow (0 or unset: one CTA per virtual CTA, the plain grid).
-enum CapKernel { CAP_SETJAC = 0, CAP_LINE = 1, CAP_BUS = 2 };
-inline int grid_cap_of(CapKernel which) {
-  struct Caps {  // read once (thread-safe function-local static)
-    int v[3];
-    Caps() {
-      const char* g = std::getenv("GRIDNLP_B200_GRID_CAP");
-      const char* names[3] = {"GRIDNLP_B200_GRID_CAP_SETJAC", "GRIDNLP_B200_GRID_CAP_LINE",
-                              "GRIDNLP_B200_GRID_CAP_BUS"};
-      for (int i = 0; i < 3; ++i) {
-        const char* e = std::getenv(names[i]);
-        v[i] = std::max(0, e ? std::atoi(e) : (g ? std::atoi(g) : 0));
-      }
-    }
-  };
-  static const Caps caps;
-  return caps.v[which];
+// Grid of `nvb` virtual CTAs capped at `cap` resident CTAs per SM (0: one CTA per virtual
+// CTA, the plain grid).  The cap of a KKT is set by gn_kkt_set_grid_cap; its default is
+// the GRIDNLP_B200_GRID_CAP environment variable.
+inline int grid_cap_default() {
+  static const int cap = [] {
+    const char* e = std::getenv("GRIDNLP_B200_GRID_CAP");
+    return std::max(0, e ? std::atoi(e) : 0);
+  }();
+  return cap;
 }
-inline unsigned grid_cap(int64_t nvb, CapKernel which) {
-  const int cap = grid_cap_of(which);
+inline unsigned grid_cap(int64_t nvb, int cap) {
   if (cap <= 0) return (unsigned)nvb;
   return (unsigned)std::min<int64_t>(nvb, (int64_t)cap * 148);
 }
@@ -64,6 +56,7 @@ struct OpfKktTab {
   int32_t maxdeg;                       // max incident lines of a bus
   int32_t s_lo, R, prev, next;          // ramp steps of a period shard (OpfDims)
   int32_t n_owned;                      // lifted columns owned (next ghosts follow)
+  int32_t grid_cap;                     // KKT kernels' resident CTAs per SM (0: uncapped)
   // fused line kernel descriptors
   const int4* ldesc0;                   // [L] (f, t, thermal slot or -1, flags: v/th free at
                                         //  min/max terminal bits 0-3, min==t bit 4, max==t bit 5)

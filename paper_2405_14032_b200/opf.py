@@ -321,6 +321,10 @@ class CondensedKkt:
     def set_stream(self, stream_handle: int):
         _check(self.lib.gn_kkt_set_stream(self.h, C.c_void_p(stream_handle)))
 
+    def set_grid_cap(self, ctas_per_sm: int):
+        """Resident CTAs per SM for the KKT kernels (0 = uncapped)."""
+        _check(self.lib.gn_kkt_set_grid_cap(self.h, int(ctas_per_sm)))
+
     def set_algorithm(self, algo: int):
         _check(self.lib.gn_kkt_set_algorithm(self.h, algo))
 
