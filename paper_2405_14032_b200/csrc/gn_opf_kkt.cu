@@ -483,6 +483,10 @@ static void launch_assemble(const OpfKktTab& t, const int32_t* type_lo, const In
     if (n <= 0) return;
     const int64_t warps = (int64_t)n * t.tchunks;
     const unsigned blocks = (unsigned)((warps * 32 + kMB - 1) / kMB);
+    static const char* names[C_TYPES] = {"k_opf_assemble<pg>", "k_opf_assemble<qg>",
+                                         "k_opf_assemble<p>", "k_opf_assemble<q>",
+                                         "k_opf_assemble<v>", "k_opf_assemble<th>"};
+    KTimer kt(names[TY], s);
     k_opf_assemble<STRUCT, TY><<<blocks, kMB, 0, s>>>(t, in, type_lo[TY], n, M, rows, bad);
     count_launch();
   };
@@ -952,7 +956,6 @@ void opf_assemble(gn_kkt* K, const double* Hfull, const double* sx, const double
   const int64_t blocks = assemble_blocks(t);
   if (blocks <= 0) return;
   In in{Hfull, K->avals.p, sx, ss, dw, dc};
-  KTimer kt("k_opf_assemble", K->stream);
   launch_assemble<false>(t, K->opf->type_lo, in, K->mvals.p, nullptr, nullptr, K->stream);
   GN_CK(cudaGetLastError());
 }
