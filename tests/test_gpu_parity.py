@@ -526,3 +526,47 @@ def test_destroy_order_any(gpu, order):
             sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, 7)
             objs[1].update_x(x, w, 1.0, sx, ss, *DELTAS[0])
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fused_kkt_randomised_networks(gpu, seed):
+    """Randomised sweep: network size, parallel lines, shared generators, fixed
+    generators / voltages, unrated lines and horizon length (partial 32-period chunks)
+    -- the fused A/M must equal the contract path bit for bit every time."""
+    from paper_2405_14032_b200.opf import load_profile
+    rng = np.random.default_rng(1000 + seed)
+    N = int(rng.integers(20, 200))
+    L = N + int(rng.integers(N // 3, N))
+    G = int(rng.integers(3, max(4, N // 4)))
+    D = int(rng.integers(N // 3, N))
+    raw = synthetic_case(N, L, G, D, seed=int(rng.integers(1, 10_000)),
+                         parallel_lines=int(rng.integers(0, 4)),
+                         shared_gens=int(rng.integers(0, 4)))
+    net = raw.network()
+    for g in rng.choice(net.n_gen, size=min(2, net.n_gen), replace=False):
+        net.gen_pmin[g] = net.gen_pmax[g]
+    for b in rng.choice(net.n_bus, size=2, replace=False):
+        if b != net.reference_bus:
+            net.bus_vmin[b] = net.bus_vmax[b]
+    net.line_smax[rng.random(net.n_line) < 0.2] = np.inf
+    net.gen_ramp[rng.random(net.n_gen) < 0.2] = np.inf
+    T = int(rng.integers(1, 70))
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale)
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, seed)
+    w = row_weights(nlp.sizes.n_cons, seed + 1, zero_every=int(rng.integers(2, 9)))
+    sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, seed + 2)
+    ow = float(rng.uniform(0, 2))
+    _fused_check(nlp, K, x, w, ow, sx, ss)
+    # and the callbacks / structures against the bit-exact C restatement
+    orc = B.OracleModel(net, T, scale)
+    for a, b in zip(orc.structure(), (*nlp.jac_structure(), *nlp.hess_structure())):
+        assert_bitexact(a, b, "structure")
+    for name, args in [("eval_g", (x,)), ("eval_jac", (x,)), ("eval_hess", (x, w, ow))]:
+        ok, v = getattr(nlp, name)(*args)
+        oko, vo, _ = getattr(orc, name)(*args)
+        assert ok and oko
+        assert_close(v, vo, what=name)
