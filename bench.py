@@ -37,6 +37,9 @@ METRIC = "callback+KKT-assembly nnz/s (J+H+M per IPM iteration)"
 UNIT = "nnz/s"
 PERIODS_PER_RANK = 96
 CONFIG = "synthetic30k"
+# BASELINE.json `configs` index of each workload (configs[0], case118 x 1, is the CPU parity case)
+CONFIG_INDEX = {"case118": 0, "case1354pegase": 1, "case9241pegase": 2, "case13659pegase": 3,
+                "synthetic30k": 4}
 
 
 def peaks():
@@ -201,15 +204,16 @@ def kernel_bytes(s, kkt, nlp, net, T):
     m_cls = [int(lens[vth & (cls[np.clip(ent, 0, N - 1)] == k)].sum()) for k in range(8)]
     bus_cls = {nm: m_cls[k] + 4 * int((cls == k).sum()) * T + 2.5 * int(deg[cls == k].sum()) * T
                for k, nm in enumerate(names)}
+    # balance rows (bus), flow / angle / thermal rows (line), ramp rows
+    cb_g = ((2 * N * T + 2 * L * T + 2 * G * T + 2 * D * T) + (5 * L * T + 2 * N * T + 3 * LTh * T)
+            + (GR * R + G * T))
     b = {
-        "k_gen<F>": G * T, "k_gen<GRAD>": 2 * G * T,
-        "k_bus<G>": 2 * N * T + 2 * L * T + 2 * G * T + 2 * D * T,
-        "k_line<G>": 5 * L * T + 2 * N * T + 3 * LTh * T,  # thermal rows folded in
-        "k_ramp<G>": GR * R + G * T,
-        "k_line<J>": 16 * L * T + 2 * N * T + 4 * LTh * T, "k_gen<J>": 2 * G * T,
-        "k_ramp<J>": 2 * GR * R,
-        "k_line<H>": 39 * L * T + 2 * N * T + 6 * LTh * T, "k_gen<H>": 4 * G * T,
-        "k_ramp<H>": 3 * GR * R,
+        # one launch per callback: its element classes' block ranges (gn_eval.cu)
+        "k_eval<F>": G * T, "k_eval<GRAD>": 2 * G * T,
+        "k_eval<G>": cb_g, "k_eval<FG>": cb_g + G * T,
+        # line (+ thermal) records, generator and ramp records
+        "k_eval<J>": 16 * L * T + 2 * N * T + 4 * LTh * T + 2 * G * T + 2 * GR * R,
+        "k_eval<H>": 39 * L * T + 2 * N * T + 6 * LTh * T + 4 * G * T + 3 * GR * R,
         "k_opf_set_jac_fused": annz - 2 * LTh * T + 2 * N * T,
         "k_opf_set_jac_fused<noflow>": annz - a_flow + 2 * LTh * T,
         "k_opf_set_jac_thermal": 4 * LTh * T,
@@ -654,7 +658,8 @@ def run_ours(args, rank, world, local_rank, dist):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.config} x {args.periods} periods per GPU "
-                               f"(BASELINE configs[4]; {s.n_vars} vars/GPU)",
+                               f"(BASELINE configs[{CONFIG_INDEX.get(args.config, '-')}]; "
+                               f"{s.n_vars} vars/GPU)",
                    "network": {"buses": net.n_bus, "lines": net.n_line, "gens": net.n_gen,
                                "loads": net.n_load},
                    "periods_per_gpu": args.periods, "periods_total": args.periods * world,
@@ -819,7 +824,7 @@ def run_reference(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{args.config} network x {args.cpu_periods} periods "
-                               "(bounded CPU sample of the 96-period workload)",
+                               f"(bounded CPU sample of the {args.periods}-period workload)",
                    "parallelism": "host threads"},
         "cpu_baseline": cpu,
         "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,

@@ -267,6 +267,7 @@ static int ctx_create(const gn_network* net, int32_t periods_total, int32_t firs
   c->status.alloc(1);
   GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof(unsigned long long), s));
   c->fpart.alloc(gnb::fpart_size(c->d));
+  GN_CK(cudaMemsetAsync(c->fpart.p, 0, sizeof(double) * gnb::fpart_size(c->d), s));
   GN_CK(cudaStreamSynchronize(s));
   *out = c;
   return ok(err);
@@ -467,8 +468,7 @@ int gn_eval_fg(gn_ctx* c, const double* x, double* f, double* g, int mem, gn_err
   }
   if (!is_async(mem))
     GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof(unsigned long long), s));
-  gnb::launch_eval(gnb::EV_F, d, c->net(), dx, nullptr, 0.0, df, c->fpart.p, c->status.p, s);
-  gnb::launch_eval(gnb::EV_G, d, c->net(), dx, nullptr, 0.0, dg, c->fpart.p, c->status.p, s);
+  gnb::launch_eval(gnb::EV_FG, d, c->net(), dx, nullptr, 0.0, dg, c->fpart.p, c->status.p, s, df);
   if (is_async(mem)) return ok(err);
   if (!is_device(mem)) {
     GN_CK(cudaMemcpyAsync(g, dg, sizeof(double) * d.m, cudaMemcpyDeviceToHost, s));

@@ -1,7 +1,9 @@
-// Per-element NLP callbacks: one kernel per element class (line x period,
-// generator x period, rated-line x period, ramping-generator x step,
+// Per-element NLP callbacks: one block body per element class (line x period
+// with its rated-line thermal rows, generator x period, ramping-generator x step,
 // bus x period), each writing its patterns' COO slots in the reference's
-// freeze order.  Closed-form derivatives of the 12 OPF patterns
+// freeze order.  Each callback is ONE launch (k_eval<MODE>) whose grid is the
+// concatenation of the classes' block ranges (heavy line blocks first, the short
+// generator / ramp blocks fill the tail), so a callback costs one kernel boundary.  Closed-form derivatives of the 12 OPF patterns
 // replace the reference's interpreted tape AD
 // (model/tape.hpp); value expressions keep the tape's operation order and
 // the library is built with -fmad=false, so g and J agree with the reference
@@ -71,13 +73,13 @@ __device__ __forceinline__ void const_out(double* __restrict__ out, int nb,
 // 12 (thermal) for rated lines: its rows / records of (line k, period t) are
 // written by the same thread, which already holds p and q.
 template <int MODE>
-__global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const double* __restrict__ x,
-                                              const double* __restrict__ w,
-                                              double* __restrict__ out,
-                                              unsigned long long* st) {
-  __shared__ __align__(16) double sm[kBS * 15 + 2];
+__device__ __forceinline__ void line_body(const OpfDims& d, const DevNet& net,
+                                          const double* __restrict__ x,
+                                          const double* __restrict__ w,
+                                          double* __restrict__ out, unsigned long long* st,
+                                          int64_t blk, double* sm) {
   const int64_t nrec = (int64_t)d.L * d.T;
-  const int64_t r0 = (int64_t)blockIdx.x * kBS;
+  const int64_t r0 = blk * kBS;
   const int64_t r = r0 + threadIdx.x;
   const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
   const bool valid = r < nrec;
@@ -192,14 +194,20 @@ __global__ void __launch_bounds__(kBS) k_line(OpfDims d, DevNet net, const doubl
 
 // ------------------------------------------------------------- generators
 // Pattern 0 (cost: f, grad, H) and 3, 4 (injections: J = 1, H = 0).
+// EV_F: each block reduces its records in a fixed tree into fpart[blk]; the last
+// block to finish (completion counter) sums the partials in a fixed order --
+// contiguous per-thread chunks, then a tree -- and resets the counter, so f is
+// independent of block scheduling.
 template <int MODE>
-__global__ void __launch_bounds__(kBS) k_gen(OpfDims d, DevNet net, const double* __restrict__ x,
-                                             double ow, double* __restrict__ out,
-                                             double* __restrict__ fpart,
-                                             unsigned long long* st) {
+__device__ __forceinline__ void gen_body(const OpfDims& d, const DevNet& net,
+                                         const double* __restrict__ x, double ow,
+                                         double* __restrict__ out, double* __restrict__ fpart,
+                                         unsigned int* cnt, unsigned long long* st, int64_t blk,
+                                         int64_t nblk_gen) {
   __shared__ double red[kBS];
+  __shared__ bool last;
   const int64_t nrec = (int64_t)d.G * d.T;
-  const int64_t r0 = (int64_t)blockIdx.x * kBS;
+  const int64_t r0 = blk * kBS;
   const int64_t r = r0 + threadIdx.x;
   const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
   const bool valid = r < nrec;
@@ -224,7 +232,29 @@ __global__ void __launch_bounds__(kBS) k_gen(OpfDims d, DevNet net, const double
       if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
       __syncthreads();
     }
-    if (threadIdx.x == 0) fpart[blockIdx.x] = red[0];
+    if (threadIdx.x == 0) {
+      fpart[blk] = red[0];
+      __threadfence();
+      last = atomicAdd(cnt, 1u) == (unsigned int)(nblk_gen - 1);
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      const int n = (int)nblk_gen, chunk = (n + kBS - 1) / kBS;
+      const int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
+      double a = 0.0;
+      for (int i = lo; i < hi; ++i) a += __ldcg(fpart + i);
+      red[threadIdx.x] = a;
+      __syncthreads();
+      for (int s = kBS / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+        __syncthreads();
+      }
+      if (threadIdx.x == 0) {
+        *out = red[0];
+        *cnt = 0u;
+      }
+    }
   } else if constexpr (MODE == EV_GRAD) {
     if (valid) {
       const double gr = grad_cost(c2, c1, pg);  // reverse sweep order
@@ -251,36 +281,19 @@ __global__ void __launch_bounds__(kBS) k_gen(OpfDims d, DevNet net, const double
   (void)nb;
 }
 
-// Fixed-order final sum of the objective partials (one block).
-__global__ void k_sum_partials(const double* __restrict__ part, int n, double* out) {
-  __shared__ double red[kBS];
-  double v = 0.0;
-  // each thread sums a contiguous chunk in order, then a fixed tree
-  const int chunk = (n + kBS - 1) / kBS;
-  const int lo = threadIdx.x * chunk, hi = min(n, lo + chunk);
-  for (int i = lo; i < hi; ++i) v += part[i];
-  red[threadIdx.x] = v;
-  __syncthreads();
-  for (int s = kBS / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *out = red[0];
-}
-
 // ----------------------------------------------------------------- thermal
 // Pattern 9: p^2 + q^2 over rated lines (opf.hpp:323-332).
 
 // -------------------------------------------------------------------- ramp
 // Pattern 11: pg(g,t) - pg(g,t-1), t = 1..T-1 (opf.hpp:343-351).
 template <int MODE>
-__global__ void __launch_bounds__(kBS) k_ramp(OpfDims d, DevNet net,
-                                              const double* __restrict__ x,
-                                              double* __restrict__ out,
-                                              unsigned long long* st) {
+__device__ __forceinline__ void ramp_body(const OpfDims& d, const DevNet& net,
+                                          const double* __restrict__ x,
+                                          double* __restrict__ out, unsigned long long* st,
+                                          int64_t blk) {
   const int32_t Tm = d.R;
   const int64_t nrec = (int64_t)d.GR * (Tm > 0 ? Tm : 0);
-  const int64_t r0 = (int64_t)blockIdx.x * kBS;
+  const int64_t r0 = blk * kBS;
   const int64_t r = r0 + threadIdx.x;
   const int nb = (int)(nrec - r0 < kBS ? nrec - r0 : kBS);
   if constexpr (MODE == EV_G) {
@@ -304,9 +317,10 @@ __global__ void __launch_bounds__(kBS) k_ramp(OpfDims d, DevNet net,
 // Balance rows (n,t): 0 (+) lines by ascending l (+) generators (+) loads —
 // exactly the order the reference's pattern-by-pattern `g[row] += contrib`
 // produces (pattern_model.hpp:307-324), so the sums are bit-identical.
-__global__ void __launch_bounds__(kBS) k_bus(OpfDims d, DevNet net, const double* __restrict__ x,
-                                             double* __restrict__ g, unsigned long long* st) {
-  const int64_t r = (int64_t)blockIdx.x * kBS + threadIdx.x;
+__device__ __forceinline__ void bus_body(const OpfDims& d, const DevNet& net,
+                                         const double* __restrict__ x, double* __restrict__ g,
+                                         unsigned long long* st, int64_t blk) {
+  const int64_t r = blk * kBS + threadIdx.x;
   if (r >= (int64_t)d.N * d.T) return;
   const int32_t n = (int32_t)(r / d.T), t = (int32_t)(r - (int64_t)n * d.T);
   double ap = 0.0, aq = 0.0;
@@ -344,63 +358,110 @@ __global__ void __launch_bounds__(kBS) k_bus(OpfDims d, DevNet net, const double
   g[d.bal_q0 + r] = aq;
 }
 
+// ------------------------------------------------------------------ kernel
+// Block ranges of one callback launch, in grid order.
+struct EvalSegs {
+  int64_t line, bus, ramp, gen;
+};
+
+// MODE = EV_F / EV_GRAD / EV_G / EV_J / EV_H, or EV_FG (the line-search trial:
+// the EV_G classes plus the objective, `out` = g, `fout` = f).  The class branch
+// is block-uniform, so the bodies' barriers are safe.
+template <int MODE>
+__global__ void __launch_bounds__(kBS) k_eval(OpfDims d, DevNet net, const double* __restrict__ x,
+                                              const double* __restrict__ w, double ow,
+                                              double* __restrict__ out, double* __restrict__ fout,
+                                              double* __restrict__ fpart, unsigned int* cnt,
+                                              unsigned long long* st, EvalSegs sg) {
+  constexpr int CM = MODE == EV_FG ? EV_G : MODE;  // mode of the constraint classes
+  constexpr bool cons = CM == EV_G || CM == EV_J || CM == EV_H;
+  int64_t b = blockIdx.x;
+  if constexpr (cons) {
+    if (b < sg.line) {
+      if constexpr (CM == EV_G) {
+        line_body<EV_G>(d, net, x, w, out, st, b, nullptr);
+      } else {
+        __shared__ __align__(16) double sm[kBS * 15 + 2];
+        line_body<CM>(d, net, x, w, out, st, b, sm);
+      }
+      return;
+    }
+    b -= sg.line;
+  }
+  if constexpr (CM == EV_G) {
+    if (b < sg.bus) {
+      bus_body(d, net, x, out, st, b);
+      return;
+    }
+    b -= sg.bus;
+  }
+  if constexpr (cons) {
+    if (b < sg.ramp) {
+      ramp_body<CM>(d, net, x, out, st, b);
+      return;
+    }
+    b -= sg.ramp;
+  }
+  if constexpr (MODE == EV_FG) gen_body<EV_F>(d, net, x, ow, fout, fpart, cnt, st, b, sg.gen);
+  else if constexpr (MODE != EV_G) gen_body<MODE>(d, net, x, ow, out, fpart, cnt, st, b, sg.gen);
+}
+
 // ------------------------------------------------------------------ driver
 static unsigned nblk(int64_t n) { return (unsigned)((n + kBS - 1) / kBS); }
 
+static const char* eval_name(int mode) {
+  switch (mode) {
+    case EV_F: return "k_eval<F>";
+    case EV_GRAD: return "k_eval<GRAD>";
+    case EV_G: return "k_eval<G>";
+    case EV_J: return "k_eval<J>";
+    case EV_H: return "k_eval<H>";
+    default: return "k_eval<FG>";
+  }
+}
+
+// the completion counter of the objective's last-block sum lives after the partials
+static unsigned int* fcount(const OpfDims& d, double* fpart) {
+  return reinterpret_cast<unsigned int*>(fpart + nblk((int64_t)d.G * d.T));
+}
+
 void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
                  const double* w, double ow, double* out, double* fpart,
-                 unsigned long long* st, cudaStream_t s) {
+                 unsigned long long* st, cudaStream_t s, double* fout) {
   const int64_t nl = (int64_t)d.L * d.T, ng = (int64_t)d.G * d.T,
                 nr = d.pid[K_RAMP] >= 0 ? (int64_t)d.GR * d.R : 0,
                 nb = (int64_t)d.N * d.T;
-  switch (mode) {
-    case EV_F: {
-      const unsigned blocks = nblk(ng);
-      if (blocks) {
-        { KTimer kt("k_gen<F>", s); k_gen<EV_F><<<blocks, kBS, 0, s>>>(d, net, x, ow, out, fpart, st); }
-        count_launch();
-        { KTimer kt("k_sum_partials", s); k_sum_partials<<<1, kBS, 0, s>>>(fpart, (int)blocks, out); }
-        count_launch();
-      } else {
-        GN_CK(cudaMemsetAsync(out, 0, sizeof(double), s));
-      }
-      break;
+  EvalSegs sg{0, 0, 0, 0};
+  const bool wants_f = mode == EV_F || mode == EV_FG;
+  if (mode == EV_FG || mode == EV_G || mode == EV_J || mode == EV_H) {
+    sg.line = nblk(nl);
+    sg.ramp = nblk(nr);
+  }
+  if (mode == EV_FG || mode == EV_G) sg.bus = nblk(nb);
+  if (mode != EV_G) sg.gen = nblk(ng);
+  if (mode == EV_GRAD && d.n > d.qg0)  // zero the non-generator blocks; the kernel writes pg
+    GN_CK(cudaMemsetAsync(out + d.qg0, 0, sizeof(double) * (d.n - d.qg0), s));
+  double* fo = mode == EV_FG ? fout : out;
+  if (wants_f && !sg.gen) GN_CK(cudaMemsetAsync(fo, 0, sizeof(double), s));  // no generators
+  const int64_t blocks = sg.line + sg.bus + sg.ramp + sg.gen;
+  if (blocks) {
+    KTimer kt(eval_name(mode), s);
+    unsigned int* cnt = fcount(d, fpart);
+    const dim3 grid((unsigned)blocks);
+    switch (mode) {
+      case EV_F: k_eval<EV_F><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
+      case EV_GRAD: k_eval<EV_GRAD><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
+      case EV_G: k_eval<EV_G><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
+      case EV_J: k_eval<EV_J><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
+      case EV_H: k_eval<EV_H><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
+      default: k_eval<EV_FG><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
     }
-    case EV_GRAD:
-      // zero the non-generator blocks, then the cost gradient over pg
-      if (d.n > d.qg0) GN_CK(cudaMemsetAsync(out + d.qg0, 0, sizeof(double) * (d.n - d.qg0), s));
-      if (ng) { KTimer kt("k_gen<GRAD>", s); k_gen<EV_GRAD><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st); count_launch(); }
-      break;
-    case EV_G:
-      if (nb) { KTimer kt("k_bus<G>", s); k_bus<<<nblk(nb), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
-      if (nl) { KTimer kt("k_line<G>", s); k_line<EV_G><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st); count_launch(); }
-      if (nr) { KTimer kt("k_ramp<G>", s); k_ramp<EV_G><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st); count_launch(); }
-      break;
-    case EV_J:
-    case EV_H:
-      if (nl) {
-        KTimer kt(mode == EV_J ? "k_line<J>" : "k_line<H>", s);
-        if (mode == EV_J) k_line<EV_J><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st);
-        else k_line<EV_H><<<nblk(nl), kBS, 0, s>>>(d, net, x, w, out, st);
-        count_launch();
-      }
-      if (ng) {
-        KTimer kt(mode == EV_J ? "k_gen<J>" : "k_gen<H>", s);
-        if (mode == EV_J) k_gen<EV_J><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
-        else k_gen<EV_H><<<nblk(ng), kBS, 0, s>>>(d, net, x, ow, out, fpart, st);
-        count_launch();
-      }
-      if (nr) {
-        KTimer kt(mode == EV_J ? "k_ramp<J>" : "k_ramp<H>", s);
-        if (mode == EV_J) k_ramp<EV_J><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st);
-        else k_ramp<EV_H><<<nblk(nr), kBS, 0, s>>>(d, net, x, out, st);
-        count_launch();
-      }
-      break;
+    count_launch();
   }
   GN_CK(cudaGetLastError());
 }
 
-size_t fpart_size(const OpfDims& d) { return nblk((int64_t)d.G * d.T) + 1; }
+// objective partials + one completion counter (zeroed at context creation)
+size_t fpart_size(const OpfDims& d) { return nblk((int64_t)d.G * d.T) + 2; }
 
 }  // namespace gnb

@@ -3,12 +3,14 @@
 
 namespace gnb {
 
-enum EvalMode { EV_F = 0, EV_GRAD = 1, EV_G = 2, EV_J = 3, EV_H = 4 };
+// EV_FG: the line-search trial, g into `out` and f into `fout`, one launch
+enum EvalMode { EV_F = 0, EV_GRAD = 1, EV_G = 2, EV_J = 3, EV_H = 4, EV_FG = 5 };
 
-// Enqueue one callback on stream s; failures are latched into *st.
+// Enqueue one callback (one kernel, plus a memset for EV_GRAD) on stream s;
+// failures are latched into *st.  fpart: fpart_size(d) doubles, zeroed once.
 void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
                  const double* w, double ow, double* out, double* fpart,
-                 unsigned long long* st, cudaStream_t s);
+                 unsigned long long* st, cudaStream_t s, double* fout = nullptr);
 size_t fpart_size(const OpfDims& d);
 
 void build_structure(gn_ctx* c, int32_t* jr, int32_t* jc, int32_t* hr, int32_t* hc);

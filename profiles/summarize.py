@@ -34,13 +34,13 @@ def short(name: str) -> str:
     return name.split("(")[0].replace("void ", "").strip()
 
 
-MODES = {"0": "F", "1": "GRAD", "2": "G", "3": "J", "4": "H"}
+MODES = {"0": "F", "1": "GRAD", "2": "G", "3": "J", "4": "H", "5": "FG"}
 
 
 def pretty(name: str) -> str:
-    """gnb::k_line<4> -> k_line<H>; value-mode fused kernels <0> -> plain name."""
+    """gnb::k_eval<4> -> k_eval<H>; value-mode fused kernels <0> -> plain name."""
     n = name.replace("gnb::", "")
-    for k in ("k_line", "k_gen", "k_thermal", "k_ramp"):
+    for k in ("k_eval", "k_line", "k_gen", "k_thermal", "k_ramp"):
         if n.startswith(k + "<") and n[len(k) + 1:-1] in MODES:
             return f"{k}<{MODES[n[len(k) + 1:-1]]}>"
     import re
@@ -71,7 +71,8 @@ def launches(path: str, out: str):
         agg.setdefault(short(r["Kernel Name"]), []).append(us)
     counts = Counter(len(v) for k, v in agg.items() if k.startswith("gnb::"))
     # steps in the capture = launches of a once-per-step kernel (the Hessian callback)
-    S = len(agg["gnb::k_line<4>"]) if "gnb::k_line<4>" in agg else max(counts, key=lambda c: (counts[c], c))
+    hk = next((k for k in ("gnb::k_eval<4>", "gnb::k_line<4>") if k in agg), None)
+    S = len(agg[hk]) if hk else max(counts, key=lambda c: (counts[c], c))
     step = {k: v for k, v in agg.items() if len(v) % S == 0 and k.startswith("gnb::")}
     setup = {k: v for k, v in agg.items() if k not in step}
     tot = sum(sum(v) for v in step.values()) / S
