@@ -518,10 +518,28 @@ static bool ensure_aux(gn_kkt* K) {
   return true;
 }
 
-// The column kernels write disjoint parts of M.  In value mode they are forked over
-// the KKT stream and two auxiliary streams (fork/join by events: capturable in a CUDA
-// graph), so the short, low-occupancy degree-class launches overlap the flow-column
-// kernel instead of each paying its own tail.  Per-kernel profiling runs them serially.
+// The column kernels write disjoint parts of M.  In value mode the bus classes are forked
+// over auxiliary streams (fork/join by events: capturable in a CUDA graph) beside the
+// flow-column kernel on the KKT stream, so the short, low-occupancy degree-class launches
+// overlap it instead of each paying its own tail.  Per-kernel profiling runs them serially.
+// Bus-class lanes: one for large problems (the classes are long and fill the SMs; more
+// concurrent KKT kernels only crowd out the flow-column kernel and the callback stream),
+// four when the whole bus sweep is a few thousand warps (the step is then the chain of
+// short latency-bound launches, which parallel lanes shorten).  Measured, step ms for
+// 1 / 2 / 4 / 8 lanes: 1354 x 24: 0.059 / 0.058 / 0.044 / 0.050; 9241 x 48: 0.255 /
+// 0.270 / 0.274 / 0.274; 30k x 96: 1.179 / 1.190 / 1.217 / 1.246.
+// GRIDNLP_B200_BUS_LANES overrides (1 .. kBusClasses).
+static int bus_lanes(const OpfKkt* X) {
+  static const int env = [] {
+    const char* e = std::getenv("GRIDNLP_B200_BUS_LANES");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env > 0) return env < kBusClasses ? env : kBusClasses;
+  int64_t warps = 0;
+  for (int k = 0; k < kBusClasses; ++k) warps += (int64_t)X->n_bus_cls[k] * X->t.tchunks;
+  return warps <= 4096 ? 4 : 1;
+}
+
 template <bool STRUCT>
 static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, int32_t* rows,
                          int32_t* bad) {
@@ -529,21 +547,18 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   const OpfKktTab& t = X->t;
   cudaStream_t s = K->stream;
   const bool fork = !STRUCT && ensure_aux(K);
-  cudaStream_t lane[3] = {s, s, s};
+  const int nlanes = fork ? bus_lanes(X) : 1;
   if (fork) {
     GN_CK(cudaEventRecord(X->ev_fork, s));
-    for (int a = 0; a < 2; ++a) {
-      GN_CK(cudaStreamWaitEvent(X->aux[a], X->ev_fork, 0));
-      lane[a + 1] = X->aux[a];
-    }
+    for (int a = 0; a < nlanes; ++a) GN_CK(cudaStreamWaitEvent(X->aux[a], X->ev_fork, 0));
   }
-  // degree classes 1..6, le8, rest: alternate the two auxiliary lanes, largest first
+  // degree classes 1..6, le8, rest: round-robin over the lanes, largest first
   static const int order[kBusClasses] = {2, 3, 1, 4, 5, 6, 7, 0};
   for (int i = 0; i < kBusClasses; ++i) {
     const int k = order[i];
     launch_fz_bus(t, X->bus_cls[k].p, X->n_bus_cls[k],
                   k < kBusRegMax ? k + 1 : (k == kBusRegMax ? 8 : X->maxdeg_rest), k, in, dv, M,
-                  rows, bad, lane[1 + (i & 1)]);
+                  rows, bad, fork ? X->aux[i % nlanes] : s);
   }
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
@@ -563,7 +578,7 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
     count_launch();
   }
   if (fork) {
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < nlanes; ++a) {
       GN_CK(cudaEventRecord(X->ev_join[a], X->aux[a]));
       GN_CK(cudaStreamWaitEvent(s, X->ev_join[a], 0));
     }
@@ -615,11 +630,12 @@ void opf_update_fused(gn_kkt* K, const double* x, const double* w, double ow, co
   OpfKkt* X = K->opf;
   if (ensure_aux(K)) {
     GN_CK(cudaEventRecord(X->ev_fork2, K->stream));
-    GN_CK(cudaStreamWaitEvent(X->aux[2], X->ev_fork2, 0));
-    set_jac_launch(K, x, 0, X->aux[2]);
-    GN_CK(cudaEventRecord(X->ev_join[2], X->aux[2]));
+    cudaStream_t sj = X->aux[OpfKkt::kAuxSetJac];
+    GN_CK(cudaStreamWaitEvent(sj, X->ev_fork2, 0));
+    set_jac_launch(K, x, 0, sj);
+    GN_CK(cudaEventRecord(X->ev_join[OpfKkt::kAuxSetJac], sj));
     opf_assemble_fused(K, x, w, ow, sx, ss, dw, dc);
-    GN_CK(cudaStreamWaitEvent(K->stream, X->ev_join[2], 0));
+    GN_CK(cudaStreamWaitEvent(K->stream, X->ev_join[OpfKkt::kAuxSetJac], 0));
   } else {
     set_jac_launch(K, x, 0, K->stream);
     opf_assemble_fused(K, x, w, ow, sx, ss, dw, dc);

@@ -103,8 +103,10 @@ struct OpfKkt {
   bool ready = false;
   int32_t type_lo[C_TYPES + 1] = {};  // items of column type ty: [type_lo[ty], type_lo[ty+1])
   // fork/join of the column kernels over auxiliary streams (same priority as the KKT's)
-  cudaStream_t aux[3] = {nullptr, nullptr, nullptr};
-  cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join[3] = {nullptr, nullptr, nullptr};
+  // aux[0 .. kBusClasses-1]: bus-class lanes; aux[kAuxSetJac]: set_jacobian beside assemble
+  static constexpr int kAuxSetJac = kBusClasses, kAux = kBusClasses + 1;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t ev_fork = nullptr, ev_fork2 = nullptr, ev_join[kAux] = {};
   int aux_prio = 0;
   ~OpfKkt() {
     for (auto& a : aux) if (a) cudaStreamDestroy(a);
