@@ -628,7 +628,11 @@ void opf_update_fused(gn_kkt* K, const double* x, const double* w, double ow, co
   // A (set_jacobian) and M (assemble) are independent given x: A is built on a third
   // auxiliary stream beside the M kernels, so the two latency-bound phases overlap
   OpfKkt* X = K->opf;
-  if (ensure_aux(K)) {
+  static const bool fork_sj = [] {
+    const char* e = std::getenv("GRIDNLP_B200_SETJAC_FORK");
+    return !e || std::atoi(e) != 0;
+  }();
+  if (fork_sj && ensure_aux(K)) {
     GN_CK(cudaEventRecord(X->ev_fork2, K->stream));
     cudaStream_t sj = X->aux[OpfKkt::kAuxSetJac];
     GN_CK(cudaStreamWaitEvent(sj, X->ev_fork2, 0));
