@@ -55,7 +55,9 @@ __device__ __forceinline__ void stage_out(double* sm, const double (&v)[K], bool
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     if (rest & 1) out[total - 1] = sm[shift + total - 1];
-    if (body > 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    // wait until the engine has READ the staging buffer (reusable, or the CTA may exit);
+    // the global writes complete asynchronously, visible at the kernel boundary
+    if (body > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   }
   __syncthreads();
 }
