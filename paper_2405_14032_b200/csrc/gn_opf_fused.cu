@@ -172,6 +172,17 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
 // the warp writes the span back coalesced.  Direct per-lane writes would make
 // every 8-byte store its own L2 sector write (4x the write transactions, and
 // partial-sector fills from HBM).
+// resident-CTA floors of the launch bounds (register caps); overridable for tuning builds
+// (scripts/build_variant.py)
+#ifndef GN_FL_GS_MINB
+#define GN_FL_GS_MINB 3
+#endif
+#ifndef GN_SJ_MINB
+#define GN_SJ_MINB 6
+#endif
+#ifndef GN_SJ_GS_MINB
+#define GN_SJ_GS_MINB 6
+#endif
 constexpr int kFLW = 8;     // warps per CTA
 constexpr int kFLCap = 16;  // staged slots per column (longer columns are written in place)
 template <bool STRUCT>
@@ -310,7 +321,7 @@ __global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, int64_t nvb,
   fz_line_body<STRUCT>(blockIdx.x, t, x, w, sx, dw, dv, M, rows, bad);
 }
 template <bool STRUCT>
-__global__ void __launch_bounds__(kFLW * 32, 3) k_fz_line_gs(OpfKktTab t, int64_t nvb,
+__global__ void __launch_bounds__(kFLW * 32, GN_FL_GS_MINB) k_fz_line_gs(OpfKktTab t, int64_t nvb,
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ w,
                                                          const double* __restrict__ sx, double dw,
@@ -480,14 +491,14 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
   }
 }
 
-__global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused(OpfKktTab t, int64_t nvb,
+__global__ void __launch_bounds__(kSJW * 32, GN_SJ_MINB) k_opf_set_jac_fused(OpfKktTab t, int64_t nvb,
                                                                 int32_t m,
                                                                 const double* __restrict__ x,
                                                                 double* __restrict__ A,
                                                                 int skip_flow) {
   set_jac_body(blockIdx.x, t, m, x, A, skip_flow);
 }
-__global__ void __launch_bounds__(kSJW * 32, 6) k_opf_set_jac_fused_gs(OpfKktTab t, int64_t nvb,
+__global__ void __launch_bounds__(kSJW * 32, GN_SJ_GS_MINB) k_opf_set_jac_fused_gs(OpfKktTab t, int64_t nvb,
                                                                    int32_t m,
                                                                    const double* __restrict__ x,
                                                                    double* __restrict__ A,

@@ -32,7 +32,10 @@ namespace gnb {
 
 constexpr int kBW3 = 4;  // warps per CTA
 // resident CTAs per SM the register allocation of k_fz_busr<DEG> must allow
-constexpr int kBusrMinBlocks[7] = {1, 8, 5, 4, 3, 2, 2};
+#ifndef GN_BUSR_MINB
+#define GN_BUSR_MINB 1, 8, 5, 4, 3, 2, 2
+#endif
+constexpr int kBusrMinBlocks[7] = {GN_BUSR_MINB};
 constexpr int kSV = 11;
 constexpr int kBusSmemMax = 200 * 1024;  // dynamic shared memory cap of the bus kernel  // shared doubles per (line, lane): Cs Sn cs sn vf vt w7 w8 d7 d8 d10
 
