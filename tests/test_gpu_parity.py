@@ -570,3 +570,40 @@ def test_fused_kkt_randomised_networks(gpu, seed):
         oko, vo, _ = getattr(orc, name)(*args)
         assert ok and oko
         assert_close(v, vo, what=name)
+
+
+@pytest.mark.parametrize("T", [40, 96])
+def test_bitwise_reproducible_across_launch_shapes(gpu, T):
+    """Outputs are bitwise independent of the launch configuration and of repetition
+    (pattern_model.hpp:270-273): KKT grid caps (grid-stride virtual CTAs), the bus-class
+    lanes chosen for the size, and repeated calls (the objective's last-block sum)."""
+    from paper_2405_14032_b200.opf import load_profile
+    raw = synthetic_case(400, 620, 90, 330, seed=17, parallel_lines=3, shared_gens=3)
+    net = raw.network()
+    nlp = OpfNlp(net, T, load_profile(net.n_load, T))
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, T + 5)
+    w = row_weights(nlp.sizes.n_cons, T + 6, zero_every=7)
+    sx, ss = sigmas(nlp.sizes.n_free, nlp.sizes.n_cons, T + 7)
+    ref = None
+    for cap in (0, 1, 2, 3, 0):
+        K.set_grid_cap(cap)
+        K.update_x(x, w, 1.0, sx, ss, *DELTAS[1])
+        a, m = K.values()
+        if ref is None:
+            ref = (a.copy(), m.copy())
+        assert_bitexact(a, ref[0], f"A cap={cap}")
+        assert_bitexact(m, ref[1], f"M cap={cap}")
+    outs = []
+    for _ in range(3):
+        ok, f = nlp.eval_f(x)
+        ok2, fg_f, fg_g = nlp.eval_fg(x)
+        ok3, h = nlp.eval_hess(x, w, 1.0)
+        assert ok and ok2 and ok3 and f == fg_f
+        outs.append((f, fg_g, h))
+    for f, g, h in outs[1:]:
+        assert f == outs[0][0]
+        assert np.array_equal(g, outs[0][1]) and np.array_equal(h, outs[0][2])
+    K.close()
