@@ -370,6 +370,7 @@ def run_ours(args, rank, world, local_rank, dist):
     dsx = torch.from_numpy(sx).to(dev)
     dss = torch.from_numpy(ss).to(dev)
     f = torch.zeros(1, **f64)
+    f_global = torch.zeros(1, **f64)
     grad = torch.empty(s.n_vars, **f64)
     g = torch.empty(s.n_cons, **f64)
     J = torch.empty(s.jac_nnz, **f64)
@@ -444,6 +445,10 @@ def run_ours(args, rank, world, local_rank, dist):
                                 sync=False)
             if name in cb_mark:
                 mark(cb_mark[name])
+        if world > 1:  # the global objective: shard partials added in rank order (one all-gather)
+            from paper_2405_14032_b200.shard import global_objective
+            with torch.cuda.stream(stream):
+                f_global.copy_(global_objective(f, world))
         if fused and ks is not stream:
             ev_k.record(ks)
             stream.wait_event(ev_k)

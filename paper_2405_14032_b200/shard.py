@@ -192,6 +192,23 @@ def exchange_halo(plan: dict, x, sigma_s, rank: int):
         sigma_s.index_copy_(0, plan["rows_ghost"], recv["sn"])
 
 
+def global_objective(f_local, world: int):
+    """The global problem's objective from the shards' partial objectives:
+    all-gather the per-rank partials (one double each) and add them in rank order, so
+    every rank holds the same, run-to-run identical value.  (The reference sums the
+    records of all periods in one sequence; the rank-order sum of the period-shard
+    partials agrees with it to rounding.)  `f_local` is a 1-element tensor on the rank's
+    device; returns a 1-element tensor."""
+    import torch
+    import torch.distributed as tdist
+    parts = [torch.empty_like(f_local) for _ in range(world)]
+    tdist.all_gather(parts, f_local)
+    total = parts[0].clone()
+    for p in parts[1:]:
+        total += p
+    return total
+
+
 def halo_exchange(maps: list[ShardMap], xs: list[np.ndarray], sigma_s: list[np.ndarray]):
     """In-process halo fill (all ranks' arrays at hand): what the distributed
     exchange in bench.py / tests/test_shard_gloo.py does with send/recv."""

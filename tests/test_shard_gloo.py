@@ -84,6 +84,19 @@ def _worker(rank, world, port, T_total, out):
         rows = mp_.loc.ramp0 + np.arange(mp_.GR * mp_.loc.R)
         owned = own[rows]
         assert np.array_equal(ramp_local[owned], g[rg[rows]][owned])
+        # ---- global objective: rank-order sum of the shard partials, equal on every rank
+        from paper_2405_14032_b200.shard import global_objective
+        ok, f_all, _ = orc.eval_f(x)
+        assert ok
+        orc_loc = B.OracleModel(net, T, scale[t0:t0 + T])
+        xo = np.ascontiguousarray(x[vg][:orc_loc.sizes[0]])  # owned block precedes the ghosts
+        ok, f_loc, _ = orc_loc.eval_f(xo)
+        assert ok
+        ft = global_objective(torch.tensor([f_loc], dtype=torch.float64), world)
+        f_ranks = [torch.empty(1, dtype=torch.float64) for _ in range(world)]
+        dist.all_gather(f_ranks, ft)
+        assert all(float(v) == float(ft) for v in f_ranks)
+        assert abs(float(ft) - f_all) <= 1e-12 * abs(f_all)
         # every global row is owned by exactly one rank
         owned_global = torch.zeros(orc.sizes[1], dtype=torch.int32)
         owned_global[torch.from_numpy(rg[own])] = 1
