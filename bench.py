@@ -290,6 +290,24 @@ def ipm_vector_ops(nlp, kkt, J, grad, g, dsx, dss, flush, stream, peak, reps=5):
             b_.record(stream)
     torch.cuda.synchronize()
     ms = float(np.median([a_.elapsed_time(b_) for a_, b_ in evs]))
+    # per-kernel event times (library KTimer), L2 flushed before each iteration
+    from paper_2405_14032_b200 import abi
+    L = abi.lib()
+    L.gn_profile_reset()
+    L.gn_profile_enable(1)
+    for _ in range(3):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+            iteration()
+    torch.cuda.synchronize()
+    L.gn_profile_enable(0)
+    kern = {}
+    for i in range(L.gn_profile_count()):
+        kms, kn = C.c_double(), C.c_int64()
+        name = L.gn_profile_get(i, C.byref(kms), C.byref(kn)).decode()
+        if name.startswith("k_ipm"):
+            kern[name] = round(kms.value / 3, 5)  # ms per iteration
+    L.gn_profile_reset()
     annz = kkt.a_nnz
     vec = {  # algorithmic reads + writes per op, in doubles (index maps excluded)
         "residuals": nj + (4 * n + 5 * m) + (n + m) + 2 * (n + m) + (3 * n + 4 * m),
@@ -307,7 +325,8 @@ def ipm_vector_ops(nlp, kkt, J, grad, g, dsx, dss, flush, stream, peak, reps=5):
     ipm.close()
     return {"ms": ms, "alg_bytes": alg, "gbs": alg / (ms * 1e-3) / 1e9,
             "frac": alg / (ms * 1e-3) / 1e9 / peak, "n": n, "m": m,
-            "ops": list(vec.keys())}
+            "ops": list(vec.keys()),
+            "kernels_ms": dict(sorted(kern.items(), key=lambda kv: -kv[1]))}
 
 
 def abi_dev_async():

@@ -409,13 +409,19 @@ gn_ipm* ipm_create(gn_kkt* K, const double* xl, const double* xu, const double* 
 }
 
 void ipm_jac_t(gn_ipm* P, const double* jv, const double* y, double* out, cudaStream_t s) {
-  k_list_product<<<nblk(P->n), kIB, 0, s>>>(P->n, P->jt.ptr.p, P->jt.seg.p, P->jt.src.p, jv,
-                                            P->K->ctx->jr_l.p, y, out);
+  {
+    KTimer kt("k_ipm_jac_t", s);
+    k_list_product<<<nblk(P->n), kIB, 0, s>>>(P->n, P->jt.ptr.p, P->jt.seg.p, P->jt.src.p, jv,
+                                              P->K->ctx->jr_l.p, y, out);
+  }
   count_launch();
 }
 void ipm_jac(gn_ipm* P, const double* jv, const double* x, double* out, cudaStream_t s) {
-  k_list_product<<<nblk(P->m), kIB, 0, s>>>(P->m, P->jr.ptr.p, P->jr.seg.p, P->jr.src.p, jv,
-                                            P->K->ctx->jc_l.p, x, out);
+  {
+    KTimer kt("k_ipm_jac", s);
+    k_list_product<<<nblk(P->m), kIB, 0, s>>>(P->m, P->jr.ptr.p, P->jr.seg.p, P->jr.src.p, jv,
+                                              P->K->ctx->jc_l.p, x, out);
+  }
   count_launch();
 }
 
@@ -438,21 +444,33 @@ void ipm_residuals(gn_ipm* P, const gn_iterate& it, const double* grad, const do
 
 void ipm_condense(gn_ipm* P, const gn_iterate& it, const gn_residuals& r, double* sx, double* ss,
                   double* qx, double* qs, cudaStream_t s) {
-  k_condense<<<nblk(P->n), kIB, 0, s>>>(P->n, it.x, it.zlx, it.zux, r.px, r.pzlx, r.pzux, P->xl.p,
-                                        P->xu.p, sx, qx);
+  {
+    KTimer kt("k_ipm_condense_x", s);
+    k_condense<<<nblk(P->n), kIB, 0, s>>>(P->n, it.x, it.zlx, it.zux, r.px, r.pzlx, r.pzux, P->xl.p,
+                                          P->xu.p, sx, qx);
+  }
   count_launch();
-  k_condense<<<nblk(P->m), kIB, 0, s>>>(P->m, it.s, it.zls, it.zus, r.ps, r.pzls, r.pzus, P->sl.p,
-                                        P->su.p, ss, qs);
+  {
+    KTimer kt("k_ipm_condense_s", s);
+    k_condense<<<nblk(P->m), kIB, 0, s>>>(P->m, it.s, it.zls, it.zus, r.ps, r.pzls, r.pzus, P->sl.p,
+                                          P->su.p, ss, qs);
+  }
   count_launch();
 }
 
 void ipm_recover(gn_ipm* P, const gn_iterate& it, const gn_residuals& r, const gn_direction& d,
                  cudaStream_t s) {
-  k_recover<<<nblk(P->n), kIB, 0, s>>>(P->n, it.x, d.dx, it.zlx, it.zux, r.pzlx, r.pzux, P->xl.p,
-                                       P->xu.p, d.dzlx, d.dzux);
+  {
+    KTimer kt("k_ipm_recover_x", s);
+    k_recover<<<nblk(P->n), kIB, 0, s>>>(P->n, it.x, d.dx, it.zlx, it.zux, r.pzlx, r.pzux, P->xl.p,
+                                         P->xu.p, d.dzlx, d.dzux);
+  }
   count_launch();
-  k_recover<<<nblk(P->m), kIB, 0, s>>>(P->m, it.s, d.ds, it.zls, it.zus, r.pzls, r.pzus, P->sl.p,
-                                       P->su.p, d.dzls, d.dzus);
+  {
+    KTimer kt("k_ipm_recover_s", s);
+    k_recover<<<nblk(P->m), kIB, 0, s>>>(P->m, it.s, d.ds, it.zls, it.zus, r.pzls, r.pzus, P->sl.p,
+                                         P->su.p, d.dzls, d.dzus);
+  }
   count_launch();
 }
 
@@ -460,9 +478,15 @@ void ipm_kkt_error(gn_ipm* P, const gn_iterate& it, const gn_residuals& r, doubl
                    cudaStream_t s) {
   KktIn a{P->n, P->m, it.x, it.s, it.y, it.zlx, it.zux, it.zls, it.zus, r.px, r.ps, r.py,
           P->xl.p, P->xu.p, P->sl.p, P->su.p, mu};
-  k_kkt_err<<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  {
+    KTimer kt("k_ipm_kkt_err", s);
+    k_kkt_err<<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  }
   count_launch();
-  k_kkt_err_final<<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, P->m, out);
+  {
+    KTimer kt("k_ipm_kkt_err_final", s);
+    k_kkt_err_final<<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, P->m, out);
+  }
   count_launch();
 }
 
@@ -478,9 +502,15 @@ void ipm_barrier(gn_ipm* P, double f, const double* x, const double* sv, double 
                  cudaStream_t s) {
   ScalIn a = scal(P);
   a.x = x; a.s = sv; a.mu = mu;
-  k_scalar<S_BARRIER><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  {
+    KTimer kt("k_ipm_barrier", s);
+    k_scalar<S_BARRIER><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  }
   count_launch();
-  k_scalar_final<S_BARRIER><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, f, mu, out);
+  {
+    KTimer kt("k_ipm_final", s);
+    k_scalar_final<S_BARRIER><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, f, mu, out);
+  }
   count_launch();
 }
 
@@ -488,9 +518,15 @@ void ipm_slope(gn_ipm* P, const double* grad, const gn_iterate& it, const gn_dir
                double mu, double* out, cudaStream_t s) {
   ScalIn a = scal(P);
   a.x = it.x; a.s = it.s; a.grad = grad; a.dx = d.dx; a.ds = d.ds; a.mu = mu;
-  k_scalar<S_SLOPE><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  {
+    KTimer kt("k_ipm_slope", s);
+    k_scalar<S_SLOPE><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  }
   count_launch();
-  k_scalar_final<S_SLOPE><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, 0.0, mu, out);
+  {
+    KTimer kt("k_ipm_final", s);
+    k_scalar_final<S_SLOPE><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, 0.0, mu, out);
+  }
   count_launch();
 }
 
@@ -498,9 +534,15 @@ void ipm_violation(gn_ipm* P, const double* g, const double* sv, double* out, cu
   ScalIn a = scal(P);
   a.g = g; a.s = sv; a.x = sv;  // x is not read for the m-range
   a.n = 0;                      // m entries only
-  k_scalar<S_VIOL><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  {
+    KTimer kt("k_ipm_violation", s);
+    k_scalar<S_VIOL><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  }
   count_launch();
-  k_scalar_final<S_VIOL><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, 0.0, 0.0, out);
+  {
+    KTimer kt("k_ipm_final", s);
+    k_scalar_final<S_VIOL><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, 0.0, 0.0, out);
+  }
   count_launch();
 }
 
@@ -511,9 +553,15 @@ void ipm_ftb(gn_ipm* P, const gn_iterate& it, const gn_direction& d, double tau,
   a.zlx = it.zlx; a.zux = it.zux; a.zls = it.zls; a.zus = it.zus;
   a.dzlx = d.dzlx; a.dzux = d.dzux; a.dzls = d.dzls; a.dzus = d.dzus;
   a.tau = tau;
-  k_scalar<S_FTB><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  {
+    KTimer kt("k_ipm_ftb", s);
+    k_scalar<S_FTB><<<kRedBlocks, kIB, 0, s>>>(a, P->part.p);
+  }
   count_launch();
-  k_scalar_final<S_FTB><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, 0.0, 0.0, out);
+  {
+    KTimer kt("k_ipm_final", s);
+    k_scalar_final<S_FTB><<<1, kIB, 0, s>>>(P->part.p, kRedBlocks, 0.0, 0.0, out);
+  }
   count_launch();
 }
 
@@ -521,10 +569,16 @@ void kkt_solve_rhs(gn_ipm* P, const double* qx, const double* qs, const double* 
                    const double* ss, double dw, double dc, double* rhs, double* tm,
                    cudaStream_t s) {
   gn_kkt* K = P->K;
-  k_solve_tm<<<nblk(P->m), kIB, 0, s>>>(P->m, qs, qy, ss, dw, dc, tm);
+  {
+    KTimer kt("k_ipm_solve_tm", s);
+    k_solve_tm<<<nblk(P->m), kIB, 0, s>>>(P->m, qs, qy, ss, dw, dc, tm);
+  }
   count_launch();
-  k_solve_rhs<<<nblk(P->n), kIB, 0, s>>>(P->n, P->at.ptr.p, P->at.seg.p, P->at.src.p, K->avals.p,
-                                         K->arow.p, tm, qx, rhs);
+  {
+    KTimer kt("k_ipm_solve_rhs", s);
+    k_solve_rhs<<<nblk(P->n), kIB, 0, s>>>(P->n, P->at.ptr.p, P->at.seg.p, P->at.src.p, K->avals.p,
+                                           K->arow.p, tm, qx, rhs);
+  }
   count_launch();
 }
 
@@ -532,8 +586,11 @@ void kkt_solve_finish(gn_ipm* P, const double* dx, const double* qs, const doubl
                       const double* ss, double dw, double dc, double* ds, double* dy,
                       cudaStream_t s) {
   gn_kkt* K = P->K;
-  k_solve_finish<<<nblk(P->m), kIB, 0, s>>>(P->m, K->A.ptr.p, K->A.idx.p, K->avals.p, dx, qs, qy,
-                                            ss, dw, dc, ds, dy);
+  {
+    KTimer kt("k_ipm_solve_finish", s);
+    k_solve_finish<<<nblk(P->m), kIB, 0, s>>>(P->m, K->A.ptr.p, K->A.idx.p, K->avals.p, dx, qs, qy,
+                                              ss, dw, dc, ds, dy);
+  }
   count_launch();
 }
 
