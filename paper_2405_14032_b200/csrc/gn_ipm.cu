@@ -47,28 +47,36 @@ __global__ void k_col_keys(int64_t n, const int32_t* __restrict__ c, uint64_t* k
   if (i < n) key[i] = (uint64_t)(uint32_t)c[i];
 }
 
-__global__ void k_list_product(int32_t n, const int32_t* __restrict__ ptr,
-                               const int32_t* __restrict__ seg, const int32_t* __restrict__ src,
-                               const double* __restrict__ vals, const int32_t* __restrict__ other,
-                               const double* __restrict__ v, double* __restrict__ out) {
+__global__ void k_list_product(int32_t n, const int2* __restrict__ be,
+                               const int32_t* __restrict__ src, const int32_t* __restrict__ oth,
+                               const double* __restrict__ vals, const double* __restrict__ v,
+                               double* __restrict__ out) {
   const int32_t c = blockIdx.x * kIB + threadIdx.x;
   if (c >= n) return;
+  const int2 b = be[c];
   double acc = 0.0;
-  if (ptr[c + 1] > ptr[c]) {
-    const int32_t sl = ptr[c];
-    for (int32_t q = seg[sl]; q < seg[sl + 1]; ++q) {
-      const int32_t k = src[q];
-      acc += vals[k] * v[other[k]];
-    }
-  }
+  for (int32_t q = b.x; q < b.y; ++q) acc += vals[src[q]] * v[oth[q]];
   out[c] = acc;
+}
+
+// list bounds and contributor "other" indices (see gn_ipm::jt_be)
+__global__ void k_list_be(int32_t n, const int32_t* __restrict__ ptr,
+                          const int32_t* __restrict__ seg, int2* __restrict__ be) {
+  const int32_t c = blockIdx.x * kIB + threadIdx.x;
+  if (c >= n) return;
+  be[c] = ptr[c + 1] > ptr[c] ? make_int2(seg[ptr[c]], seg[ptr[c] + 1]) : make_int2(0, 0);
+}
+__global__ void k_list_oth(int64_t nnz, const int32_t* __restrict__ src,
+                           const int32_t* __restrict__ other, int32_t* __restrict__ oth) {
+  const int64_t q = (int64_t)blockIdx.x * kIB + threadIdx.x;
+  if (q < nnz) oth[q] = other[src[q]];
 }
 
 // ------------------------------------------------------------ residuals
 // px = grad - J^T y - zlx + zux (J^T y in COO order), pzl/pzu with the bounds.
-__global__ void k_res_x(int32_t n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ seg,
+__global__ void k_res_x(int32_t n, const int2* __restrict__ be,
                         const int32_t* __restrict__ src, const double* __restrict__ jv,
-                        const int32_t* __restrict__ jrow, const double* __restrict__ y,
+                        const int32_t* __restrict__ oth, const double* __restrict__ y,
                         const double* __restrict__ grad, const double* __restrict__ x,
                         const double* __restrict__ zl, const double* __restrict__ zu,
                         const double* __restrict__ xl, const double* __restrict__ xu, double mu,
@@ -76,14 +84,9 @@ __global__ void k_res_x(int32_t n, const int32_t* __restrict__ ptr, const int32_
                         double* __restrict__ pzu) {
   const int32_t i = blockIdx.x * kIB + threadIdx.x;
   if (i >= n) return;
+  const int2 b = be[i];
   double jty = 0.0;
-  if (ptr[i + 1] > ptr[i]) {
-    const int32_t sl = ptr[i];
-    for (int32_t q = seg[sl]; q < seg[sl + 1]; ++q) {
-      const int32_t k = src[q];
-      jty += jv[k] * y[jrow[k]];
-    }
-  }
+  for (int32_t q = b.x; q < b.y; ++q) jty += jv[src[q]] * y[oth[q]];
   px[i] = grad[i] - jty - zl[i] + zu[i];
   const double lo = xl[i], hi = xu[i], xi = x[i];
   pzl[i] = has_lo(lo) ? zl[i] * (xi - lo) - mu : 0.0;
@@ -326,20 +329,15 @@ __global__ void k_solve_tm(int32_t m, const double* __restrict__ qs, const doubl
   tm[i] = c * qs[i] + d * qy[i];
 }
 // rhs = -(qx + A^T tm): A^T tm per column in CSR row order (condensed.hpp:155-157)
-__global__ void k_solve_rhs(int32_t n, const int32_t* __restrict__ ptr, const int32_t* __restrict__ seg,
+__global__ void k_solve_rhs(int32_t n, const int2* __restrict__ be,
                             const int32_t* __restrict__ src, const double* __restrict__ av,
-                            const int32_t* __restrict__ arow, const double* __restrict__ tm,
+                            const int32_t* __restrict__ oth, const double* __restrict__ tm,
                             const double* __restrict__ qx, double* __restrict__ rhs) {
   const int32_t c = blockIdx.x * kIB + threadIdx.x;
   if (c >= n) return;
+  const int2 b = be[c];
   double acc = 0.0;
-  if (ptr[c + 1] > ptr[c]) {
-    const int32_t sl = ptr[c];
-    for (int32_t q = seg[sl]; q < seg[sl + 1]; ++q) {
-      const int32_t p = src[q];
-      acc += av[p] * tm[arow[p]];
-    }
-  }
+  for (int32_t q = b.x; q < b.y; ++q) acc += av[src[q]] * tm[oth[q]];
   rhs[c] = -(qx[c] + acc);
 }
 // tm = A dx (per row, csr_matvec); ds = c*(tm + qy - dc*qs); dy = -qs - sd*ds (condensed.hpp:164-170)
@@ -402,6 +400,22 @@ gn_ipm* ipm_create(gn_kkt* K, const double* xl, const double* xu, const double* 
   build_lists(c->jc_l.p, K->nj, P->n, P->jt, s);
   build_lists(c->jr_l.p, K->nj, P->m, P->jr, s);
   build_lists(K->A.idx.p, K->annz, P->n, P->at, s);  // CSR positions are row-major: stable by column
+  auto flatten = [&](const Csc& L, int32_t nl, const int32_t* other, int64_t nnz, DBuf<int2>& be,
+                     DBuf<int32_t>& oth) {
+    be.alloc(static_cast<size_t>(nl) + 1);
+    oth.alloc(static_cast<size_t>(nnz) + 1);
+    if (nl > 0) {
+      k_list_be<<<nblk(nl), kIB, 0, s>>>(nl, L.ptr.p, L.seg.p, be.p);
+      count_launch();
+    }
+    if (nnz > 0) {
+      k_list_oth<<<(unsigned)((nnz + kIB - 1) / kIB), kIB, 0, s>>>(nnz, L.src.p, other, oth.p);
+      count_launch();
+    }
+  };
+  flatten(P->jt, P->n, c->jr_l.p, K->nj, P->jt_be, P->jt_oth);
+  flatten(P->jr, P->m, c->jc_l.p, K->nj, P->jr_be, P->jr_oth);
+  flatten(P->at, P->n, K->arow.p, K->annz, P->at_be, P->at_oth);
   P->part.alloc(static_cast<size_t>(kRedBlocks) * 8);
   P->scratch.alloc(static_cast<size_t>(P->m) + 1);
   GN_CK(cudaStreamSynchronize(s));
@@ -411,16 +425,16 @@ gn_ipm* ipm_create(gn_kkt* K, const double* xl, const double* xu, const double* 
 void ipm_jac_t(gn_ipm* P, const double* jv, const double* y, double* out, cudaStream_t s) {
   {
     KTimer kt("k_ipm_jac_t", s);
-    k_list_product<<<nblk(P->n), kIB, 0, s>>>(P->n, P->jt.ptr.p, P->jt.seg.p, P->jt.src.p, jv,
-                                              P->K->ctx->jr_l.p, y, out);
+    k_list_product<<<nblk(P->n), kIB, 0, s>>>(P->n, P->jt_be.p, P->jt.src.p, P->jt_oth.p, jv, y,
+                                              out);
   }
   count_launch();
 }
 void ipm_jac(gn_ipm* P, const double* jv, const double* x, double* out, cudaStream_t s) {
   {
     KTimer kt("k_ipm_jac", s);
-    k_list_product<<<nblk(P->m), kIB, 0, s>>>(P->m, P->jr.ptr.p, P->jr.seg.p, P->jr.src.p, jv,
-                                              P->K->ctx->jc_l.p, x, out);
+    k_list_product<<<nblk(P->m), kIB, 0, s>>>(P->m, P->jr_be.p, P->jr.src.p, P->jr_oth.p, jv, x,
+                                              out);
   }
   count_launch();
 }
@@ -429,9 +443,9 @@ void ipm_residuals(gn_ipm* P, const gn_iterate& it, const double* grad, const do
                    const double* jv, double mu, const gn_residuals& r, cudaStream_t s) {
   {
     KTimer kt("k_ipm_res_x", s);
-    k_res_x<<<nblk(P->n), kIB, 0, s>>>(P->n, P->jt.ptr.p, P->jt.seg.p, P->jt.src.p, jv,
-                                       P->K->ctx->jr_l.p, it.y, grad, it.x, it.zlx, it.zux,
-                                       P->xl.p, P->xu.p, mu, r.px, r.pzlx, r.pzux);
+    k_res_x<<<nblk(P->n), kIB, 0, s>>>(P->n, P->jt_be.p, P->jt.src.p, jv, P->jt_oth.p, it.y,
+                                       grad, it.x, it.zlx, it.zux, P->xl.p, P->xu.p, mu, r.px,
+                                       r.pzlx, r.pzux);
   }
   count_launch();
   {
@@ -576,8 +590,8 @@ void kkt_solve_rhs(gn_ipm* P, const double* qx, const double* qs, const double* 
   count_launch();
   {
     KTimer kt("k_ipm_solve_rhs", s);
-    k_solve_rhs<<<nblk(P->n), kIB, 0, s>>>(P->n, P->at.ptr.p, P->at.seg.p, P->at.src.p, K->avals.p,
-                                           K->arow.p, tm, qx, rhs);
+    k_solve_rhs<<<nblk(P->n), kIB, 0, s>>>(P->n, P->at_be.p, P->at.src.p, K->avals.p, P->at_oth.p,
+                                           tm, qx, rhs);
   }
   count_launch();
 }

@@ -11,6 +11,11 @@ struct gn_ipm {
   gnb::Csc jt;  // per column of J: COO indices ascending (J^T y)
   gnb::Csc jr;  // per row of J: COO indices ascending (J x)
   gnb::Csc at;  // per column of A: CSR positions, rows ascending (A^T v)
+  // flattened lists for the product kernels: [begin, end) of each list in src order and
+  // the other index (row for columns, column for rows) of each contributor, so a thread's
+  // loads are two levels deep (list bounds, then src/other, then the values)
+  gnb::DBuf<int2> jt_be, jr_be, at_be;
+  gnb::DBuf<int32_t> jt_oth, jr_oth, at_oth;
   gnb::DBuf<double> part;  // reduction partials
   gnb::DBuf<double> scratch;
 };
