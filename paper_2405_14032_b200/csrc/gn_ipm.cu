@@ -35,6 +35,12 @@ void compress_keys(uint64_t* keys, int64_t nnz, int32_t nrows, int32_t ncols, Cs
 namespace {
 
 constexpr int kIB = 256;          // threads per block
+// unroll of the grid-stride reduction loops (more loads in flight; the per-thread
+// accumulation order is unchanged); tuning builds override it
+#ifndef GN_RED_UNROLL
+#define GN_RED_UNROLL 4
+#endif
+constexpr int kRedUnroll = GN_RED_UNROLL;
 constexpr int kRedBlocks = 1184;  // 8 x 148 SMs: fixed grid of the reduction passes
 
 unsigned nblk(int64_t n) { return (unsigned)((n + kIB - 1) / kIB); }
@@ -186,6 +192,7 @@ struct KktIn {
 __global__ void __launch_bounds__(kIB) k_kkt_err(KktIn a, double* __restrict__ part) {
   double sums[3] = {0.0, 0.0, 0.0}, maxs[4] = {0.0, 0.0, 0.0, 0.0};
   const int64_t total = (int64_t)a.n + a.m;
+#pragma unroll kRedUnroll
   for (int64_t i = (int64_t)blockIdx.x * kIB + threadIdx.x; i < total; i += (int64_t)gridDim.x * kIB) {
     if (i < a.n) {
       const int32_t j = (int32_t)i;
@@ -259,6 +266,7 @@ template <int KIND>
 __global__ void __launch_bounds__(kIB) k_scalar(ScalIn a, double* __restrict__ part) {
   double v[2] = {KIND == S_FTB ? 1.0 : 0.0, KIND == S_FTB ? 1.0 : 0.0};
   const int64_t total = (int64_t)a.n + a.m;
+#pragma unroll kRedUnroll
   for (int64_t i = (int64_t)blockIdx.x * kIB + threadIdx.x; i < total; i += (int64_t)gridDim.x * kIB) {
     const bool isx = i < a.n;
     const int32_t j = isx ? (int32_t)i : (int32_t)(i - a.n);
