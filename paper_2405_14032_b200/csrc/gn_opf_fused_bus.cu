@@ -30,12 +30,32 @@
 
 namespace gnb {
 
-constexpr int kBW3 = 4;  // warps per CTA
-// resident CTAs per SM the register allocation of k_fz_busr<DEG> must allow
-#ifndef GN_BUSR_MINB
-#define GN_BUSR_MINB 1, 8, 5, 4, 3, 2, 2
+#ifndef GN_BW3
+#define GN_BW3 4
 #endif
-constexpr int kBusrMinBlocks[7] = {GN_BUSR_MINB};
+constexpr int kBW3 = GN_BW3;  // warps per CTA
+// resident CTAs per SM the register allocation of k_fz_busr<DEG> must allow
+// (per degree: overridable one by one in tuning builds, GN_BUSR_MINB_D<k>)
+#ifndef GN_BUSR_MINB_D1
+#define GN_BUSR_MINB_D1 8
+#endif
+#ifndef GN_BUSR_MINB_D2
+#define GN_BUSR_MINB_D2 5
+#endif
+#ifndef GN_BUSR_MINB_D3
+#define GN_BUSR_MINB_D3 3
+#endif
+#ifndef GN_BUSR_MINB_D4
+#define GN_BUSR_MINB_D4 3
+#endif
+#ifndef GN_BUSR_MINB_D5
+#define GN_BUSR_MINB_D5 2
+#endif
+#ifndef GN_BUSR_MINB_D6
+#define GN_BUSR_MINB_D6 2
+#endif
+constexpr int kBusrMinBlocks[7] = {1, GN_BUSR_MINB_D1, GN_BUSR_MINB_D2, GN_BUSR_MINB_D3,
+                                   GN_BUSR_MINB_D4, GN_BUSR_MINB_D5, GN_BUSR_MINB_D6};
 constexpr int kSV = 11;
 constexpr int kBusSmemMax = 200 * 1024;  // dynamic shared memory cap of the bus kernel  // shared doubles per (line, lane): Cs Sn cs sn vf vt w7 w8 d7 d8 d10
 
