@@ -398,7 +398,7 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 //     +-1 per incident line, held by lane j = slot j and broadcast by shuffle);
 //   * flow_p and flow_q rows of (line, 32 periods): the line state is computed
 //     once for both rows, staged ([slot][lane]) and written back;
-//   * thermal rows of a thermal line (all periods): (2p, 2q);
+//   * thermal rows of (thermal line, 32 periods): (2p, 2q), lane = period;
 //   * angle rows of a line (all periods): (+1, -1) at the free angle slots;
 //   * ramp rows: one thread per row.
 constexpr int kSJW = 8;  // warps per CTA
@@ -456,16 +456,17 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
     return;
   }
   wg -= nflow;
-  if (wg < LT) {  // thermal rows of thermal slot k, all periods: [p, q] -> (2p, 2q)
-    const int32_t k = (int32_t)wg, l = __ldg(t.th_line + k);
-    const int64_t base = __ldg(t.rbase + 2 * t.N + 2 * t.L + k);
-    for (int32_t e = lane; e < 2 * T; e += 32) {
-      const int32_t tt = e >> 1;
-      A[base + e] = 0.0 + j_thermal(x[((e & 1) ? t.q0 : t.p0) + l * T + tt]);
-    }
+  if (wg < (int64_t)LT * tch) {  // thermal rows of (thermal slot k, 32 periods): [p, q] -> (2p, 2q)
+    const int32_t k = (int32_t)(wg / tch), tt = (int32_t)(wg - (int64_t)k * tch) * 32 + lane;
+    if (tt >= T) return;
+    const int32_t l = __ldg(t.th_line + k);
+    const int64_t at = __ldg(t.rbase + 2 * t.N + 2 * t.L + k) + 2 * (int64_t)tt;
+    const double p = x[t.p0 + l * T + tt], q = x[t.q0 + l * T + tt];
+    A[at] = 0.0 + j_thermal(p);
+    A[at + 1] = 0.0 + j_thermal(q);
     return;
   }
-  wg -= LT;
+  wg -= (int64_t)LT * tch;
   if (wg < t.L) {  // angle rows of line l, all periods: [th_f, th_t] -> (1, -1)
     const int32_t l = (int32_t)wg;
     const int pf = __ldg(t.apos + 2 * l), pt = __ldg(t.apos + 2 * l + 1);
@@ -616,8 +617,8 @@ static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream
   {
     KTimer kt(skip_flow ? "k_opf_set_jac_fused<noflow>" : "k_opf_set_jac_fused", st);
     const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
-    const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
-                          (K->m - t.ramp0 + 31) / 32;
+    const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) +
+                          LT * t.tchunks + t.L + (K->m - t.ramp0 + 31) / 32;
     const int64_t nvb = (warps + kSJW - 1) / kSJW;
     const unsigned g = grid_cap(nvb, t.grid_cap);
     if (g < nvb)
