@@ -456,17 +456,32 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
     return;
   }
   wg -= nflow;
-  if (wg < (int64_t)LT * tch) {  // thermal rows of (thermal slot k, 32 periods): [p, q] -> (2p, 2q)
-    const int32_t k = (int32_t)(wg / tch), tt = (int32_t)(wg - (int64_t)k * tch) * 32 + lane;
-    if (tt >= T) return;
-    const int32_t l = __ldg(t.th_line + k);
-    const int64_t at = __ldg(t.rbase + 2 * t.N + 2 * t.L + k) + 2 * (int64_t)tt;
-    const double p = x[t.p0 + l * T + tt], q = x[t.q0 + l * T + tt];
-    A[at] = 0.0 + j_thermal(p);
-    A[at + 1] = 0.0 + j_thermal(q);
+  if (wg < LT) {  // thermal rows of thermal slot k, all periods: [p, q] -> (2p, 2q)
+    const int32_t k = (int32_t)wg, l = __ldg(t.th_line + k);
+    const int64_t base = __ldg(t.rbase + 2 * t.N + 2 * t.L + k);
+    const double* xp = x + t.p0 + l * T;
+    const double* xq = x + t.q0 + l * T;
+    constexpr int kU = 4;  // periods per lane per round: all loads of a round, then its stores
+    for (int32_t c0 = 0; c0 < T; c0 += 32 * kU) {
+      double pv[kU], qv[kU];
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const int32_t tt = c0 + 32 * j + lane;
+        pv[j] = tt < T ? xp[tt] : 0.0;
+        qv[j] = tt < T ? xq[tt] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < kU; ++j) {
+        const int32_t tt = c0 + 32 * j + lane;
+        if (tt < T) {
+          A[base + 2 * tt] = 0.0 + j_thermal(pv[j]);
+          A[base + 2 * tt + 1] = 0.0 + j_thermal(qv[j]);
+        }
+      }
+    }
     return;
   }
-  wg -= (int64_t)LT * tch;
+  wg -= LT;
   if (wg < t.L) {  // angle rows of line l, all periods: [th_f, th_t] -> (1, -1)
     const int32_t l = (int32_t)wg;
     const int pf = __ldg(t.apos + 2 * l), pt = __ldg(t.apos + 2 * l + 1);
@@ -617,8 +632,8 @@ static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream
   {
     KTimer kt(skip_flow ? "k_opf_set_jac_fused<noflow>" : "k_opf_set_jac_fused", st);
     const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
-    const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) +
-                          LT * t.tchunks + t.L + (K->m - t.ramp0 + 31) / 32;
+    const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
+                          (K->m - t.ramp0 + 31) / 32;
     const int64_t nvb = (warps + kSJW - 1) / kSJW;
     const unsigned g = grid_cap(nvb, t.grid_cap);
     if (g < nvb)
