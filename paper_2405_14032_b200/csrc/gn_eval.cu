@@ -19,6 +19,9 @@
 
 namespace gnb {
 
+#ifndef GN_G_BUS_FIRST
+#define GN_G_BUS_FIRST 1
+#endif
 constexpr int kBS = 128;  // records per block (one per thread; 128 measured marginally ahead of 256)
 
 __device__ __forceinline__ void report(unsigned long long* st, int pid, int64_t rec) {
@@ -396,6 +399,15 @@ __global__ void __launch_bounds__(kBS) k_eval(OpfDims d, DevNet net, const doubl
   constexpr int CM = MODE == EV_FG ? EV_G : MODE;  // mode of the constraint classes
   constexpr bool cons = CM == EV_G || CM == EV_J || CM == EV_H;
   int64_t b = blockIdx.x;
+#if GN_G_BUS_FIRST
+  if constexpr (CM == EV_G) {  // the latency-bound balance rows first, the line stream after
+    if (b < sg.bus) {
+      bus_body(d, net, x, out, st, b);
+      return;
+    }
+    b -= sg.bus;
+  }
+#endif
   if constexpr (cons) {
     if (b < sg.line) {
       if constexpr (CM == EV_G) {
@@ -408,6 +420,7 @@ __global__ void __launch_bounds__(kBS) k_eval(OpfDims d, DevNet net, const doubl
     }
     b -= sg.line;
   }
+#if !GN_G_BUS_FIRST
   if constexpr (CM == EV_G) {
     if (b < sg.bus) {
       bus_body(d, net, x, out, st, b);
@@ -415,6 +428,7 @@ __global__ void __launch_bounds__(kBS) k_eval(OpfDims d, DevNet net, const doubl
     }
     b -= sg.bus;
   }
+#endif
   if constexpr (cons) {
     if (b < sg.ramp) {
       ramp_body<CM>(d, net, x, out, st, b);
