@@ -184,7 +184,7 @@ def kernel_bytes(s, kkt, nlp, net, T):
     vth = (blk == 4) | (blk == 5)
     m_pq = int(lens[(blk == 2) | (blk == 3)].sum())
     m_g = int(lens[blk <= 1].sum())
-    # bus-column kernels by class (as the library forms them): buses of exactly D = 1..8
+    # bus-column kernels by class (as the library forms them): buses of exactly D = 1..6
     # lines without parallel lines -> k_fz_busr<dD>; the others -> k_fz_bus3<le8> (<= 8
     # lines) / k_fz_bus3<rest>.  Per class: its M slots, x(v, th) + Sx(v, th) of its
     # buses, and its share (half per line end) of the line inputs w(flow_p, flow_q),
@@ -197,12 +197,11 @@ def kernel_bytes(s, kkt, nlp, net, T):
     dup = uk[cnt > 1]
     par[(dup // N)] = True
     par[(dup % N)] = True
-    reg_max = 8  # kBusRegMax (gn_opf_kkt.cuh)
-    simple = (deg >= 1) & (deg <= reg_max) & ~par
-    cls = np.where(simple, deg - 1, np.where(deg <= 8, reg_max, reg_max + 1))
-    names = [f"k_fz_busr<d{k}>" for k in range(1, reg_max + 1)] + ["k_fz_bus3<le8>",
-                                                                  "k_fz_bus3<rest>"]
-    m_cls = [int(lens[vth & (cls[np.clip(ent, 0, N - 1)] == k)].sum()) for k in range(len(names))]
+    simple = (deg >= 1) & (deg <= 6) & ~par
+    cls = np.where(simple, deg - 1, np.where(deg <= 8, 6, 7))
+    names = ["k_fz_busr<d1>", "k_fz_busr<d2>", "k_fz_busr<d3>", "k_fz_busr<d4>", "k_fz_busr<d5>",
+             "k_fz_busr<d6>", "k_fz_bus3<le8>", "k_fz_bus3<rest>"]
+    m_cls = [int(lens[vth & (cls[np.clip(ent, 0, N - 1)] == k)].sum()) for k in range(8)]
     bus_cls = {nm: m_cls[k] + 4 * int((cls == k).sum()) * T + 2.5 * int(deg[cls == k].sum()) * T
                for k, nm in enumerate(names)}
     # balance rows (bus), flow / angle / thermal rows (line), ramp rows

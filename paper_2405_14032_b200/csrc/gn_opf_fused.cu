@@ -579,8 +579,8 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
     GN_CK(cudaEventRecord(X->ev_fork, s));
     for (int a = 0; a < nlanes; ++a) GN_CK(cudaStreamWaitEvent(X->aux[a], X->ev_fork, 0));
   }
-  // degree classes 1..8, le8, rest: round-robin over the lanes, largest first
-  static const int order[kBusClasses] = {2, 3, 1, 4, 5, 6, 7, 8, 9, 0};
+  // degree classes 1..6, le8, rest: round-robin over the lanes, largest first
+  static const int order[kBusClasses] = {2, 3, 1, 4, 5, 6, 7, 0};
   for (int i = 0; i < kBusClasses; ++i) {
     const int k = order[i];
     launch_fz_bus(t, X->bus_cls[k].p, X->n_bus_cls[k],

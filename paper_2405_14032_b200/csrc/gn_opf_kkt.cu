@@ -796,7 +796,7 @@ bool opf_kkt_prepare(gn_kkt* K) {
     }
     up(X->blx, blx, s);
     up(X->blgb, blgb, s);
-    // Register-resident classes (buses of exactly DEG = 1..8 lines, no parallel lines):
+    // Register-resident classes (buses of exactly DEG = 1..6 lines, no parallel lines):
     // per incidence the in-column offsets of its neighbour slots, read off the slot
     // program: (v(o), v(n)) | (th(o), v(n)) << 8 | (th(o), th(n)) << 16, 0xff = absent.
     std::vector<int32_t> bpos(bl.size(), 0xffffff);

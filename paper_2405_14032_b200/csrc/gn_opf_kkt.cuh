@@ -91,7 +91,7 @@ struct FIn {
 void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32_t maxdeg,
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows,
                    int32_t* bad, cudaStream_t s);
-constexpr int kBusRegMax = 8;
+constexpr int kBusRegMax = 6;
 // per bus: (n, bl begin, deg [| program length << 8], boff | program begin),
 // (lifted v rank, lifted th rank, 0, 0), (M start of v(n, t=0), v column length,
 // M start of th(n, t=0), th column length)
