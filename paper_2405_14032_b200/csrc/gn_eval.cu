@@ -3,7 +3,8 @@
 // bus x period), each writing its patterns' COO slots in the reference's
 // freeze order.  Each callback is ONE launch (k_eval<MODE>) whose grid is the
 // concatenation of the classes' block ranges (heavy line blocks first, the short
-// generator / ramp blocks fill the tail), so a callback costs one kernel boundary.  Closed-form derivatives of the 12 OPF patterns
+// generator / ramp blocks fill the tail), so a callback costs one kernel boundary.
+// Closed-form derivatives of the 12 OPF patterns
 // replace the reference's interpreted tape AD
 // (model/tape.hpp); value expressions keep the tape's operation order and
 // the library is built with -fmad=false, so g and J agree with the reference
@@ -19,6 +20,7 @@
 
 namespace gnb {
 
+// tuning-build switch (scripts/build_variant.py): balance-row blocks first in the trial launch
 #ifndef GN_G_BUS_FIRST
 #define GN_G_BUS_FIRST 1
 #endif
