@@ -24,7 +24,10 @@ namespace gnb {
 #ifndef GN_G_BUS_FIRST
 #define GN_G_BUS_FIRST 1
 #endif
-constexpr int kBS = 128;  // records per block (one per thread; 128 measured marginally ahead of 256)
+#ifndef GN_EVAL_BS
+#define GN_EVAL_BS 128
+#endif
+constexpr int kBS = GN_EVAL_BS;  // records per block (one per thread; 128 measured ahead of 256)
 
 __device__ __forceinline__ void report(unsigned long long* st, int pid, int64_t rec) {
   atomicMin(st, (static_cast<unsigned long long>(pid) << 32) |
