@@ -30,6 +30,10 @@
 
 namespace gnb {
 
+// multiplier of the KKT grid cap for the register-resident bus classes (tuning builds)
+#ifndef GN_BUSR_CAP_MUL
+#define GN_BUSR_CAP_MUL 1
+#endif
 #ifndef GN_BW3
 #define GN_BW3 4
 #endif
@@ -485,10 +489,10 @@ static void launch_busr(const OpfKktTab& t, const int4* buses, int32_t n_buses, 
   const int64_t nvb = (warps + kBW3 - 1) / kBW3;
   KTimer kt(names[DEG], s);
   if (rows)
-    k_fz_busr<DEG, true><<<grid_cap(nvb, t.grid_cap), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+    k_fz_busr<DEG, true><<<grid_cap(nvb, t.grid_cap * GN_BUSR_CAP_MUL), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
                                                              rows, bad);
   else
-    k_fz_busr<DEG, false><<<grid_cap(nvb, t.grid_cap), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
+    k_fz_busr<DEG, false><<<grid_cap(nvb, t.grid_cap * GN_BUSR_CAP_MUL), kBW3 * 32, 0, s>>>(t, nvb, buses, n_buses, in, dv, M,
                                                               rows, bad);
   count_launch();
 }
