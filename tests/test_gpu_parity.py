@@ -5,6 +5,8 @@ Bar (BASELINE.json north_star): structures and scatter maps bit-exact; values
 within 1e-12 relative with a 1e-14 absolute floor (helpers.REL/ABS); sums with
 no transcendental (balance rows, gradient, A, M given equal inputs) bit-exact.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -528,7 +530,7 @@ def test_destroy_order_any(gpu, order):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("GN_TEST_SEEDS", "8"))))
 def test_fused_kkt_randomised_networks(gpu, seed):
     """Randomised sweep: network size, parallel lines, shared generators, fixed
     generators / voltages, unrated lines and horizon length (partial 32-period chunks)
