@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
 // resident-CTA floors of the launch bounds (register caps); overridable for tuning builds
 // (scripts/build_variant.py)
 #ifndef GN_FL_GS_MINB
-#define GN_FL_GS_MINB 3
+#define GN_FL_GS_MINB 6
 #endif
 #ifndef GN_SJ_MINB
 #define GN_SJ_MINB 6
@@ -183,7 +183,10 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
 #ifndef GN_SJ_GS_MINB
 #define GN_SJ_GS_MINB 6
 #endif
-constexpr int kFLW = 8;     // warps per CTA
+#ifndef GN_FLW
+#define GN_FLW 4
+#endif
+constexpr int kFLW = GN_FLW;  // warps per CTA
 constexpr int kFLCap = 16;  // staged slots per column (longer columns are written in place)
 template <bool STRUCT>
 __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
@@ -401,7 +404,10 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 //   * thermal rows of (thermal line, 32 periods): (2p, 2q), lane = period;
 //   * angle rows of a line (all periods): (+1, -1) at the free angle slots;
 //   * ramp rows: one thread per row.
-constexpr int kSJW = 8;  // warps per CTA
+#ifndef GN_SJW
+#define GN_SJW 8
+#endif
+constexpr int kSJW = GN_SJW;  // warps per CTA
 __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t, int32_t m,
                                              const double* __restrict__ x,
                                              double* __restrict__ A, int skip_flow) {
