@@ -404,6 +404,10 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 //   * thermal rows of (thermal line, 32 periods): (2p, 2q), lane = period;
 //   * angle rows of a line (all periods): (+1, -1) at the free angle slots;
 //   * ramp rows: one thread per row.
+// the A kernel's own grid cap under a capped KKT (tuning builds; 0 = the KKT's cap)
+#ifndef GN_SJ_CAP
+#define GN_SJ_CAP 0
+#endif
 #ifndef GN_SJW
 #define GN_SJW 8
 #endif
@@ -654,7 +658,7 @@ static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream
     const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
                           (K->m - t.ramp0 + 31) / 32;
     const int64_t nvb = (warps + kSJW - 1) / kSJW;
-    const unsigned g = grid_cap(nvb, t.grid_cap);
+    const unsigned g = grid_cap(nvb, (GN_SJ_CAP > 0 && t.grid_cap > 0) ? GN_SJ_CAP : t.grid_cap);
     if (g < nvb)
       k_opf_set_jac_fused_gs<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
     else
