@@ -438,8 +438,10 @@ def run_ours(args, rank, world, local_rank, dist):
     assert sorted(cb_order) == sorted(["f", "grad", "g", "jac", "hess"]), cb_order
     cb_mark = {"f": 1, "g": 2, "jac": 3, "hess": 4}
 
-    def step(ev=None, serial=False):
-        """One unit; serial=True runs the KKT on the callback stream (per-kernel timing)."""
+    def step(ev=None, serial=False, kkt_wait=None, after_cb=None):
+        """One unit; serial=True runs the KKT on the callback stream (per-kernel timing).
+        kkt_wait: an extra event the KKT waits for (e2e: its Sigma copy); after_cb: called
+        once the callbacks are enqueued (e2e: their device-to-host copies)."""
         ks = stream if serial else kstream
         kkt.set_stream(ks.cuda_stream)  # no-op (no sync) when unchanged: capturable
 
@@ -453,6 +455,8 @@ def run_ours(args, rank, world, local_rank, dist):
         ev_x.record(stream)  # x (with its halo) ready
         if fused and ks is not stream:
             ks.wait_event(ev_x)
+            if kkt_wait is not None:
+                ks.wait_event(kkt_wait)
             mark(6, ks)
             kkt.update_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)  # set_jacobian + assemble
             mark(7, ks)
@@ -468,10 +472,14 @@ def run_ours(args, rank, world, local_rank, dist):
             from paper_2405_14032_b200.shard import global_objective
             with torch.cuda.stream(stream):
                 f_global.copy_(global_objective(f, world))
+        if after_cb is not None:
+            after_cb()
         if fused and ks is not stream:
             ev_k.record(ks)
             stream.wait_event(ev_k)
         elif fused:
+            if kkt_wait is not None:
+                stream.wait_event(kkt_wait)
             mark(6)
             kkt.update_x(dx, dwt, 1.0, dsx, dss, dw_reg, dc_reg, mem=A)  # set_jacobian + assemble
             mark(7)
@@ -601,20 +609,44 @@ def run_ours(args, rank, world, local_rank, dist):
         tsx.copy_(torch.from_numpy(sx)); tss.copy_(torch.from_numpy(ss))
         tf, tgrad, tg = pin(1), pin(s.n_vars), pin(s.n_cons)
         tA, tM = pin(kkt.a_nnz), pin(kkt.m_nnz)
-        ev_cb = torch.cuda.Event()
+        copy_s = torch.cuda.Stream(device=dev)  # Sigma host -> device beside the callbacks
+        d2h_s = torch.cuda.Stream(device=dev)   # f, grad, g device -> host beside the KKT
+        ev_sig, ev_cbdone, ev_d2h, ev_vals = (torch.cuda.Event() for _ in range(4))
 
         def e2e_fused_step():
+            # PCIe is full duplex: x and w go first (the callbacks need only them), Sigma
+            # follows on a copy stream while the callbacks run (the KKT waits for it), and
+            # f, grad, g return while the KKT runs; A and M return after the assembly.
             with torch.cuda.stream(stream):
                 dx.copy_(tx, non_blocking=True)
                 dwt.copy_(tw, non_blocking=True)
-                dsx.copy_(tsx, non_blocking=True)
-                dss.copy_(tss, non_blocking=True)
-            step()
-            with torch.cuda.stream(stream):  # the KKT stream has been joined by step()
-                tf.copy_(f, non_blocking=True)
-                tgrad.copy_(grad, non_blocking=True)
-                tg.copy_(g, non_blocking=True)
-                kkt.values_device(tA, tM, sync=False)  # pinned host is UVA-addressable
+            kw = None
+            if halo is None:
+                copy_s.wait_stream(stream)  # also orders the reuse of dsx / dss after the last step
+                with torch.cuda.stream(copy_s):
+                    dsx.copy_(tsx, non_blocking=True)
+                    dss.copy_(tss, non_blocking=True)
+                ev_sig.record(copy_s)
+                kw = ev_sig
+            else:  # the halo exchange at the start of the step reads / writes Sigma_s
+                with torch.cuda.stream(stream):
+                    dsx.copy_(tsx, non_blocking=True)
+                    dss.copy_(tss, non_blocking=True)
+
+            def after_cb():
+                ev_cbdone.record(stream)
+                d2h_s.wait_event(ev_cbdone)
+                with torch.cuda.stream(d2h_s):
+                    tf.copy_(f, non_blocking=True)
+                    tgrad.copy_(grad, non_blocking=True)
+                    tg.copy_(g, non_blocking=True)
+                ev_d2h.record(d2h_s)
+
+            step(kkt_wait=kw, after_cb=after_cb)
+            kkt.values_device(tA, tM, sync=False)  # on the KKT's stream, after the assembly
+            ev_vals.record(kstream)
+            stream.wait_event(ev_vals)  # the step ends when every copy has landed
+            stream.wait_event(ev_d2h)
 
         def timed(fn, k):
             fn()
@@ -640,13 +672,22 @@ def run_ours(args, rank, world, local_rank, dist):
             kkt.set_stream(stream.cuda_stream)
             e_ms = timed(e2e_fused_step, ksteps)
             assert nlp.status()
+            # the host copies of the last step are the device results, bit for bit
+            dA = torch.empty(kkt.a_nnz, **f64)
+            dM = torch.empty(kkt.m_nnz, **f64)
+            kkt.values_device(dA, dM, sync=True)
+            torch.cuda.synchronize()
+            assert torch.equal(tA.to(dev), dA) and torch.equal(tM.to(dev), dM), "e2e A/M copies"
+            assert torch.equal(tg.to(dev), g) and torch.equal(tgrad.to(dev), grad), "e2e g/grad"
+            assert torch.equal(tf.to(dev), f), "e2e f"
+            del dA, dM
             h2d = 8 * (s.n_vars + 2 * s.n_cons + s.n_free)
             d2h = 8 * (1 + s.n_vars + s.n_cons + kkt.a_nnz + kkt.m_nnz)
             e2e = {"value": nnz_step * world / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
                    "steps": ksteps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "path": "pinned host x, w, Sigma -> device; C-ABI device-pointer calls "
                            "(callbacks + fused KKT, as the timed step); f, grad, g, A, M -> "
-                           "pinned host"}
+                           "pinned host; Sigma in and f, grad, g out overlap the compute"}
 
         hx, hw, hsx, hss = tx.numpy(), tw.numpy(), tsx.numpy(), tss.numpy()
         hf, hgrad, hg = tf.numpy(), tgrad.numpy(), tg.numpy()
