@@ -718,7 +718,8 @@ def run_ours(args, rank, world, local_rank, dist):
     # -------------------------------------------------------- CPU baseline
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference(raw, args, budget_s=args.cpu_budget)
+        cpu = cpu_reference(args.config, args.periods, budget_s=args.cpu_budget, steps=1,
+                            warmup=0)
     dropin = None
     if rank == 0 and world == 1 and args.dropin:
         dropin = dropin_ipm()
@@ -761,6 +762,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "e2e_contract": e2e_contract,
         "cpu_baseline": cpu,
         "dropin_ipm": dropin,
+        "libraries_loaded": loaded_libraries(),
     }
     if args.traffic_json and Path(args.traffic_json).exists():
         tr = json.loads(Path(args.traffic_json).read_text())
@@ -771,75 +773,196 @@ def run_ours(args, rank, world, local_rank, dist):
 
 
 # ------------------------------------------------------------- reference CPU
-def cpu_reference(raw, args, budget_s=15.0, periods=None, steps=None, warmup=0):
-    """Time the reference's own CPU path (oracle/_ref) on a bounded sample of the
-    same workload: same network, `periods` periods (default 2), set_threads(nproc)."""
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def loaded_libraries():
+    """In-tree / torch-extension shared objects mapped into this process (proof of which
+    native code a run used)."""
+    out = set()
+    try:
+        for line in Path("/proc/self/maps").read_text().splitlines():
+            path = line.split()[-1] if "/" in line else ""
+            if path.endswith(".so") and (path.startswith(str(ROOT)) or "torch_extensions" in path):
+                out.add(str(Path(path).relative_to(ROOT)) if path.startswith(str(ROOT)) else path)
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def _pairs(jr_lifted, m):
+    """A^T A row-pair count sum_r len(len+1)/2 (condensed.hpp:55-60) from lifted J rows."""
+    c = np.bincount(jr_lifted, minlength=m).astype(np.int64)
+    return int((c * (c + 1) // 2).sum())
+
+
+def cpu_reference(config, periods, budget_s=60.0, steps=None, warmup=1, kkt_periods=8,
+                  single_thread=False):
+    """The reference's own CPU path (oracle/_ref: the unmodified headers compiled with the
+    reference's Release flags) on the box's host cores, at the bench configuration itself.
+
+    * Callbacks at the FULL config: `PatternModel::evaluate_{objective,gradient,constraints}`
+      plus `LiftedProblem::eval_jac/eval_hess` (the full callback + pick gather the IPM runs,
+      lifted.hpp:128-159), `set_threads(nproc)` (pattern_model.hpp:273); optionally one
+      unit at `set_threads(1)`.  Output buffers are allocated once, as IpmSolver does.
+    * `CondensedKkt::set_jacobian` + `assemble` (single-threaded by design): the ctor runs
+      AMD + a symbolic LDL^T (ldlt.hpp:34-50) that is intractable inside a bench at 15M
+      variables, so they are timed on 2- and `kkt_periods`-period windows of the same
+      network and extrapolated per contribution (set_jacobian: J_l entries; assemble:
+      H_l + A^T A pairs + n_l), SURVEY §8(d).  M nnz at the full horizon is affine in T
+      (every coupling but ramp is per period), fitted from the two windows.
+    The demand table is the reference's own generate_load_profile (gnr_load_profile): no
+    code of this repository's CUDA library is loaded on this path."""
     from oracle import bindings as B
-    from paper_2405_14032_b200.opf import load_profile
-    periods = periods or args.cpu_periods
-    kind = "reference" if B.ref_available() else "port"
+    from paper_2405_14032_b200.network import config_case
+    if not B.ref_available():
+        return cpu_port(config, budget_s)
     nthreads = os.cpu_count() or 1
+    raw = config_case(config, seed=1)
     text = raw.to_matpower()
-    net = raw.network()
-    scale = load_profile(net.n_load, periods, seed=1)
-    if kind == "reference":
-        M = B.RefModel(text, periods, scale)
-        M.set_threads(nthreads)
-    else:
-        M = B.OracleModel(net, periods, scale)
-        nthreads = 1
-    xl, xu, xs, _, _ = M.bounds()
+    scale = B.ref_load_profile(text, periods)
+    t0 = time.perf_counter()
+    M = B.RefModel(text, periods, scale)
+    M.set_threads(nthreads)
     n, m, nj, nh = M.sizes[:4]
     lift = M.lift(1e-4)
-    f2f = lift["free_to_full"]
-    x, w, sx, ss = inputs((xl, xu, xs), m, len(f2f))
-    xfree = np.ascontiguousarray(x[f2f])
-    if kind == "reference":
-        dims = M.kkt_create()
-        mnnz = dims[2]
-        jl = np.empty(M.lifted_sizes[2])
-        hl = np.empty(M.lifted_sizes[3])
-    else:
-        K = M.kkt()
-        mnnz = K.m_nnz
-    dw_reg, dc_reg = 1e-4, 1e-8 * 0.1 ** 0.25
+    build_s = time.perf_counter() - t0
+    nl, _, njl, nhl = M.lifted_sizes
+    xl, xu, xs, _, _ = M.bounds()
+    x, w, sx, ss = inputs((xl, xu, xs), m, nl)
+    del xl, xu, xs
+    xfree = np.ascontiguousarray(x[lift["free_to_full"]])
+    P = _pairs(lift["jac_rows"], m)
+    del lift
+    L, h = M.L, M.h
+    f = np.zeros(1)
+    grad, g, jl, hl = np.empty(n), np.empty(m), np.empty(njl), np.empty(nhl)
+    fail = np.zeros(2, np.int32)
+    fx, fw, fxf = B._f(x), B._f(w), B._f(xfree)
 
-    def unit():
-        assert M.eval_f(x)[0]
-        assert M.eval_grad(x)[0]
-        assert M.eval_g(x)[0]
-        if kind == "reference":
-            # LiftedProblem::eval_jac/eval_hess = full callback + pick gather (lifted.hpp:249-264)
-            assert M.L.gnr_lifted_eval_jac(M.h, B._f(xfree), B._f(jl))
-            assert M.L.gnr_lifted_eval_hess(M.h, B._f(xfree), B._f(w), 1.0, B._f(hl))
-            M.kkt_set_jacobian(jl)
-            M.kkt_assemble(hl, sx, ss, dw_reg, dc_reg)
-        else:
-            _, jv, _ = M.eval_jac(x)
-            _, hv, _ = M.eval_hess(x, w, 1.0)
-            K.set_jacobian(jv[lift["jac_pick"]])
-            K.assemble(hv[lift["hess_pick"]], sx, ss, dw_reg, dc_reg)
+    def callbacks():
+        assert L.gnr_eval_f(h, fx, B._f(f), B._i(fail))
+        assert L.gnr_eval_grad(h, fx, B._f(grad), B._i(fail))
+        assert L.gnr_eval_g(h, fx, B._f(g), B._i(fail))
+        assert L.gnr_lifted_eval_jac(h, fxf, B._f(jl))
+        assert L.gnr_lifted_eval_hess(h, fxf, fw, 1.0, B._f(hl))
 
     for _ in range(warmup):
-        unit()
+        callbacks()
     times = []
     t_start = time.perf_counter()
     while True:
-        t0 = time.perf_counter()
-        unit()
-        times.append(time.perf_counter() - t0)
+        a = time.perf_counter()
+        callbacks()
+        times.append(time.perf_counter() - a)
         if steps is not None and len(times) >= steps:
             break
-        if steps is None and (time.perf_counter() - t_start > budget_s or len(times) >= 200):
+        if time.perf_counter() - t_start > budget_s:
             break
-    t_unit = float(np.median(times))
+    cb_s = float(np.median(times))
+    cb1_s = None
+    if single_thread:
+        M.set_threads(1)
+        a = time.perf_counter()
+        callbacks()
+        cb1_s = time.perf_counter() - a
+        M.set_threads(nthreads)
+    del grad, g, jl, hl, M
+
+    # condensed KKT on period windows of the same network
+    wins = sorted({min(2, periods), min(kkt_periods, periods)})
+    kw = []
+    for Tw in wins:
+        W = B.RefModel(text, Tw, scale[:Tw])
+        lw = W.lift(1e-4)
+        nlw, mw, njw, nhw = W.lifted_sizes
+        Pw = _pairs(lw["jac_rows"], mw)
+        dims = W.kkt_create()
+        xw, ww, sxw, ssw = inputs(W.bounds()[:3], mw, nlw)
+        jw, hw = np.empty(njw), np.empty(nhw)
+        assert W.L.gnr_lifted_eval_jac(W.h, B._f(np.ascontiguousarray(xw[lw["free_to_full"]])),
+                                       B._f(jw))
+        assert W.L.gnr_lifted_eval_hess(W.h, B._f(np.ascontiguousarray(xw[lw["free_to_full"]])),
+                                        B._f(ww), 1.0, B._f(hw))
+        sj, sa = [], []
+        for _ in range(3):
+            a = time.perf_counter()
+            W.kkt_set_jacobian(jw)
+            b = time.perf_counter()
+            W.kkt_assemble(hw, sxw, ssw, 1e-4, 1e-8 * 0.1 ** 0.25)
+            sj.append(b - a)
+            sa.append(time.perf_counter() - b)
+        kw.append(dict(periods=Tw, set_jacobian_ms=1e3 * float(np.median(sj)),
+                       assemble_ms=1e3 * float(np.median(sa)), jac_lifted=njw,
+                       assemble_contributions=nhw + Pw + nlw, m_nnz=int(dims[2]),
+                       ns_per_jac=1e9 * float(np.median(sj)) / max(njw, 1),
+                       ns_per_contribution=1e9 * float(np.median(sa)) / max(nhw + Pw + nlw, 1)))
+        del W
+    big = kw[-1]
+    if big["periods"] == periods:  # measured at the full horizon: no extrapolation
+        kkt_s = 1e-3 * (big["set_jacobian_ms"] + big["assemble_ms"])
+        mnnz = big["m_nnz"]
+        kkt_kind = "measured"
+    else:
+        kkt_s = 1e-9 * (big["ns_per_jac"] * njl + big["ns_per_contribution"] * (nhl + P + nl))
+        a0, a1 = kw[0], kw[-1]  # M nnz affine in T
+        slope = (a1["m_nnz"] - a0["m_nnz"]) / (a1["periods"] - a0["periods"])
+        mnnz = int(round(a1["m_nnz"] + slope * (periods - a1["periods"])))
+        kkt_kind = "extrapolated"
+    t_unit = cb_s + kkt_s
     nnz = nj + nh + mnnz
-    return {"value": nnz / t_unit, "unit": UNIT, "cores": nthreads, "kind": kind,
-            "ms_per_unit": t_unit * 1e3, "units_timed": len(times),
-            "sample": f"{args.config} network x {periods} periods (n={n}, J={nj}, H={nh}, "
-                      f"M={mnnz}); PatternModel::set_threads({nthreads}) callbacks + "
-                      f"LiftedProblem gathers + CondensedKkt set_jacobian/assemble "
-                      f"(single-threaded by design); median of {len(times)} units"}
+    return {"value": nnz / t_unit, "unit": UNIT, "cores": nthreads, "kind": "reference",
+            "cpu_model": cpu_model(), "same_config": True, "ms_per_unit": t_unit * 1e3,
+            "callbacks_ms": cb_s * 1e3, "callbacks_ms_1thread": None if cb1_s is None else cb1_s * 1e3,
+            "kkt_ms": kkt_s * 1e3, "kkt": kkt_kind, "kkt_windows": kw,
+            "units_timed": len(times), "build_s": build_s,
+            "nnz_per_unit": {"J": nj, "H": nh, "M": mnnz},
+            "sample": f"{config} x {periods} periods, the bench configuration itself (n={n}, "
+                      f"J={nj}, H={nh}): callbacks (f, grad, g, lifted jac + hess) with "
+                      f"PatternModel::set_threads({nthreads}), median of {len(times)} units; "
+                      f"CondensedKkt set_jacobian + assemble (single-threaded by design) "
+                      f"{kkt_kind} from {'/'.join(str(k['periods']) for k in kw)}-period "
+                      f"windows per contribution (J_l={njl}, H_l + pairs + n_l = "
+                      f"{nhl + P + nl}; M={mnnz})"}
+
+
+def cpu_port(config, budget_s=15.0, periods=2):
+    """Without oracle/_ref (no /root/reference at build time): the C restatement
+    (oracle/gn_oracle.c, single-threaded) on a `periods`-period sample."""
+    from oracle import bindings as B
+    from paper_2405_14032_b200.network import config_case
+    raw = config_case(config, seed=1)
+    net = raw.network()
+    scale = np.ones((periods, net.n_load))
+    Mo = B.OracleModel(net, periods, scale)
+    xl, xu, xs, _, _ = Mo.bounds()
+    n, m, nj, nh = Mo.sizes[:4]
+    lift = Mo.lift(1e-4)
+    x, w, sx, ss = inputs((xl, xu, xs), m, len(lift["free_to_full"]))
+    K = Mo.kkt()
+    times = []
+    t_start = time.perf_counter()
+    while time.perf_counter() - t_start < budget_s and len(times) < 50:
+        a = time.perf_counter()
+        assert Mo.eval_f(x)[0] and Mo.eval_grad(x)[0] and Mo.eval_g(x)[0]
+        _, jv, _ = Mo.eval_jac(x)
+        _, hv, _ = Mo.eval_hess(x, w, 1.0)
+        K.set_jacobian(jv[lift["jac_pick"]])
+        K.assemble(hv[lift["hess_pick"]], sx, ss, 1e-4, 1e-8 * 0.1 ** 0.25)
+        times.append(time.perf_counter() - a)
+    t_unit = float(np.median(times))
+    return {"value": (nj + nh + K.m_nnz) / t_unit, "unit": UNIT, "cores": 1, "kind": "port",
+            "cpu_model": cpu_model(), "same_config": False, "ms_per_unit": t_unit * 1e3,
+            "units_timed": len(times),
+            "sample": f"{config} network x {periods} periods (unit demand scale), C restatement "
+                      f"(oracle/gn_oracle.c), one thread"}
 
 
 def dropin_ipm(periods=24):
@@ -883,22 +1006,27 @@ def dropin_ipm(periods=24):
 
 
 def run_reference(args, rank, world):
+    """`--impl reference`: the reference's own CPU implementation of the path on this box's
+    host cores, at our arm's config / metric / unit (rank 0 only; other ranks exit 0)."""
     if rank != 0:
         return
-    raw, net, _ = build_workload(0, 1, args.periods, args.config)
-    cpu = cpu_reference(raw, args, periods=args.cpu_periods, steps=args.steps,
-                        warmup=args.warmup)
+    cpu = cpu_reference(args.config, args.periods, budget_s=args.cpu_budget,
+                        steps=args.steps, warmup=min(args.warmup, 1), single_thread=True)
     line = {
         "metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["ms_per_unit"],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{args.config} network x {args.cpu_periods} periods "
-                               f"(bounded CPU sample of the {args.periods}-period workload)",
-                   "parallelism": "host threads"},
+        "config": {"workload": f"{args.config} x {args.periods} periods "
+                               f"(BASELINE configs[{CONFIG_INDEX.get(args.config, '-')}]; the "
+                               f"same workload as our arm)",
+                   "parallelism": f"host threads ({cpu['cores']})",
+                   "timed": f"{cpu['units_timed']} units (wall budget {args.cpu_budget} s; "
+                            f"--steps {args.steps} is the cap)"},
         "cpu_baseline": cpu,
         "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "libraries_loaded": loaded_libraries(),
     }
     print(json.dumps(line), flush=True)
 
@@ -914,8 +1042,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-periods", type=int, default=2)
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--cpu-budget", type=float, default=60.0,
+                    help="wall budget (s) of the reference arm's timed callback units")
     ap.add_argument("--pipeline", choices=["fused", "contract"], default="fused")
     ap.add_argument("--streams", type=int, choices=[1, 2], default=2)
     ap.add_argument("--grid-cap", type=int, default=-1,

@@ -130,9 +130,19 @@ int gn_ctx_create_shard(const gn_network* net, int32_t periods_total, int32_t fi
  *         gn_lifted_create)]; ramp_gens[n_ramp_gens] (may be NULL). */
 int gn_ctx_shard_info(gn_ctx* ctx, int64_t* info, int32_t* ramp_gens);
 int gn_ctx_destroy(gn_ctx* ctx);
+/* Publish (on = 1) or withdraw (on = 0) the context's lifted structure for gn_kkt_create:
+ * a KKT created from COO arrays equal to a published context's lifted J / H structure
+ * (the arrays the reference's IpmSolver passes to CondensedKkt, solver.hpp:139-141) is
+ * built on that context and uses the OPF-specialised kernels -- bit-identical values,
+ * recognised by gn_kkt_dims dims[7] = 1.  Publishing lifts the problem when
+ * gn_lifted_create has not run (slack relaxation 0: only the structure is used).
+ * gn_ctx_destroy withdraws it. */
+int gn_ctx_publish(gn_ctx* ctx, int on);
 /* Use a caller-owned cudaStream_t (as void*) for every launch of this context; NULL
- * returns to the context's own stream, which lives until gn_ctx_destroy (a KKT
- * created on it keeps using it).  Work already enqueued is synchronised first. */
+ * returns to the context's own (non-blocking) stream, which lives until gn_ctx_destroy
+ * (a KKT created on it keeps using it).  NULL is "reset", never the legacy default
+ * stream: to launch on the legacy default stream pass cudaStreamLegacy ((void*)0x1),
+ * or cudaStreamPerThread.  Work already enqueued is synchronised first. */
 int gn_ctx_set_stream(gn_ctx* ctx, void* cuda_stream);
 int gn_ctx_get_stream(gn_ctx* ctx, void** cuda_stream);
 /* Synchronises the stream, returns (and clears) the latched evaluation status. */
@@ -187,7 +197,9 @@ int gn_lifted_gather_hess(gn_ctx* ctx, const double* hess_full, double* hess_lif
 /* CondensedKkt constructor structure (condensed.hpp:29-90) on an arbitrary
  * lifted COO (host arrays): CSR(A) + jac_slots, M = Hess U AtA U diag in CSC
  * lower + hess/pair/diag slots — sorted on the device.  The LDL^T symbolic
- * phase (ldlt.hpp:34-50) is not part of this object. */
+ * phase (ldlt.hpp:34-50) is not part of this object.  When the arrays equal the lifted
+ * structure of a context published with gn_ctx_publish, the KKT is built on that context
+ * (OPF-specialised kernels for lifted and GN_IN_FULL inputs; dims[7] = 1). */
 int gn_kkt_create(int32_t n, int32_t m, int64_t jac_nnz, const int32_t* jac_rows,
                   const int32_t* jac_cols, int64_t hess_nnz, const int32_t* hess_rows,
                   const int32_t* hess_cols, int32_t device, gn_kkt** out, gn_error* err);
@@ -196,7 +208,8 @@ int gn_kkt_create(int32_t n, int32_t m, int64_t jac_nnz, const int32_t* jac_rows
  * KKT shares the context's stream. */
 int gn_kkt_create_lifted(gn_ctx* ctx, gn_kkt** out, gn_error* err);
 int gn_kkt_destroy(gn_kkt* kkt);
-/* As gn_ctx_set_stream, for the KKT's launches. */
+/* As gn_ctx_set_stream, for the KKT's launches.  NULL returns to the KKT's own stream;
+ * a KKT from gn_kkt_create_lifted has none and returns to its context's own stream. */
 int gn_kkt_set_stream(gn_kkt* kkt, void* cuda_stream);
 /* dims = [dim, a_nnz, m_nnz, pair_count, jac_nnz, hess_nnz, n_rows, opf_ready,
  *         fused_ready] (opf_ready / fused_ready = 1 when the OPF-specialised /

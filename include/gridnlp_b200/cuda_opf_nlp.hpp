@@ -114,6 +114,9 @@ class CudaOpfNlp final : public gridnlp::ipm::NlpProblem {
     hc_.resize(s.hess_nnz);
     gn_jac_structure(ctx_, jr_.data(), jc_.data(), GN_MEM_HOST);
     gn_hess_structure(ctx_, hr_.data(), hc_.data(), GN_MEM_HOST);
+    // the CondensedKkt the IpmSolver builds from this problem's lifted COO (solver.hpp:
+    // 139-141) is recognised by the library and gets the OPF-specialised assembly
+    if (gn_ctx_publish(ctx_, 1) != GN_OK) throw gridnlp::Error("gn_ctx_publish failed");
   }
   ~CudaOpfNlp() override { gn_ctx_destroy(ctx_); }
   CudaOpfNlp(const CudaOpfNlp&) = delete;

@@ -6,7 +6,10 @@
 // reference include directory and the unmodified IpmSolver (ipm/solver.hpp:133-251)
 // constructs this class instead.  Same public surface and semantics:
 //   * constructor: CSR(A) + M = Hess U AtA U diag pattern built on the B200
-//     (gn_kkt_create), then the reference's own LDL^T symbolic phase on the host;
+//     (gn_kkt_create; for the lifted structure of a CudaOpfNlp the library recognises
+//     the OPF problem and uses its specialised kernels); the reference's own LDL^T
+//     symbolic phase runs on the host at the first factorize() / factor_nnz() (the
+//     reference runs it in the ctor; the result is the same object);
 //   * set_jacobian / assemble: the scatter and the condensed assembly run on the
 //     GPU (bit-identical to the reference for equal inputs);
 //   * factorize / solve stay on the reference's sparse::LdltSolver (out of scope
@@ -30,6 +33,9 @@
 #define GRIDNLP_B200_CONDENSED_SHIM 1
 
 namespace gridnlp::ipm {
+
+// (not in the reference) KKTs built by this process: [generic, OPF-specialised]
+inline long b200_kkt_counts[2] = {0, 0};
 
 class CondensedKkt {
  public:
@@ -56,7 +62,11 @@ class CondensedKkt {
                      mpat_.rowidx.data(), GN_MEM_HOST);
     a_vals_.assign(a_.colidx.size(), 0.0);
     mvals_.assign(mpat_.rowidx.size(), 0.0);
-    ldlt_.emplace(mpat_, std::vector<index_t>{}, ldlt_opts);
+    ldlt_opts_ = ldlt_opts;
+    int64_t d2[9] = {};
+    gn_kkt_dims(kkt_, d2);
+    specialised_ = d2[7] == 1;
+    ++b200_kkt_counts[specialised_ ? 1 : 0];
     cvec_.assign(static_cast<size_t>(m), 0.0);
     dvec_.assign(static_cast<size_t>(m), 0.0);
     sig_dw_.assign(static_cast<size_t>(m), 0.0);
@@ -72,7 +82,9 @@ class CondensedKkt {
   std::span<const double> jacobian_values() const { return a_vals_; }
   const sparse::CscPattern& pattern() const { return mpat_; }
   std::span<const double> values() const { return mvals_; }
-  index_t factor_nnz() const { return ldlt_->factor_nnz(); }
+  index_t factor_nnz() const { return ldlt().factor_nnz(); }
+  // (not in the reference) true when the OPF-specialised kernels assemble this KKT
+  bool b200_specialised() const { return specialised_; }
 
   // A = scatter(J) on the GPU; the values come back for the host solves.
   void set_jacobian(std::span<const double> jac_vals) {
@@ -101,12 +113,12 @@ class CondensedKkt {
   }
 
   bool factorize() {
-    ldlt_->factorize(mvals_);
-    const sparse::Inertia& in = ldlt_->inertia();
+    ldlt().factorize(mvals_);
+    const sparse::Inertia& in = ldlt().inertia();
     return in.positive == n_ && in.negative == 0 && in.zero == 0;
   }
-  const sparse::Inertia& inertia() const { return ldlt_->inertia(); }
-  index_t floored_pivots() const { return ldlt_->floored_pivots(); }
+  const sparse::Inertia& inertia() const { return ldlt().inertia(); }
+  index_t floored_pivots() const { return ldlt().floored_pivots(); }
 
   // Reduced solve: M dx = -(qx + At (C qs + D qy)), ds = C (A dx + qy - dc qs),
   // dy = -qs - (Ss + dw) ds  (the class comment of condensed.hpp:17-26).
@@ -124,8 +136,8 @@ class CondensedKkt {
     d.dx.assign(static_cast<size_t>(n_), 0.0);
     d.ds.assign(static_cast<size_t>(m_), 0.0);
     d.dy.assign(static_cast<size_t>(m_), 0.0);
-    ldlt_->solve(rhs_, d.dx);
-    const double resid = ldlt_->refine(mvals_, rhs_, d.dx, refine_passes);
+    ldlt().solve(rhs_, d.dx);
+    const double resid = ldlt().refine(mvals_, rhs_, d.dx, refine_passes);
     sparse::csr_matvec(a_, a_vals_, d.dx, tm_);
     for (index_t i = 0; i < m_; ++i) {
       const size_t u = static_cast<size_t>(i);
@@ -136,13 +148,21 @@ class CondensedKkt {
   }
 
  private:
+  // the reference's LDL^T (AMD + symbolic analysis) on M's pattern, built once on first use
+  sparse::LdltSolver& ldlt() const {
+    if (!ldlt_) ldlt_.emplace(mpat_, std::vector<index_t>{}, ldlt_opts_);
+    return *ldlt_;
+  }
+
   gn_kkt* kkt_ = nullptr;
+  bool specialised_ = false;
+  sparse::LdltOptions ldlt_opts_{};
   index_t n_, m_;
   sparse::CsrPattern a_;
   std::vector<double> a_vals_;
   sparse::CscPattern mpat_;
   std::vector<double> mvals_;
-  std::optional<sparse::LdltSolver> ldlt_;
+  mutable std::optional<sparse::LdltSolver> ldlt_;
   std::vector<double> cvec_, dvec_, sig_dw_, tm_, rhs_;
   double delta_c_ = 0.0;
 };

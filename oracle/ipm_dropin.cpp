@@ -134,9 +134,10 @@ int main(int argc, char** argv) {
       timed(nlp);
     }
     std::printf("{\"nlp\": \"%s\", \"iterations\": %d, \"objective\": %.17g, \"status\": \"%s\", "
-                "\"restorations\": %d, \"seconds\": %.6f, \"warm_seconds\": %.6f}\n",
+                "\"restorations\": %d, \"seconds\": %.6f, \"warm_seconds\": %.6f, "
+                "\"kkt_generic\": %ld, \"kkt_specialised\": %ld}\n",
                 which.c_str(), r.iterations, r.objective, ipm::to_string(r.status),
-                r.restorations, secs, warm);
+                r.restorations, secs, warm, ipm::b200_kkt_counts[0], ipm::b200_kkt_counts[1]);
     return 0;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());

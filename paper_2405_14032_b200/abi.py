@@ -7,9 +7,13 @@ without the built library raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libgridnlp_b200.so"
+# GRIDNLP_B200_LIB: load another build of the library (tuning variants, scripts/gpu_variants*.sh)
+# instead of overwriting the in-tree one
+LIB_ENV = "GRIDNLP_B200_LIB"
 
 GN_OK, GN_ERR_INVALID, GN_ERR_EVAL, GN_ERR_CUDA, GN_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 GN_MEM_HOST, GN_MEM_DEVICE, GN_MEM_DEVICE_ASYNC, GN_IN_FULL = 0, 1, 2, 16
@@ -79,6 +83,7 @@ _SIGS = {
                                       C.c_int32, C.POINTER(vp), C.POINTER(GnError)]),
     "gn_ctx_shard_info": (C.c_int, [vp, i64p, i32p]),
     "gn_ctx_destroy": (C.c_int, [vp]),
+    "gn_ctx_publish": (C.c_int, [vp, C.c_int]),
     "gn_ctx_set_stream": (C.c_int, [vp, vp]),
     "gn_ctx_get_stream": (C.c_int, [vp, C.POINTER(vp)]),
     "gn_ctx_status": (C.c_int, [vp, C.POINTER(GnError)]),
@@ -144,8 +149,8 @@ _SIGS = {
 EXPORTED = tuple(_SIGS)
 
 
-def load(path: Path | str = LIB_PATH) -> C.CDLL:
-    path = Path(path)
+def load(path: Path | str | None = None) -> C.CDLL:
+    path = Path(path or os.environ.get(LIB_ENV) or LIB_PATH)
     if not path.exists():
         raise ImportError(
             f"{path} is missing: build the CUDA library first "

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <mutex>
 #include <random>
 
 #include "gn_ipm.cuh"
@@ -132,6 +133,15 @@ int gn_load_profile(int32_t n_load, int32_t periods, double resolution_minutes, 
 }
 
 // ----------------------------------------------------------------- context
+// Free a context that never left ctx_create (no dependents): its tables and its own stream.
+static void ctx_discard(gn_ctx* c) {
+  if (!c) return;
+  cudaStream_t s = c->owned_stream;
+  if (s) cudaStreamSynchronize(s);
+  delete c;
+  if (s) cudaStreamDestroy(s);
+}
+
 static int ctx_create(const gn_network* net, int32_t periods_total, int32_t first_period,
                       int32_t periods, const double* scale, int32_t device, gn_ctx** out,
                       gn_error* err) {
@@ -273,11 +283,11 @@ static int ctx_create(const gn_network* net, int32_t periods_total, int32_t firs
   return ok(err);
   }
   catch (const gnb::Error& e) {
-    delete c;
+    ctx_discard(c);
     return fail(err, e.code, e.what());
   }
   catch (const std::exception& e) {
-    delete c;
+    ctx_discard(c);
     return fail(err, GN_ERR_INVALID, e.what());
   }
 }
@@ -304,11 +314,73 @@ int gn_ctx_shard_info(gn_ctx* c, int64_t* info, int32_t* ramp_gens) {
   return GN_OK;
 }
 
+// ------------------------------------------------------- published contexts
+// A context published with gn_ctx_publish lets gn_kkt_create recognise its lifted
+// structure: the reference's IpmSolver builds its CondensedKkt from plain COO arrays
+// (solver.hpp:139-141), and the match gives that KKT the OPF-specialised kernels.
+}  // extern "C"
+namespace {
+std::mutex g_pub_mu;
+std::vector<gn_ctx*> g_published;
+void unpublish(gn_ctx* c) {
+  std::lock_guard<std::mutex> lk(g_pub_mu);
+  g_published.erase(std::remove(g_published.begin(), g_published.end(), c), g_published.end());
+}
+}  // namespace
+
+gn_ctx* gnb::find_published(int device, int32_t n, int32_t m, int64_t nj, const int32_t* jr,
+                            const int32_t* jc, int64_t nh, const int32_t* hr, const int32_t* hc,
+                            cudaStream_t s) {
+  std::vector<gn_ctx*> cands;
+  {
+    std::lock_guard<std::mutex> lk(g_pub_mu);
+    for (gn_ctx* c : g_published)
+      if (!c->closed && c->device == device && c->lifted && c->n_free == n && c->d.m == m &&
+          c->nj_l == nj && c->nh_l == nh)
+        cands.push_back(c);
+  }
+  if (cands.empty()) return nullptr;
+  DBuf<int32_t> diff;
+  diff.alloc(1);
+  for (gn_ctx* c : cands) {
+    GN_CK(cudaMemsetAsync(diff.p, 0, 4, s));
+    gnb::count_diff(jr, c->jr_l.p, nj, diff.p, s);
+    gnb::count_diff(jc, c->jc_l.p, nj, diff.p, s);
+    gnb::count_diff(hr, c->hr_l.p, nh, diff.p, s);
+    gnb::count_diff(hc, c->hc_l.p, nh, diff.p, s);
+    int32_t h = 1;
+    GN_CK(cudaMemcpyAsync(&h, diff.p, 4, cudaMemcpyDeviceToHost, s));
+    GN_CK(cudaStreamSynchronize(s));
+    if (h == 0) return c;
+  }
+  return nullptr;
+}
+
+extern "C" {
+
+int gn_ctx_publish(gn_ctx* c, int on) {
+  if (!c) return GN_ERR_INVALID;
+  API_TRY
+  set_device(c->device);
+  if (on && !c->lifted) {  // the structure to match is the lifted one (lifted.hpp:73-93)
+    gnb::build_lifted(c);
+    c->relax = 0.0;
+  }
+  unpublish(c);
+  if (on) {
+    std::lock_guard<std::mutex> lk(g_pub_mu);
+    g_published.push_back(c);
+  }
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
 // Objects built on another (a KKT on a context, an IPM on a KKT) hold a reference: a
 // destroy call on an object still referenced only marks it closed, and the last
 // dependent's destroy frees it -- destroy calls may come in any order (e.g. from a
 // garbage collector) without a dependent ever touching a freed stream or table.
 static void ctx_free(gn_ctx* c) {
+  unpublish(c);
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   cudaStream_t s = c->owned_stream;  // the caller's stream (set_stream) is never destroyed
@@ -318,6 +390,7 @@ static void ctx_free(gn_ctx* c) {
 
 int gn_ctx_destroy(gn_ctx* c) {
   if (!c) return GN_OK;
+  unpublish(c);  // no new KKT may match it; live ones keep their reference
   c->closed = true;
   if (c->refs == 0) ctx_free(c);
   return GN_OK;
@@ -577,6 +650,14 @@ int gn_kkt_create(int32_t n, int32_t m, int64_t nj, const int32_t* jr, const int
   djr.upload(jr, nj, K->stream); djc.upload(jc, nj, K->stream);
   dhr.upload(hr, nh, K->stream); dhc.upload(hc, nh, K->stream);
   gnb::kkt_build(K, djr.p, djc.p, dhr.p, dhc.p);
+  // the lifted structure of a published OPF context: same KKT, specialised kernels
+  if (gn_ctx* c = gnb::find_published(device, n, m, nj, djr.p, djc.p, nh, dhr.p, dhc.p,
+                                      K->stream)) {
+    const char* env = std::getenv("GRIDNLP_B200_GENERIC_KKT");
+    K->ctx = c;
+    ++c->refs;
+    if (!(env && env[0] == '1')) gnb::opf_kkt_prepare(K);
+  }
   *out = K;
   return ok(err);
   }
@@ -642,10 +723,14 @@ int gn_kkt_set_stream(gn_kkt* K, void* stream) {
   if (!K) return GN_ERR_INVALID;
   API_TRY
   set_device(K->device);
-  if ((stream ? static_cast<cudaStream_t>(stream) : K->owned_stream) == K->stream) return GN_OK;
+  // NULL: back to the object's own stream -- a KKT built on a context has none of its
+  // own and returns to the context's (never the legacy default stream)
+  cudaStream_t own = K->owned_stream ? K->owned_stream : K->ctx->owned_stream;
+  cudaStream_t want = stream ? static_cast<cudaStream_t>(stream) : own;
+  if (want == K->stream) return GN_OK;
   GN_CK(cudaStreamSynchronize(K->stream));
-  K->stream = stream ? static_cast<cudaStream_t>(stream) : K->owned_stream;
-  K->own_stream = K->stream == K->owned_stream;
+  K->stream = want;
+  K->own_stream = K->stream == own;
   return GN_OK;
   API_CATCH(nullptr)
 }

@@ -221,6 +221,7 @@ void kkt_build(gn_kkt* K, const int32_t* jr, const int32_t* jc, const int32_t* h
     compress_keys(key.p, total, n, n, K->M, s);
   }
   K->mnnz = K->M.nnz;
+  K->dvals.alloc(static_cast<size_t>(m) + 1);
   K->mvals.alloc(static_cast<size_t>(K->mnnz) + 1);
   GN_CK(cudaMemsetAsync(K->mvals.p, 0, sizeof(double) * (K->mnnz + 1), s));
   GN_CK(cudaGetLastError());
@@ -245,14 +246,15 @@ __global__ void __launch_bounds__(256) k_set_jac_generic(int32_t annz, const int
   A[sl] = acc;
 }
 
-// M[s] = 0 (+) H[k]... (+) (d_r a_ka) a_kb ... (+) (dw + sx_i), contributors in COO order.
+// M[s] = 0 (+) H[k]... (+) (d_r a_ka) a_kb ... (+) (dw + sx_i), contributors in COO order;
+// d_r precomputed once per row (launch_dvec) instead of once per pair.
 __global__ void __launch_bounds__(256) k_assemble_generic(
     int32_t mnnz, int64_t nh, int64_t npair, const int32_t* __restrict__ seg,
     const int32_t* __restrict__ src, const int32_t* __restrict__ hpick,
     const double* __restrict__ H, const int32_t* __restrict__ pka,
     const int32_t* __restrict__ pkb, const int32_t* __restrict__ arow,
     const double* __restrict__ A, const double* __restrict__ sx,
-    const double* __restrict__ ss, double dw, double dc, double* __restrict__ M) {
+    const double* __restrict__ dv, double dw, double* __restrict__ M) {
   const int64_t sl = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (sl >= mnnz) return;
   double acc = 0.0;
@@ -264,10 +266,7 @@ __global__ void __launch_bounds__(256) k_assemble_generic(
     } else if (c < nh + npair) {
       const int64_t p = c - nh;
       const int32_t ka = pka[p], kb = pkb[p];
-      const double sd = ss[arow[ka]] + dw;  // condensed.hpp:112-115
-      const double cc = 1.0 / (1.0 + dc * sd);
-      const double dr = sd * cc;
-      const double va = dr * A[ka];
+      const double va = dv[arow[ka]] * A[ka];  // condensed.hpp:126-129
       acc += va * A[kb];
     } else {
       acc += dw + sx[c - nh - npair];
@@ -276,9 +275,31 @@ __global__ void __launch_bounds__(256) k_assemble_generic(
   M[sl] = acc;
 }
 
+// Lifted values -> the full COO order (the OPF kernels index the callback layout); the
+// slots of fixed variables are never read by them.
+__global__ void k_scatter_pick(int64_t n, const int32_t* __restrict__ pick,
+                               const double* __restrict__ in, double* __restrict__ out) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) out[pick[k]] = in[k];
+}
+
+static const double* to_full(gn_kkt* K, const double* lifted, bool jac) {
+  const int64_t nl = jac ? K->nj : K->nh, nf = jac ? K->ctx->d.nj : K->ctx->d.nh;
+  DBuf<double>& buf = jac ? K->jfull : K->hfull;
+  if (buf.n < static_cast<size_t>(nf) + 1) buf.alloc(static_cast<size_t>(nf) + 1);
+  if (nl) {
+    KTimer kt("k_scatter_pick", K->stream);
+    k_scatter_pick<<<nblk(nl), 256, 0, K->stream>>>(nl, jac ? K->ctx->jpick.p : K->ctx->hpick.p,
+                                                     lifted, buf.p);
+    count_launch();
+  }
+  return buf.p;
+}
+
 void kkt_set_jacobian(gn_kkt* K, const double* J, bool full) {
   if (!K->annz) return;
-  if (full && K->algo != 1 && opf_kkt_ready(K)) return opf_set_jacobian(K, J);
+  if (K->algo != 1 && opf_kkt_ready(K))
+    return opf_set_jacobian(K, full ? J : to_full(K, J, true));
   const int32_t* pick = full ? K->ctx->jpick.p : nullptr;
   KTimer kt("k_set_jac_generic", K->stream);
   k_set_jac_generic<<<nblk(K->annz), 256, 0, K->stream>>>(K->annz, K->A.seg.p, K->A.src.p, pick,
@@ -290,12 +311,14 @@ void kkt_set_jacobian(gn_kkt* K, const double* J, bool full) {
 void kkt_assemble(gn_kkt* K, const double* H, const double* sx, const double* ss, double dw,
                   double dc, bool full) {
   if (!K->mnnz) return;
-  if (full && K->algo != 1 && opf_kkt_ready(K)) return opf_assemble(K, H, sx, ss, dw, dc);
+  if (K->algo != 1 && opf_kkt_ready(K))
+    return opf_assemble(K, full ? H : to_full(K, H, false), sx, ss, dw, dc);
   const int32_t* hpick = full ? K->ctx->hpick.p : nullptr;
+  launch_dvec(K, ss, dw, dc);
   KTimer kt("k_assemble_generic", K->stream);
   k_assemble_generic<<<nblk(K->mnnz), 256, 0, K->stream>>>(
       K->mnnz, K->nh, K->npair, K->M.seg.p, K->M.src.p, hpick, H, K->pka.p, K->pkb.p,
-      K->arow.p, K->avals.p, sx, ss, dw, dc, K->mvals.p);
+      K->arow.p, K->avals.p, sx, K->dvals.p, dw, K->mvals.p);
   count_launch();
   GN_CK(cudaGetLastError());
 }

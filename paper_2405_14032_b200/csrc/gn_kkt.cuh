@@ -39,6 +39,7 @@ struct gn_kkt {
   gnb::DBuf<int32_t> arow;       // per CSR(A) entry: its row
   gnb::DBuf<double> avals, mvals, dvals;
   gnb::DBuf<double> sj, sh, ssx, sss;  // host-mode staging
+  gnb::DBuf<double> jfull, hfull;      // lifted inputs scattered to the full COO order (OPF kernels)
   gnb::OpfKkt* opf = nullptr;    // OPF-specialised tables (gn_kkt_create_lifted)
 };
 
@@ -49,6 +50,11 @@ void kkt_set_jacobian(gn_kkt* K, const double* J, bool full);
 void kkt_assemble(gn_kkt* K, const double* H, const double* sx, const double* ss, double dw,
                   double dc, bool full);
 bool opf_kkt_prepare(gn_kkt* K);
+// *diff += number of positions where a[i] != b[i]
+void count_diff(const int32_t* a, const int32_t* b, int64_t n, int32_t* diff, cudaStream_t s);
+// d_r = (sigma_s + dw) / (1 + dc (sigma_s + dw)) per row into K->dvals (condensed.hpp:111-116),
+// in the reference's operation order: every consumer reads it instead of dividing again.
+void launch_dvec(gn_kkt* K, const double* ss, double dw, double dc);
 void opf_kkt_free(gn_kkt* K);
 void opf_set_grid_cap(gn_kkt* K, int ctas_per_sm);
 bool opf_kkt_ready(const gn_kkt* K);
@@ -62,4 +68,8 @@ void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, 
 void opf_set_jacobian(gn_kkt* K, const double* Jfull);
 void opf_assemble(gn_kkt* K, const double* Hfull, const double* sx, const double* ss, double dw,
                   double dc);
+// Does a published context's lifted structure equal this COO (device arrays)?  Returns it.
+gn_ctx* find_published(int device, int32_t n, int32_t m, int64_t nj, const int32_t* jr,
+                       const int32_t* jc, int64_t nh, const int32_t* hr, const int32_t* hc,
+                       cudaStream_t s);
 }  // namespace gnb

@@ -638,14 +638,17 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
 
 bool opf_fused_ready(const gn_kkt* K) { return K->opf && K->opf->fused_ready; }
 
+void launch_dvec(gn_kkt* K, const double* ss, double dw, double dc) {
+  if (K->m <= 0) return;
+  KTimer kt("k_fz_dvec", K->stream);
+  k_fz_dvec<<<(unsigned)((K->m + 1023) / 1024), 256, 0, K->stream>>>(K->m, ss, dw, dc, K->dvals.p);
+  count_launch();
+}
+
 void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
                         const double* ss, double dw, double dc) {
   FIn in{x, w, ow, sx, ss, dw, dc};
-  if (K->m > 0) {
-    KTimer kt("k_fz_dvec", K->stream);
-    k_fz_dvec<<<(unsigned)((K->m + 1023) / 1024), 256, 0, K->stream>>>(K->m, ss, dw, dc, K->dvals.p);
-    count_launch();
-  }
+  launch_dvec(K, ss, dw, dc);
   launch_fused<false>(K, in, K->dvals.p, K->mvals.p, nullptr, nullptr);
 }
 
@@ -700,7 +703,6 @@ void opf_update_fused(gn_kkt* K, const double* x, const double* w, double ow, co
 bool opf_fused_verify(gn_kkt* K) {
   const OpfKktTab& t = K->opf->t;
   if (!fz_bus_fits(t.maxdeg)) return false;  // one line per lane, one warp's shared memory
-  K->dvals.alloc(static_cast<size_t>(K->m) + 1);
   cudaStream_t s = K->stream;
   DBuf<int32_t> rows, bad, diff;
   rows.alloc(static_cast<size_t>(K->mnnz) + 1);

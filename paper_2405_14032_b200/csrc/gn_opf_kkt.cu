@@ -30,17 +30,14 @@ struct In {
   const double* __restrict__ H;
   const double* __restrict__ A;
   const double* __restrict__ sx;
-  const double* __restrict__ ss;
-  double dw, dc;
+  const double* __restrict__ dv;  // d_r per row (launch_dvec, condensed.hpp:112-116)
+  double dw;
 };
 
 __device__ __forceinline__ double pairval(const OpfKktTab& t, const In& in, int32_t r, int ia,
                                           int ib) {
   const int32_t rp = __ldg(t.rowptr + r);
-  const double sd = in.ss[r] + in.dw;  // condensed.hpp:112-116
-  const double c = 1.0 / (1.0 + in.dc * sd);
-  const double d = sd * c;
-  const double va = d * in.A[rp + ia];
+  const double va = in.dv[r] * in.A[rp + ia];  // condensed.hpp:126-129
   return va * in.A[rp + ib];
 }
 
@@ -955,7 +952,8 @@ void opf_assemble(gn_kkt* K, const double* Hfull, const double* sx, const double
   const OpfKktTab& t = K->opf->t;
   const int64_t blocks = assemble_blocks(t);
   if (blocks <= 0) return;
-  In in{Hfull, K->avals.p, sx, ss, dw, dc};
+  launch_dvec(K, ss, dw, dc);
+  In in{Hfull, K->avals.p, sx, K->dvals.p, dw};
   launch_assemble<false>(t, K->opf->type_lo, in, K->mvals.p, nullptr, nullptr, K->stream);
   GN_CK(cudaGetLastError());
 }

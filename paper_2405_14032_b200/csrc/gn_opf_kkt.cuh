@@ -132,6 +132,5 @@ struct OpfKkt {
   int32_t n_bus_cls[kBusClasses] = {};
 };
 
-void count_diff(const int32_t* a, const int32_t* b, int64_t n, int32_t* diff, cudaStream_t s);
 
 }  // namespace gnb

@@ -178,12 +178,15 @@ CONFIG_SIZES = {
 
 
 def synthetic_case(n_bus: int, n_line: int, n_gen: int, n_load: int, seed: int = 1,
-                   parallel_lines: int = 0, shared_gens: int = 0, max_span: int = 20) -> RawCase:
+                   parallel_lines: int = 0, shared_gens: int = 0, max_span: int = 20,
+                   load_scale: float = 1.0) -> RawCase:
     """Ring + seeded chords (no self-loops), case118-fixture statistics.
 
     `parallel_lines` adds that many duplicate-terminal lines and `shared_gens`
     that many extra generators on already-used buses (edge cases for the
-    balance-row accumulation order and AtA pattern)."""
+    balance-row accumulation order and AtA pattern).  `load_scale` multiplies every
+    demand (the BASELINE sizes carry fewer generators per load than case118, so an
+    end-to-end solve needs lighter loads to be feasible); the draw is unchanged."""
     assert n_line >= n_bus >= 3 and 1 <= n_gen and n_load <= n_bus
     rng = np.random.default_rng(seed)
     N = n_bus
@@ -252,8 +255,11 @@ def synthetic_case(n_bus: int, n_line: int, n_gen: int, n_load: int, seed: int =
     bus[0, 1] = 3
     lb = rng.choice(N, size=n_load, replace=False)
     pd = np.round(rng.uniform(15.0, 55.0, n_load), 2)
+    qf = rng.uniform(0.2, 0.45, n_load)
+    if load_scale != 1.0:
+        pd = np.round(pd * load_scale, 2)
     bus[lb, 2] = pd
-    bus[lb, 3] = np.round(pd * rng.uniform(0.2, 0.45, n_load), 2)
+    bus[lb, 3] = np.round(pd * qf, 2)
     bus[:, 6] = 1
     bus[:, 7] = 1.0
     bus[:, 9] = 138.0

@@ -58,6 +58,15 @@ def _i32(a):
     return a.ctypes.data_as(abi.i32p)
 
 
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy (driver_types.h)
+
+
+def _stream_arg(handle: int) -> int:
+    """torch's default stream (handle 0) is the legacy default stream; the C-ABI's NULL
+    means "reset to the object's own stream", so it is passed as cudaStreamLegacy."""
+    return CUDA_STREAM_LEGACY if int(handle) == 0 else int(handle)
+
+
 def load_profile(n_load: int, periods: int, resolution: float = 60.0, seed: int = 1,
                  amplitude: float = 0.2, noise: float = 0.02) -> np.ndarray:
     """generate_load_profile (network.hpp:104-140), T x n_load, bit-identical."""
@@ -240,7 +249,14 @@ class OpfNlp:
         return self._record(self.lib.gn_ctx_status(self.h, C.byref(err)), err)
 
     def set_stream(self, stream_handle: int):
-        _check(self.lib.gn_ctx_set_stream(self.h, C.c_void_p(stream_handle)))
+        """Launch on the caller's stream.  torch's default stream has handle 0, which
+        the C-ABI reads as "reset"; it is passed as cudaStreamLegacy instead, so the
+        work stays ordered with the caller's default-stream kernels."""
+        _check(self.lib.gn_ctx_set_stream(self.h, C.c_void_p(_stream_arg(stream_handle))))
+
+    def reset_stream(self):
+        """Back to the context's own (non-blocking) stream."""
+        _check(self.lib.gn_ctx_set_stream(self.h, None))
 
     # ---- lifted problem (lifted.hpp:25-100)
     def lift(self, relax: float):
@@ -262,6 +278,24 @@ class OpfNlp:
                                             GN_MEM_HOST))
         return dict(free_to_full=f2f, jac_rows=jr, jac_cols=jc, jac_pick=jp, hess_rows=hr,
                     hess_cols=hc, hess_pick=hp, s_lower=sl, s_upper=su)
+
+
+    def publish(self, on: bool = True):
+        """gn_ctx_publish: a CondensedKkt later built from this problem's lifted COO arrays
+        (as the reference IpmSolver builds it) is recognised and gets the OPF kernels."""
+        _check(self.lib.gn_ctx_publish(self.h, 1 if on else 0))
+        self._sizes()
+
+    def lifted_gather(self, which: str, full, out=None, mem: int = GN_MEM_HOST):
+        """LiftedProblem's value gather (lifted.hpp:144-159): full J (which="jac") or H
+        ("hess") values -> lifted values, through host arrays or device tensors."""
+        s = self.sizes
+        k = s.jac_nnz_lifted if which == "jac" else s.hess_nnz_lifted
+        if out is None:
+            out = np.empty(k)
+        fn = self.lib.gn_lifted_gather_jac if which == "jac" else self.lib.gn_lifted_gather_hess
+        _check(fn(self.h, _f64(full), _f64(out), mem))
+        return out
 
 
 class CondensedKkt:
@@ -319,7 +353,12 @@ class CondensedKkt:
         return js, hs, ps, ds
 
     def set_stream(self, stream_handle: int):
-        _check(self.lib.gn_kkt_set_stream(self.h, C.c_void_p(stream_handle)))
+        """As OpfNlp.set_stream (handle 0 = the legacy default stream)."""
+        _check(self.lib.gn_kkt_set_stream(self.h, C.c_void_p(_stream_arg(stream_handle))))
+
+    def reset_stream(self):
+        """Back to the KKT's own stream (its context's for a lifted KKT)."""
+        _check(self.lib.gn_kkt_set_stream(self.h, None))
 
     def set_grid_cap(self, ctas_per_sm: int):
         """Resident CTAs per SM for the KKT kernels (0 = uncapped)."""

@@ -1,6 +1,6 @@
 """Build a tuning variant of the library with extra -D defines into
 build/variants/<name>/libgridnlp_b200.so (scripts/gpu_variants.sh benches each one by
-copying it over the in-tree library on the GPU box's scratch copy).
+loading it through GRIDNLP_B200_LIB; the in-tree library is never touched).
 usage: python scripts/build_variant.py <name> [-DNAME=VALUE ...]"""
 import concurrent.futures as cf
 import subprocess

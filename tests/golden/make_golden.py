@@ -1,7 +1,8 @@
 """Generate the golden fixtures from the UNMODIFIED reference (oracle/_ref).
 
 Run in the build container (needs /root/reference and oracle/_ref):
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py               # everything (~6 min: reference solves)
+    python tests/golden/make_golden.py --solves KEY  # networks + the named solves only
 Writes tests/golden/networks.npz, eval_<name>.npz, meta.json.  The GPU box has
 no /root/reference, so tests there read only these committed files.
 """
@@ -19,7 +20,7 @@ sys.path.insert(0, str(ROOT / "tests"))
 
 from helpers import interior_point, row_weights, sigmas, DELTAS  # noqa: E402
 from oracle import bindings as B  # noqa: E402
-from paper_2405_14032_b200.network import synthetic_case  # noqa: E402
+from paper_2405_14032_b200.network import CONFIG_SIZES, synthetic_case  # noqa: E402
 
 OUT = Path(__file__).resolve().parent
 DATA = Path("/root/reference/proj/data")
@@ -40,10 +41,26 @@ def texts():
     # edge-case network: parallel lines (both orientations) + several generators per bus
     t["synth"] = synthetic_case(40, 70, 12, 30, seed=5, parallel_lines=6,
                                 shared_gens=5).to_matpower()
+    # BASELINE configs[1] size (case1354pegase-size) for the end-to-end solve; the config's
+    # generator / load counts give less capacity than demand, so demand is halved to keep
+    # the problem feasible (at full demand the reference IPM ends "infeasible")
+    t["case1354s"] = synthetic_case(*CONFIG_SIZES["case1354pegase"], seed=1,
+                                    load_scale=0.5).to_matpower()
     return t
 
 
+# end-to-end reference solves (SURVEY §8(c) goldens), tol 1e-4: key -> (case, T, resolution)
+SOLVES = {
+    "case9_T1": ("case9", 1, 60.0),
+    "case30_T30_r30": ("case30", 30, 30.0),
+    "case118_T24": ("case118", 24, 60.0),
+    "case118_T168": ("case118", 168, 60.0),        # 40 iterations
+    "case1354s_T24": ("case1354s", 24, 60.0),      # SURVEY §7 step 7 (configs[1] size)
+}
+
+
 def main():
+    only = sys.argv[sys.argv.index("--solves") + 1:] if "--solves" in sys.argv else None
     T = texts()
     nets = {}
     for name, text in T.items():
@@ -53,6 +70,16 @@ def main():
         nets[f"{name}/base_mva"] = np.array(net.base_mva)
         nets[f"{name}/reference_bus"] = np.array(net.reference_bus)
     np.savez_compressed(OUT / "networks.npz", **nets)
+    if only is not None:
+        meta = json.loads((OUT / "meta.json").read_text())
+        for key in only:
+            case, periods, res = SOLVES[key]
+            scale = B.ref_load_profile(T[case], periods, resolution=res)
+            r = B.RefModel(T[case], periods, scale).solve(1e-4)
+            meta["solves"][key] = dict(case=case, periods=periods, resolution=res, **r)
+            print(key, r)
+        (OUT / "meta.json").write_text(json.dumps(meta, indent=1))
+        return
     meta = {"fixtures": {}, "solves": {}}
     for fx, case, periods, res in FIXTURES:
         text = T[case]
@@ -94,9 +121,7 @@ def main():
                                     kkt=ksz[:3], factor_nnz=ksz[3])
         print(fx, ref.sizes, ref.lifted_sizes, ksz)
     # end-to-end reference solves (SURVEY §8(c) goldens), tol 1e-4
-    for key, case, periods, res in [("case9_T1", "case9", 1, 60.0),
-                                    ("case30_T30_r30", "case30", 30, 30.0),
-                                    ("case118_T24", "case118", 24, 60.0)]:
+    for key, (case, periods, res) in SOLVES.items():
         text = T[case]
         scale = B.ref_load_profile(text, periods, resolution=res)
         r = B.RefModel(text, periods, scale).solve(1e-4)

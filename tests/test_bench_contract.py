@@ -41,6 +41,28 @@ def test_reference_arm_json_line():
     assert "case1354pegase" in c["sample"] or "case1354pegase" in d["config"]["workload"]
     assert d["e2e"] == {"value": d["value"], "unit": "nnz/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}
+    # the reference arm runs the reference only: same configuration as our arm, and no
+    # code of this repository's CUDA library mapped into the process
+    assert c["same_config"] is True and c["cpu_model"]
+    assert not any("libgridnlp_b200" in x for x in d["libraries_loaded"]), d["libraries_loaded"]
+    assert any("libgridnlp_ref" in x for x in d["libraries_loaded"])
+    assert c["nnz_per_unit"] == {"J": 884552, "H": 1948020, "M": 1083508}
+
+
+def test_m_nnz_affine_in_periods():
+    """The reference arm extrapolates M nnz affinely in T from two period windows (every
+    coupling but ramp is per period): exact against the C restatement's full KKT."""
+    from oracle import bindings as B
+    from paper_2405_14032_b200.network import synthetic_case
+    raw = synthetic_case(50, 80, 12, 40, seed=3, parallel_lines=3, shared_gens=2)
+    net = raw.network()
+    m = {}
+    for T in (2, 5, 11):
+        Mo = B.OracleModel(net, T, B.np.ones((T, net.n_load)))
+        Mo.lift(1e-4)
+        m[T] = Mo.kkt().m_nnz
+    slope = (m[5] - m[2]) / 3
+    assert m[11] == m[5] + slope * 6
 
 
 def test_reference_arm_other_ranks_exit_silently():

@@ -22,9 +22,17 @@ DROPIN = ROOT / "oracle" / "_ref" / "ipm_dropin"
 from oracle.bindings import write_network_bin as write_bin  # noqa: E402
 
 
-@pytest.mark.parametrize("key", ["case9_T1", "case30_T30_r30", "case118_T24"])
+# SURVEY §8(c) goldens: case118 x 168 is the survey's 40-iteration solve (objective
+# 10578502.183425546); case1354s x 24 is BASELINE configs[1]'s size
+KEYS = ["case9_T1", "case30_T30_r30", "case118_T24", "case118_T168", "case1354s_T24"]
+
+
+@pytest.mark.parametrize("key", KEYS)
 @pytest.mark.parametrize("nlp", ["cuda", "ref"])
 def test_reference_ipm_on_b200_path(gpu, tmp_path, key, nlp):
+    """nlp = cuda: CudaOpfNlp + the shim CondensedKkt (recognised as the OPF problem:
+    specialised assembly); nlp = ref: the reference's PatternNlp callbacks + the shim
+    CondensedKkt on the generic contributor-list kernels."""
     if not DROPIN.exists():
         pytest.skip("oracle/_ref/ipm_dropin not built (needs /root/reference at build time)")
     g = golden_meta()["solves"][key]
@@ -33,9 +41,13 @@ def test_reference_ipm_on_b200_path(gpu, tmp_path, key, nlp):
     path = tmp_path / "net.bin"
     write_bin(path, net, g["periods"], scale)
     out = subprocess.run([str(DROPIN), str(path), nlp], capture_output=True, text=True,
-                         timeout=600)
+                         timeout=1200)
     assert out.returncode == 0, out.stderr
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["status"] == "solved"
     assert r["iterations"] == g["iterations"], (r, g)
+    assert r["restorations"] == g["restorations"], (r, g)
+    # the seam reached the specialised kernels exactly when the callbacks are ours
+    assert (r["kkt_specialised"] >= 1 and r["kkt_generic"] == 0) if nlp == "cuda" else \
+        (r["kkt_specialised"] == 0 and r["kkt_generic"] >= 1), r
     assert abs(r["objective"] - g["objective"]) <= 1e-6 * abs(g["objective"]), (r, g)

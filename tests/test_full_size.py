@@ -1,17 +1,28 @@
-"""GPU: parity at the bench's full size (synthetic30k x 96 periods), through properties
-that do not need a full-size CPU run:
+"""GPU: parity at every BASELINE.json configuration as named (configs[1]-[4]), against the
+UNMODIFIED reference (oracle/_ref) -- VERDICT r1 "what's missing" #2.
 
-* period locality -- every pattern except ramp is per-period, so the callbacks of the
-  96-period problem restricted to a window of 2 periods equal the reference's own
-  2-period problem on the same network and load slice (ramp rows inside the window
-  included).  g, grad, J and H are compared entry by entry (J/H through their COO
-  (row, col) keys mapped into the window problem);
-* path identity -- the fused A/M (straight from x) equal set_jacobian(eval_jac(x)) /
-  assemble(eval_hess(x)) bit for bit at full size;
-* shard identity -- a period shard of the full problem reproduces its rows bit for bit
-  (tests/test_shard.py does this exhaustively at small sizes).
+The reference cannot run the 13659 x 168 or 30k x 96 problems' condensed KKT (its ctor
+runs AMD + a symbolic LDL^T), so parity is taken on *period windows*, which is exact
+because every pattern except ramp is per period (opf.hpp:236-351):
 
-Tolerance for values: 1e-12 relative / 1e-14 absolute (CUDA vs glibc sin/cos ulps)."""
+* window problem = the reference's own TW-period problem on the same network and the
+  load-profile rows [T0, T0 + TW).  Its COO structure must equal, entry for entry and IN
+  ORDER, the full problem's records of those periods (ramp records: steps T0+1 ..
+  T0+TW-1), mapped into the window's numbering -- a bit-exact structural check of
+  `freeze` (pattern_model.hpp:158-207) at the full configuration;
+* callbacks: the full problem's f-free outputs (g, grad, J, H) on those records equal the
+  reference's window callbacks at the window slice of x within 1e-12 rel / 1e-14 abs
+  (CUDA vs glibc sin/cos ulps; BASELINE north_star);
+* condensed KKT: the reference `CondensedKkt` of the window (condensed.hpp:29-135), fed
+  the window slice of OUR full-problem J/H values (identical doubles), equals our full
+  A rows and M columns BIT FOR BIT -- for the contract path (set_jacobian/assemble of
+  the callback outputs) and the fused path (straight from x) -- on every column except
+  the pg columns of ramping generators at a window edge inside the horizon (the full
+  problem couples those to a period outside the window through a ramp row).
+
+A window of the whole horizon (T0 = 0, TW = T) is the full problem: configs[1]
+(1354 x 24) and configs[2] (9241 x 48) are checked that way, whole.
+"""
 import numpy as np
 import pytest
 
@@ -23,28 +34,25 @@ from paper_2405_14032_b200.opf import CondensedKkt, OpfNlp, load_profile
 
 pytestmark = pytest.mark.gpu
 
-T, T0, TW = 96, 40, 2  # full horizon, window start, window length
+# BASELINE.json configs[1..4] and their windows (T0, TW)
+CONFIGS = {
+    "case1354pegase": (24, [(0, 24)]),
+    "case9241pegase": (48, [(0, 48), (20, 3)]),
+    "case13659pegase": (168, [(0, 3), (80, 3), (165, 3)]),
+    "synthetic30k": (96, [(0, 3), (40, 3), (93, 3)]),
+}
+CASES = [(c, w) for c, (_, ws) in CONFIGS.items() for w in ws]
 
 
-@pytest.fixture(scope="module")
-def full():
-    raw = config_case("synthetic30k")
-    net = raw.network()
-    scale = load_profile(net.n_load, T)
-    nlp = OpfNlp(net, T, scale)
-    xl, xu, xs, _, _ = nlp.bounds()
-    x = interior_point(xl, xu, xs, 99)
-    w = row_weights(nlp.n_cons(), 98, zero_every=11)
-    return dict(raw=raw, net=net, scale=scale, nlp=nlp, x=x, w=w)
-
-
-class _Layout:
-    """Row / variable (entity, period) decomposition of the OPF layout (opf.hpp:16-60)."""
+class Layout:
+    """Row / variable (block, entity, period) decomposition (OpfLayout, opf.hpp:16-60)."""
 
     def __init__(self, N, L, G, LT, GR, T):
         self.T = T
         self.voff = np.cumsum([0, G * T, G * T, L * T, L * T, N * T, N * T])
         self.roff = np.cumsum([0, N * T, N * T, L * T, L * T, LT * T, L * T, GR * max(T - 1, 0)])
+        # Hessian slot range of the ramp pattern (SURVEY A.2: last pattern, 3 slots/record)
+        self.h_ramp0 = 3 * G * T + 37 * L * T + 3 * LT * T
 
     def var(self, v):
         b = np.searchsorted(self.voff, v, side="right") - 1
@@ -52,13 +60,12 @@ class _Layout:
         return b, r // self.T, r % self.T
 
     def row(self, r):
+        """(block, entity, period); ramp rows (block 6): the step s (pg_s - pg_{s-1})."""
         b = np.searchsorted(self.roff, r, side="right") - 1
         q = r - self.roff[b]
         ramp = b == 6
         Tm = max(self.T - 1, 1)
-        e = np.where(ramp, q // Tm, q // self.T)
-        t = np.where(ramp, q % Tm + 1, q % self.T)  # ramp: the step s (rows pg_s - pg_{s-1})
-        return b, e, t
+        return b, np.where(ramp, q // Tm, q // self.T), np.where(ramp, q % Tm + 1, q % self.T)
 
     def var_index(self, b, e, t):
         return self.voff[b] + e * self.T + t
@@ -69,99 +76,186 @@ class _Layout:
                         self.roff[b] + e * self.T + t)
 
 
-def _window(full):
-    net, s = full["net"], full["nlp"].sizes
-    N, L, G = net.n_bus, net.n_line, net.n_gen
-    LT, GR = s.n_thermal, s.n_ramp_gens
-    big, small = _Layout(N, L, G, LT, GR, T), _Layout(N, L, G, LT, GR, TW)
-    text = full["raw"].to_matpower()
-    ref = B.RefModel(text, TW, full["scale"][T0:T0 + TW])
-    # window x: every variable block, periods [T0, T0 + TW)
-    vb, ve, vt = small.var(np.arange(ref.sizes[0]))
-    xw = full["x"][big.var_index(vb, ve, vt + T0)]
-    rb, re_, rt = small.row(np.arange(ref.sizes[1]))
-    wrow = big.row_index(rb, re_, rt + T0)
-    return big, small, ref, xw, wrow
+def build_full(cfg, raw, T, backend="gpu"):
+    """The full problem at x, w, Sigma: callbacks, structures, contract (and fused) KKT.
+    backend "gpu": this repository's CUDA path; "oracle": the C restatement (CPU test of
+    the window machinery itself)."""
+    net = raw.network()
+    scale = load_profile(net.n_load, T) if backend == "gpu" else B.ref_load_profile(
+        raw.to_matpower(), T)
+    P = OpfNlp(net, T, scale) if backend == "gpu" else B.OracleModel(net, T, scale)
+    n, m = (P.n_vars(), P.n_cons()) if backend == "gpu" else P.sizes[:2]
+    xl, xu, xs, _, _ = P.bounds()
+    x = interior_point(xl, xu, xs, 99)
+    w = row_weights(m, 98, zero_every=11)
+    del xl, xu, xs
+    ok = [P.eval_g(x), P.eval_grad(x), P.eval_jac(x), P.eval_hess(x, w, 0.8)]
+    assert all(o[0] for o in ok)
+    g, grad, J, H = (o[1] for o in ok)
+    kkt = {}
+    if backend == "gpu":
+        jr, jc = P.jac_structure()
+        hr, hc = P.hess_structure()
+        P.lift(1e-4)
+        f2f = P.lifted_structure()["free_to_full"]
+        n_free, LT, GR = P.sizes.n_free, P.sizes.n_thermal, P.sizes.n_ramp_gens
+        K = CondensedKkt(nlp=P)
+        assert K.fused_ready == 1
+        sx, ss = sigmas(n_free, m, 97)
+        rp, ci, cp, ri = K.structure()
+        for i, (dw, dc) in enumerate(DELTAS):
+            K.set_jacobian(J, mem=GN_IN_FULL)
+            K.assemble(H, sx, ss, dw, dc, mem=GN_IN_FULL)
+            a_c, m_c = K.values()
+            K.update_x(x, w, 0.8, sx, ss, dw, dc)
+            a_f, m_f = K.values()
+            assert_bitexact(a_f, a_c, f"{cfg}: fused A vs contract A, dw={dw}")
+            assert_bitexact(m_f, m_c, f"{cfg}: fused M vs contract M, dw={dw}")
+            kkt[i] = (a_c, m_c)
+        K.close()
+        P.close()
+    else:
+        jr, jc, hr, hc = P.structure()
+        lift = P.lift(1e-4)
+        f2f = lift["free_to_full"]
+        n_free, LT, GR = len(f2f), P.sizes[4], P.sizes[5]
+        K = P.kkt()
+        sx, ss = sigmas(n_free, m, 97)
+        rp, ci, cp, ri = K.structure()
+        K.set_jacobian(J[lift["jac_pick"]])
+        for i, (dw, dc) in enumerate(DELTAS):
+            K.assemble(H[lift["hess_pick"]], sx, ss, dw, dc)
+            kkt[i] = K.values()
+    lay = Layout(net.n_bus, net.n_line, net.n_gen, LT, GR, T)
+    inv = np.full(n, -1, np.int64)
+    inv[f2f] = np.arange(len(f2f))
+    mcol = np.repeat(np.arange(len(cp) - 1, dtype=np.int64), np.diff(cp))
+    return dict(cfg=cfg, T=T, raw=raw, net=net, scale=scale, x=x, w=w, g=g, grad=grad, J=J,
+                H=H, jr=jr, jc=jc, hr=hr, hc=hc, lay=lay, inv=inv, n_free=n_free, sx=sx,
+                ss=ss, rp=rp, ci=ci, mkey=mcol * n_free + ri, kkt=kkt)
 
 
-def _coo_window(big, small, rows, cols, vals, nvars_small):
-    """Entries of the full COO whose row lies in the window, keyed in the window problem."""
-    r = rows.astype(np.int64)
-    ramp = r >= big.roff[6]
-    t = np.where(ramp, (r - big.roff[6]) % max(T - 1, 1) + 1, r % T)
-    keep = np.flatnonzero((t >= T0) & (t < T0 + TW) & (~ramp | (t > T0)))  # ramp: steps T0+1..
-    rb, re_, rt = big.row(r[keep])
-    rt = rt - T0
-    cb, ce, ct = big.var(cols[keep].astype(np.int64))
-    assert np.all((ct >= T0) & (ct < T0 + TW)), "a window row references a period outside it"
-    vals = vals[keep]
-    key = small.row_index(rb, re_, rt) * nvars_small + small.var_index(cb, ce, ct - T0)
-    return key, vals
+@pytest.fixture(scope="module")
+def full(request, gpu):
+    """Our full problem on the GPU at the BASELINE configuration."""
+    cfg = request.param
+    return build_full(cfg, config_case(cfg), CONFIGS[cfg][0])
 
 
-def _summed(key, vals):
-    o = np.argsort(key, kind="stable")
-    key, vals = key[o], vals[o]
-    u, start = np.unique(key, return_index=True)
-    return u, np.add.reduceat(vals, start) if len(vals) else vals
+def _window(F, T0, TW):
+    """The reference's TW-period problem and the maps from its numbering into ours."""
+    T, big, net = F["T"], F["lay"], F["net"]
+    ref = B.RefModel(F["raw"].to_matpower(), TW, F["scale"][T0:T0 + TW])
+    n_w, m_w = ref.sizes[0], ref.sizes[1]
+    s = Layout(net.n_bus, net.n_line, net.n_gen, ref.sizes[4], ref.sizes[5], TW)
+    vb, ve, vt = s.var(np.arange(n_w))
+    vmap = big.var_index(vb, ve, vt + T0)            # window var -> full var
+    rb, re_, rt = s.row(np.arange(m_w))
+    rmap = big.row_index(rb, re_, rt + T0)           # window row -> full row
+
+    def in_window_rows(rows):
+        b, _, t = big.row(rows.astype(np.int64))
+        return np.where(b == 6, (t > T0) & (t < T0 + TW), (t >= T0) & (t < T0 + TW))
+
+    jk = np.flatnonzero(in_window_rows(F["jr"]))     # full J entries of the window, in order
+    h0 = big.h_ramp0
+    tper = F["hr"][:h0] % T                          # block offsets are multiples of T
+    step = np.arange(len(F["hr"]) - h0) // 3 % max(T - 1, 1) + 1
+    hk = np.concatenate([np.flatnonzero((tper >= T0) & (tper < T0 + TW)),
+                         h0 + np.flatnonzero((step > T0) & (step < T0 + TW))])
+    return ref, s, vmap, rmap, jk, hk
 
 
-def test_period_locality_callbacks(full):
-    nlp = full["nlp"]
-    big, small, ref, xw, wrow = _window(full)
-    ok, g = nlp.eval_g(full["x"])
-    okr, gr, _ = ref.eval_g(xw)
-    assert ok and okr
-    assert_close(g[wrow], gr, what="g window")
-    ok, grad = nlp.eval_grad(full["x"])
-    okr, gradr, _ = ref.eval_grad(xw)
-    vb, ve, vt = small.var(np.arange(ref.sizes[0]))
-    assert_bitexact(grad[big.var_index(vb, ve, vt + T0)], gradr, "grad window")
-    jr, jc = nlp.jac_structure()
-    hr, hc = nlp.hess_structure()
+def _to_window(idx_full, vmap):
+    """full var index -> window var index (vmap is increasing)."""
+    pos = np.searchsorted(vmap, idx_full)
+    assert np.all(vmap[np.minimum(pos, len(vmap) - 1)] == idx_full), "entry outside the window"
+    return pos
+
+
+IDS = [f"{c}-T0={w[0]}-TW={w[1]}" for c, w in CASES]
+
+
+@pytest.mark.parametrize("full,win", CASES, ids=IDS, indirect=["full"])
+def test_window_structure_and_callbacks(full, win):
+    check_window_callbacks(full, *win)
+
+
+@pytest.mark.parametrize("full,win", CASES, ids=IDS, indirect=["full"])
+def test_window_condensed_kkt_bitexact(full, win):
+    check_window_kkt(full, *win)
+
+
+def check_window_callbacks(F, T0, TW):
+    cfg = F["cfg"]
+    ref, s, vmap, rmap, jk, hk = _window(F, T0, TW)
     rjr, rjc, rhr, rhc = ref.structure()
-    nvs = ref.sizes[0]
-    ok, J = nlp.eval_jac(full["x"])
-    okr, Jr, _ = ref.eval_jac(xw)
-    assert ok and okr
-    k, v = _coo_window(big, small, jr, jc, J, nvs)
-    u, s_ = _summed(k, v)
-    ur, sr = _summed(rjr.astype(np.int64) * nvs + rjc, Jr)
-    assert np.array_equal(u, ur), "J window pattern"
-    assert_close(s_, sr, what="J window")
-    wv = full["w"]
-    ok, H = nlp.eval_hess(full["x"], wv, 0.8)
-    okr, Hr, _ = ref.eval_hess(xw, wv[wrow], 0.8)
-    assert ok and okr
-    # H entries whose two variables both lie in the window (every variable block's offset
-    # is a multiple of T, so the period is the index mod T).  Entries across the window
-    # edge come only from ramp steps outside it; ramp Hessians are zero, so the summed
-    # values of the kept keys are the window problem's.
-    keep = np.flatnonzero(((hr % T) >= T0) & ((hr % T) < T0 + TW) &
-                          ((hc % T) >= T0) & ((hc % T) < T0 + TW))
-    rb, re_, rt = big.var(hr[keep].astype(np.int64))
-    cb, ce, ct = big.var(hc[keep].astype(np.int64))
-    key = small.var_index(rb, re_, rt - T0) * nvs + small.var_index(cb, ce, ct - T0)
-    u, s_ = _summed(key, H[keep])
-    ur, sr = _summed(rhr.astype(np.int64) * nvs + rhc, Hr)
-    assert np.array_equal(u, ur), "H window pattern"
-    assert_close(s_, sr, what="H window")
+    # structure: our records of the window, mapped, are the reference's freeze order
+    rows_w = np.searchsorted(rmap, F["jr"][jk])
+    assert np.array_equal(rmap[rows_w], F["jr"][jk])
+    assert_bitexact(rows_w.astype(np.int32), rjr, f"{cfg} window J rows")
+    assert_bitexact(_to_window(F["jc"][jk], vmap).astype(np.int32), rjc, f"{cfg} window J cols")
+    assert_bitexact(_to_window(F["hr"][hk], vmap).astype(np.int32), rhr, f"{cfg} window H rows")
+    assert_bitexact(_to_window(F["hc"][hk], vmap).astype(np.int32), rhc, f"{cfg} window H cols")
+    # callback values at the window slice of x
+    xw = F["x"][vmap]
+    ww = F["w"][rmap]
+    res = [ref.eval_g(xw), ref.eval_grad(xw), ref.eval_jac(xw), ref.eval_hess(xw, ww, 0.8)]
+    assert all(r[0] for r in res)
+    assert_close(F["g"][rmap], res[0][1], what=f"{cfg} window g")
+    assert_bitexact(F["grad"][vmap], res[1][1], f"{cfg} window grad")
+    assert_close(F["J"][jk], res[2][1], what=f"{cfg} window J")
+    assert_close(F["H"][hk], res[3][1], what=f"{cfg} window H")
 
 
-def test_fused_equals_contract_full_size(full):
-    nlp = full["nlp"]
-    nlp.lift(1e-4)
-    K = CondensedKkt(nlp=nlp)
-    assert K.fused_ready == 1
-    sx, ss = sigmas(nlp.sizes.n_free, nlp.n_cons(), 97)
-    ok, jv = nlp.eval_jac(full["x"])
-    ok2, hv = nlp.eval_hess(full["x"], full["w"], 1.0)
-    assert ok and ok2
-    for dw, dc in DELTAS:
-        K.set_jacobian(jv, mem=GN_IN_FULL)
-        K.assemble(hv, sx, ss, dw, dc, mem=GN_IN_FULL)
-        a_ref, m_ref = K.values()
-        K.update_x(full["x"], full["w"], 1.0, sx, ss, dw, dc)
-        a, m = K.values()
-        assert_bitexact(a, a_ref, f"A full size dw={dw}")
-        assert_bitexact(m, m_ref, f"M full size dw={dw}")
+def check_window_kkt(F, T0, TW):
+    cfg = F["cfg"]
+    T = F["T"]
+    ref, s, vmap, rmap, jk, hk = _window(F, T0, TW)
+    xl, xu, _, _, _ = ref.bounds()
+    free = xl != xu                                   # lifted.hpp:33-42
+    lift = ref.lift(1e-4)
+    f2f_w = lift["free_to_full"]
+    assert np.array_equal(f2f_w, np.flatnonzero(free))
+    jc_w = _to_window(F["jc"][jk], vmap)
+    jpick = np.flatnonzero(free[jc_w])
+    hr_w, hc_w = _to_window(F["hr"][hk], vmap), _to_window(F["hc"][hk], vmap)
+    hpick = np.flatnonzero(free[hr_w] & free[hc_w])
+    assert len(jpick) == len(lift["jac_rows"]) and len(hpick) == len(lift["hess_rows"])
+    lmap = F["inv"][vmap[f2f_w]]                      # window lifted var -> our lifted var
+    assert np.all(lmap >= 0) and np.all(np.diff(lmap) > 0)
+    ref.kkt_create()
+    rp, ci, cp, ri = ref.kkt_structure()
+    sx_w, ss_w = F["sx"][lmap], F["ss"][rmap]
+    ref.kkt_set_jacobian(F["J"][jk][jpick])
+    # columns to compare: all but the pg columns of ramping generators at an inner window edge
+    nl = len(f2f_w)
+    fb, fe, ft = s.var(f2f_w)
+    ramping = np.zeros(F["net"].n_gen, bool)
+    ramping[np.isfinite(F["net"].gen_ramp)] = True
+    edge = (fb == 0) & ramping[np.where(fb == 0, fe, 0)] & (
+        ((ft == 0) & (T0 > 0)) | ((ft == TW - 1) & (T0 + TW < T)))
+    cols = np.flatnonzero(~edge)
+    ccount = np.diff(cp)
+    wcol = np.repeat(np.arange(nl, dtype=np.int64), ccount)
+    keep = ~edge[wcol]
+    keys = lmap[wcol[keep]] * F["n_free"] + lmap[ri[keep].astype(np.int64)]
+    pos = np.searchsorted(F["mkey"], keys)
+    assert np.array_equal(F["mkey"][np.minimum(pos, len(F["mkey"]) - 1)], keys), \
+        f"{cfg}: a window M slot is missing from the full pattern"
+    # the full columns hold no extra slots
+    fullcount = np.diff(np.searchsorted(F["mkey"], np.stack([lmap[cols] * F["n_free"],
+                                                             (lmap[cols] + 1) * F["n_free"]])),
+                        axis=0)[0]
+    assert np.array_equal(fullcount, ccount[cols]), f"{cfg}: column slot counts"
+    # A rows of the window (all rows: the window has no edge rows)
+    arow_w = np.repeat(np.arange(len(rp) - 1), np.diff(rp))
+    fr = rmap[arow_w]
+    astart = F["rp"][fr] + (np.arange(len(ci)) - rp[arow_w])
+    assert np.array_equal(F["ci"][astart], lmap[ci]), f"{cfg}: CSR(A) columns"
+    for i, (dw, dc) in enumerate(DELTAS):
+        ref.kkt_assemble(F["H"][hk][hpick], sx_w, ss_w, dw, dc)
+        a_w, m_w = ref.kkt_values()
+        a_full, m_full = F["kkt"][i]
+        assert_bitexact(a_full[astart], a_w, f"{cfg} window A dw={dw}")
+        assert_bitexact(m_full[pos], m_w[keep], f"{cfg} window M dw={dw} (contract = fused)")
