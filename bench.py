@@ -127,13 +127,24 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ workload
-def build_workload(rank: int, world: int, periods: int, config: str):
+def shard_of(rank: int, world: int, periods: int, strong: bool):
+    """(T_total, first period, periods) of this rank: weak scaling = `periods` per rank of a
+    world * periods horizon; strong = a `periods` horizon partitioned over the ranks."""
+    if not strong:
+        return periods * world, periods * rank, periods
+    from paper_2405_14032_b200.shard import partition
+    t0, T = partition(periods, world)[rank]
+    return periods, t0, T
+
+
+def build_workload(rank: int, world: int, periods: int, config: str, strong: bool = False):
     from paper_2405_14032_b200.network import config_case
     from paper_2405_14032_b200.opf import load_profile
     raw = config_case(config, seed=1)
     net = raw.network()
-    scale = load_profile(net.n_load, periods * world, seed=1)
-    return raw, net, np.ascontiguousarray(scale[rank * periods:(rank + 1) * periods])
+    T_total, first, T = shard_of(rank, world, periods, strong)
+    scale = load_profile(net.n_load, T_total, seed=1)
+    return raw, net, np.ascontiguousarray(scale[first:first + T])
 
 
 def alg_bytes(s, kkt):
@@ -364,11 +375,11 @@ def run_ours(args, rank, world, local_rank, dist):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    raw, net, scale = build_workload(rank, world, args.periods, args.config)
-    T_total, first = args.periods * world, args.periods * rank
+    raw, net, scale = build_workload(rank, world, args.periods, args.config, args.strong)
+    T_total, first, T_rank = shard_of(rank, world, args.periods, args.strong)
     t0 = time.time()
-    # period shard [first, first + periods) of the T_total horizon (world == 1: the whole horizon)
-    nlp = OpfNlp(net, args.periods, scale, device=local_rank, shard=(T_total, first))
+    # period shard [first, first + T_rank) of the T_total horizon (world == 1: the whole horizon)
+    nlp = OpfNlp(net, T_rank, scale, device=local_rank, shard=(T_total, first))
     stream = torch.cuda.Stream(device=dev, priority=int(os.environ.get("GN_CB_PRIORITY", "0")))
     nlp.set_stream(stream.cuda_stream)
     nlp.lift(1e-4)
@@ -407,18 +418,28 @@ def run_ours(args, rank, world, local_rank, dist):
         raise SystemExit("period shards run the fused KKT path")
 
     # ---- ramp halo: boundary set-points forward/backward, the
-    # sigma_s of the boundary ramp rows backward; G doubles each, over NCCL.
-    halo = None
+    # sigma_s of the boundary ramp rows backward (G doubles each) and the objective
+    # partials.  --halo peer (default): gn_halo, the neighbours store straight into this
+    # GPU's memory over NVLink / NVSwitch, one kernel per exchange, capturable in the
+    # step's CUDA graph; --halo nccl: torch.distributed point-to-point (eager only).
+    halo = peer = None
     if world > 1:
-        from paper_2405_14032_b200.shard import ShardMap
-        info = nlp.shard_info()
-        mp_ = ShardMap(net.n_bus, net.n_line, net.n_gen, s.n_thermal, info["ramp_gens"],
-                       T_total, first, args.periods)
-        halo = mp_.halo_plan(dev)
+        from paper_2405_14032_b200.shard import DeviceHalo, ShardMap
+        if args.halo == "peer":
+            peer = DeviceHalo(nlp, rank, world)
+            peer.connect()
+        else:
+            info = nlp.shard_info()
+            mp_ = ShardMap(net.n_bus, net.n_line, net.n_gen, s.n_thermal, info["ramp_gens"],
+                           T_total, first, T_rank)
+            halo = mp_.halo_plan(dev)
 
     def exchange():
-        from paper_2405_14032_b200.shard import exchange_halo
-        exchange_halo(halo, dx, dss, rank)
+        if peer is not None:
+            peer.exchange(dx, dss, DeviceHalo.BOTH, torch.cuda.current_stream().cuda_stream)
+        else:
+            from paper_2405_14032_b200.shard import exchange_halo
+            exchange_halo(halo, dx, dss, rank)
 
     # Two streams: the callbacks on `stream`, the KKT on `kstream`.  Given x, w
     # and Sigma, f/grad/g/J/H and the fused A/M are independent (the fused KKT
@@ -449,7 +470,7 @@ def run_ours(args, rank, world, local_rank, dist):
             if ev is not None:
                 ev[i].record(st or stream)
         mark(0)
-        if halo is not None:
+        if world > 1:
             with torch.cuda.stream(stream):
                 exchange()
         ev_x.record(stream)  # x (with its halo) ready
@@ -468,10 +489,13 @@ def run_ours(args, rank, world, local_rank, dist):
                                 sync=False)
             if name in cb_mark:
                 mark(cb_mark[name])
-        if world > 1:  # the global objective: shard partials added in rank order (one all-gather)
-            from paper_2405_14032_b200.shard import global_objective
+        if world > 1:  # the global objective: shard partials added in rank order
             with torch.cuda.stream(stream):
-                f_global.copy_(global_objective(f, world))
+                if peer is not None:
+                    peer.objective(f, f_global, DeviceHalo.BOTH, stream.cuda_stream)
+                else:
+                    from paper_2405_14032_b200.shard import global_objective
+                    f_global.copy_(global_objective(f, world))
         if after_cb is not None:
             after_cb()
         if fused and ks is not stream:
@@ -525,7 +549,7 @@ def run_ours(args, rank, world, local_rank, dist):
     # ---- CUDA graph (one graph per unit of work on device-resident
     # buffers).  The whole step -- both streams, fork/join events included -- is
     # captured once and replayed; this is the production launch mode and `value`.
-    graph_mode = args.graph and halo is None
+    graph_mode = args.graph and halo is None  # the NCCL halo stays eager; the peer halo is captured
     if graph_mode:
         graph = torch.cuda.CUDAGraph()
         torch.cuda.synchronize()
@@ -554,8 +578,14 @@ def run_ours(args, rank, world, local_rank, dist):
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
         ms = float(t.item())
-    nnz_step = s.jac_nnz + s.hess_nnz + kkt.m_nnz
-    value = nnz_step * world / (ms * 1e-3)
+    nnz_rank = s.jac_nnz + s.hess_nnz + kkt.m_nnz
+    nnz_step = nnz_rank  # summed over ranks (shards differ by their ghost rows / columns)
+    if dist:
+        import torch.distributed as tdist
+        tt_ = torch.tensor([float(nnz_rank)], dtype=torch.float64, device=dev)
+        tdist.all_reduce(tt_)
+        nnz_step = int(tt_.item())
+    value = nnz_step / (ms * 1e-3)
 
     # roofline of the dominant kernel: per-kernel CUDA events on the launch stream
     # (library KTimer), measured over extra steps after the timed region
@@ -563,7 +593,7 @@ def run_ours(args, rank, world, local_rank, dist):
     kkt.set_grid_cap(0)  # standalone per-kernel times: each kernel alone, full grid
     kprof = profile_kernels(L, step, max(3, min(args.steps, 10)), stream, flush)
     kkt.set_grid_cap(grid_cap)
-    kb = kernel_bytes(s, kkt, nlp, net, args.periods)
+    kb = kernel_bytes(s, kkt, nlp, net, T_rank)
     dom = max(kprof, key=lambda k: kprof[k][0] * kprof[k][1])
     dom_ms = kprof[dom][0]
     achieved = kb.get(dom, 0.0) / (dom_ms * 1e-3) / 1e9
@@ -621,7 +651,7 @@ def run_ours(args, rank, world, local_rank, dist):
                 dx.copy_(tx, non_blocking=True)
                 dwt.copy_(tw, non_blocking=True)
             kw = None
-            if halo is None:
+            if world == 1:
                 copy_s.wait_stream(stream)  # also orders the reuse of dsx / dss after the last step
                 with torch.cuda.stream(copy_s):
                     dsx.copy_(tsx, non_blocking=True)
@@ -683,7 +713,7 @@ def run_ours(args, rank, world, local_rank, dist):
             del dA, dM
             h2d = 8 * (s.n_vars + 2 * s.n_cons + s.n_free)
             d2h = 8 * (1 + s.n_vars + s.n_cons + kkt.a_nnz + kkt.m_nnz)
-            e2e = {"value": nnz_step * world / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
+            e2e = {"value": nnz_step / (e_ms * 1e-3), "unit": UNIT, "ms_per_step": e_ms,
                    "steps": ksteps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                    "path": "pinned host x, w, Sigma -> device; C-ABI device-pointer calls "
                            "(callbacks + fused KKT, as the timed step); f, grad, g, A, M -> "
@@ -708,7 +738,7 @@ def run_ours(args, rank, world, local_rank, dist):
         c_ms = timed(e2e_contract_step, ksteps)
         h2d = 8 * (5 * s.n_vars + s.n_cons + s.jac_nnz + s.hess_nnz + s.n_free + s.n_cons)
         d2h = 8 * (1 + s.n_vars + s.n_cons + s.jac_nnz + s.hess_nnz + kkt.a_nnz + kkt.m_nnz)
-        e2e_contract = {"value": nnz_step * world / (c_ms * 1e-3), "unit": UNIT, "ms_per_step": c_ms,
+        e2e_contract = {"value": nnz_step / (c_ms * 1e-3), "unit": UNIT, "ms_per_step": c_ms,
                         "steps": ksteps, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                         "path": "C-ABI GN_MEM_HOST calls (pinned host buffers), "
                                 "NlpProblem/CondensedKkt-style (J, H round trips)"}
@@ -726,15 +756,22 @@ def run_ours(args, rank, world, local_rank, dist):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if args.strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.config} x {args.periods} periods per GPU "
-                               f"(BASELINE configs[{CONFIG_INDEX.get(args.config, '-')}]; "
-                               f"{s.n_vars} vars/GPU)",
+        "config": {"workload": (f"{args.config} x {args.periods} periods"
+                                + (f", period-sharded over {world} GPUs" if args.strong
+                                   else " per GPU")
+                                + f" (BASELINE configs[{CONFIG_INDEX.get(args.config, '-')}]; "
+                                  f"{s.n_vars} vars on rank 0)"),
                    "network": {"buses": net.n_bus, "lines": net.n_line, "gens": net.n_gen,
                                "loads": net.n_load},
-                   "periods_per_gpu": args.periods, "periods_total": args.periods * world,
+                   "periods_per_gpu": T_rank, "periods_total": T_total,
                    "parallelism": f"period-shard x{world}",
+                   "halo": None if world == 1 else (f"{args.halo}: " + (
+                       "gn_halo peer-memory stores over NVLink, one kernel per exchange, in "
+                       "the CUDA graph" if peer is not None else
+                       "torch.distributed NCCL point-to-point, eager")),
                    "nnz_per_step_per_gpu": {"J": s.jac_nnz, "H": s.hess_nnz, "M": kkt.m_nnz},
                    "l2": "256 MB buffer rewritten between timed steps (outside step events); "
                          "per-step working set ~5.8 GB >> 126 MB L2",
@@ -1057,7 +1094,12 @@ def main():
     ap.add_argument("--no-ipm-ops", action="store_true",
                     help="skip the device-resident IPM vector-op measurement")
     ap.add_argument("--graph", type=int, choices=[0, 1], default=1,
-                    help="replay the step as one CUDA graph (single rank / no halo)")
+                    help="replay the step as one CUDA graph (with the peer halo under torchrun)")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: --periods is the whole horizon, partitioned over the "
+                         "ranks (e.g. configs[3]: --config case13659pegase --periods 168)")
+    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+                    help="period-shard halo: peer-memory stores (gn_halo) or NCCL p2p")
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
     args = ap.parse_args()
 

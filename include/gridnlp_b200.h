@@ -129,6 +129,43 @@ int gn_ctx_create_shard(const gn_network* net, int32_t periods_total, int32_t fi
  *         ramp_row0, ramp_rows_per_gen, first_step, owned_lifted_columns (-1 before
  *         gn_lifted_create)]; ramp_gens[n_ramp_gens] (may be NULL). */
 int gn_ctx_shard_info(gn_ctx* ctx, int64_t* info, int32_t* ramp_gens);
+
+/* ---------------------------------------------------------- period-shard halo
+ * The ramp coupling between period shards (opf.hpp:343-351) over peer
+ * memory: each rank owns a small device region that its neighbours store into directly
+ * (NVLink / NVSwitch P2P), released by a step flag -- pg(., t0-1) from rank-1, pg(., t1)
+ * and the sigma_s of the step-t1 ramp rows from rank+1, and every rank's objective
+ * partial.  An exchange is one kernel on the caller's stream (no host call: capturable in
+ * a CUDA graph).  Ranks on different GPUs; see gn_halo_exchange_emulated for one GPU. */
+typedef struct gn_halo gn_halo;
+#define GN_HALO_HANDLE_BYTES 64
+#define GN_HALO_SEND 1
+#define GN_HALO_RECV 2
+#define GN_HALO_BOTH 3
+/* ctx must be the shard of `rank` of a `world`-rank partition (gn_ctx_create_shard). */
+int gn_halo_create(gn_ctx* ctx, int32_t rank, int32_t world, gn_halo** out, gn_error* err);
+/* This rank's region as an IPC handle (GN_HALO_HANDLE_BYTES bytes). */
+int gn_halo_ipc_handle(gn_halo* halo, void* handle);
+/* Map every other rank's region from the all-gathered handles (world x
+ * GN_HALO_HANDLE_BYTES; this rank's own entry is ignored). */
+int gn_halo_open(gn_halo* halo, const void* handles);
+/* Same-process alternative: the ranks' halos (index = rank) see each other's regions
+ * directly (one GPU, or GPUs with peer access enabled). */
+int gn_halo_link(gn_halo* const* halos, int32_t world);
+/* phase GN_HALO_SEND: pack pg(., first / last period) and sigma_s of the step-t0 rows into
+ * the neighbours' regions and release the step flag; GN_HALO_RECV: wait for this step's
+ * flags, write the ghost set-points into x and the ghost rows into sigma_s; BOTH: one
+ * kernel.  x / sigma_s are the shard's device vectors. */
+int gn_halo_exchange(gn_halo* halo, double* x, double* sigma_s, int phase, void* stream);
+/* Global objective = the ranks' partials f_local[0] added in rank order (the same value on
+ * every rank, run to run); device pointers, phases as above. */
+int gn_halo_objective(gn_halo* halo, const double* f_local, double* f_global, int phase,
+                      void* stream);
+/* One GPU: every rank's exchange (GN_HALO_BOTH) in ONE cooperative launch, CTA r = rank r
+ * (world <= 8, linked halos) -- the cross-rank waits are between co-resident CTAs. */
+int gn_halo_exchange_emulated(gn_halo* const* halos, int32_t world, double* const* xs,
+                              double* const* sigma_s, void* stream);
+int gn_halo_destroy(gn_halo* halo);
 int gn_ctx_destroy(gn_ctx* ctx);
 /* Publish (on = 1) or withdraw (on = 0) the context's lifted structure for gn_kkt_create:
  * a KKT created from COO arrays equal to a published context's lifted J / H structure

@@ -84,6 +84,15 @@ _SIGS = {
     "gn_ctx_shard_info": (C.c_int, [vp, i64p, i32p]),
     "gn_ctx_destroy": (C.c_int, [vp]),
     "gn_ctx_publish": (C.c_int, [vp, C.c_int]),
+    "gn_halo_create": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp), C.POINTER(GnError)]),
+    "gn_halo_ipc_handle": (C.c_int, [vp, vp]),
+    "gn_halo_open": (C.c_int, [vp, vp]),
+    "gn_halo_link": (C.c_int, [C.POINTER(vp), C.c_int32]),
+    "gn_halo_exchange": (C.c_int, [vp, f64p, f64p, C.c_int, vp]),
+    "gn_halo_objective": (C.c_int, [vp, f64p, f64p, C.c_int, vp]),
+    "gn_halo_exchange_emulated": (C.c_int, [C.POINTER(vp), C.c_int32, C.POINTER(f64p),
+                                            C.POINTER(f64p), vp]),
+    "gn_halo_destroy": (C.c_int, [vp]),
     "gn_ctx_set_stream": (C.c_int, [vp, vp]),
     "gn_ctx_get_stream": (C.c_int, [vp, C.POINTER(vp)]),
     "gn_ctx_status": (C.c_int, [vp, C.POINTER(GnError)]),

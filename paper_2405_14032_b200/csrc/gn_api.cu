@@ -388,6 +388,12 @@ static void ctx_free(gn_ctx* c) {
   if (s) cudaStreamDestroy(s);
 }
 
+}  // extern "C"
+void gnb::ctx_unref(gn_ctx* c) {
+  if (c && --c->refs == 0 && c->closed) ctx_free(c);
+}
+extern "C" {
+
 int gn_ctx_destroy(gn_ctx* c) {
   if (!c) return GN_OK;
   unpublish(c);  // no new KKT may match it; live ones keep their reference

@@ -127,6 +127,9 @@ struct DevNet {
   const uint8_t* var_fixed;    // per (block, entity): 6 blocks laid out like x / T
 };
 
+// Drop one dependent's reference on a context (frees it when destroyed and unreferenced).
+void ctx_unref(gn_ctx* c);
+
 // Status word: lexicographic min of (pattern id << 32 | record) over failures.
 constexpr unsigned long long kNoFail = ~0ull;
 

@@ -209,6 +209,94 @@ def global_objective(f_local, world: int):
     return total
 
 
+class DeviceHalo:
+    """The period-shard halo over peer memory (gn_halo, csrc/gn_halo.cu): this rank's
+    neighbours store the boundary set-points / sigma_s and their objective partials
+    straight into a small region of this rank's device memory (NVLink / NVSwitch P2P)
+    and release a step flag; one kernel per exchange, no host call, so a step that
+    contains the exchanges is capturable in one CUDA graph."""
+
+    SEND, RECV, BOTH = 1, 2, 3
+    HANDLE_BYTES = 64
+
+    def __init__(self, nlp, rank: int, world: int):
+        import ctypes as C
+        from . import abi
+        from .opf import _check
+        self.lib, self.nlp, self.rank, self.world = abi.lib(), nlp, rank, world
+        h, err = C.c_void_p(), abi.GnError()
+        _check(self.lib.gn_halo_create(nlp.h, rank, world, C.byref(h), C.byref(err)), err,
+               "gn_halo_create")
+        self.h = h
+
+    def ipc_handle(self) -> bytes:
+        import ctypes as C
+        buf = (C.c_ubyte * self.HANDLE_BYTES)()
+        self._ok(self.lib.gn_halo_ipc_handle(self.h, buf))
+        return bytes(buf)
+
+    def open(self, handles: list[bytes]):
+        """Map every other rank's region (handles[q] from rank q, e.g. all_gather_object)."""
+        import ctypes as C
+        raw = b"".join(handles)
+        assert len(raw) == self.HANDLE_BYTES * self.world
+        buf = (C.c_ubyte * len(raw)).from_buffer_copy(raw)
+        self._ok(self.lib.gn_halo_open(self.h, buf))
+
+    def connect(self):
+        """open() with the handles all-gathered over the default process group."""
+        import torch.distributed as tdist
+        handles = [None] * self.world
+        tdist.all_gather_object(handles, self.ipc_handle())
+        self.open(handles)
+
+    @staticmethod
+    def link(halos: list["DeviceHalo"]):
+        """Same process: the ranks' halos (index = rank) see each other's regions."""
+        import ctypes as C
+        arr = (C.c_void_p * len(halos))(*[x.h.value for x in halos])
+        halos[0]._ok(halos[0].lib.gn_halo_link(arr, len(halos)))
+
+    def exchange(self, x, sigma_s, phase: int = 3, stream: int = 0):
+        from .opf import _f64
+        import ctypes as C
+        self._ok(self.lib.gn_halo_exchange(self.h, _f64(x), _f64(sigma_s), phase,
+                                           C.c_void_p(stream)))
+
+    def objective(self, f_local, f_global, phase: int = 3, stream: int = 0):
+        from .opf import _f64
+        import ctypes as C
+        self._ok(self.lib.gn_halo_objective(self.h, _f64(f_local), _f64(f_global), phase,
+                                            C.c_void_p(stream)))
+
+    @staticmethod
+    def exchange_emulated(halos: list["DeviceHalo"], xs, sigma_s, stream: int = 0):
+        """All ranks' exchanges in one cooperative launch (one GPU)."""
+        import ctypes as C
+        from . import abi
+        from .opf import _f64
+        k = len(halos)
+        hs = (C.c_void_p * k)(*[x.h.value for x in halos])
+        px = (abi.f64p * k)(*[_f64(a) for a in xs])
+        ps = (abi.f64p * k)(*[_f64(a) for a in sigma_s])
+        halos[0]._ok(halos[0].lib.gn_halo_exchange_emulated(hs, k, px, ps, C.c_void_p(stream)))
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.gn_halo_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _ok(self, rc):
+        from .opf import _check
+        _check(rc, None, "gn_halo")
+
+
 def halo_exchange(maps: list[ShardMap], xs: list[np.ndarray], sigma_s: list[np.ndarray]):
     """In-process halo fill (all ranks' arrays at hand): what the distributed
     exchange in bench.py / tests/test_shard_gloo.py does with send/recv."""
