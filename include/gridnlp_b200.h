@@ -356,6 +356,13 @@ int gn_kkt_solve_finish(gn_ipm* ipm, const double* dx, const double* qs, const d
                         const double* sigma_s, double delta_w, double delta_c, double* ds,
                         double* dy, int mem);
 
+/* ------------------------------------------------------------ test support
+ * (compute-sanitizer is unavailable on the GPU pool.)  fill = 1: write `pattern` over the
+ * KKT's A and M values and the guard band allocated after each; fill = 0: out4 = {A slots
+ * still holding the pattern (never written), A guard words changed (overrun), the same for
+ * M}.  An assembly between the two calls must leave {0, 0, 0, 0}. */
+int gn_debug_kkt_guard(gn_kkt* kkt, int fill, uint64_t pattern, int64_t* out4);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,7 @@ _SIGS = {
     "gn_ctx_shard_info": (C.c_int, [vp, i64p, i32p]),
     "gn_ctx_destroy": (C.c_int, [vp]),
     "gn_ctx_publish": (C.c_int, [vp, C.c_int]),
+    "gn_debug_kkt_guard": (C.c_int, [vp, C.c_int, C.c_uint64, i64p]),
     "gn_halo_create": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp), C.POINTER(GnError)]),
     "gn_halo_ipc_handle": (C.c_int, [vp, vp]),
     "gn_halo_open": (C.c_int, [vp, vp]),

@@ -883,6 +883,51 @@ int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
   API_CATCH(nullptr)
 }
 
+// ------------------------------------------------------------ test support
+namespace {
+__global__ void k_guard_fill(int64_t n, unsigned long long* p, unsigned long long v) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) p[i] = v;
+}
+__global__ void k_guard_count(int64_t n, int64_t body, const unsigned long long* p,
+                              unsigned long long v, unsigned long long* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (i < body && p[i] == v) atomicAdd(out, 1ull);        // slot never written
+  if (i >= body && p[i] != v) atomicAdd(out + 1, 1ull);   // guard band touched
+}
+}  // namespace
+
+int gn_debug_kkt_guard(gn_kkt* K, int fill, uint64_t pattern, int64_t* out4) {
+  if (!K || (!fill && !out4)) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  cudaStream_t s = K->stream;
+  struct B { double* p; int64_t body; } bufs[2] = {{K->avals.p, K->annz}, {K->mvals.p, K->mnnz}};
+  DBuf<unsigned long long> cnt;
+  if (!fill) {
+    cnt.alloc(4);
+    GN_CK(cudaMemsetAsync(cnt.p, 0, 4 * sizeof(unsigned long long), s));
+  }
+  for (int b = 0; b < 2; ++b) {
+    const int64_t n = bufs[b].body + gnb::kGuard;
+    auto* p = reinterpret_cast<unsigned long long*>(bufs[b].p);
+    const unsigned g = (unsigned)((n + 255) / 256);
+    if (fill) k_guard_fill<<<g, 256, 0, s>>>(n, p, pattern);
+    else k_guard_count<<<g, 256, 0, s>>>(n, bufs[b].body, p, pattern, cnt.p + 2 * b);
+  }
+  GN_CK(cudaGetLastError());
+  if (!fill) {
+    unsigned long long h[4];
+    GN_CK(cudaMemcpyAsync(h, cnt.p, sizeof h, cudaMemcpyDeviceToHost, s));
+    GN_CK(cudaStreamSynchronize(s));
+    for (int i = 0; i < 4; ++i) out4[i] = static_cast<int64_t>(h[i]);
+  }
+  GN_CK(cudaStreamSynchronize(s));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
 int gn_kkt_set_grid_cap(gn_kkt* K, int ctas_per_sm) {
   if (!K || ctas_per_sm < 0) return GN_ERR_INVALID;
   gnb::opf_set_grid_cap(K, ctas_per_sm);

@@ -184,8 +184,8 @@ void kkt_build(gn_kkt* K, const int32_t* jr, const int32_t* jc, const int32_t* h
     compress_keys(key.p, K->nj, n, m, K->A, s);
   }
   K->annz = K->A.nnz;
-  K->avals.alloc(static_cast<size_t>(K->annz) + 1);
-  GN_CK(cudaMemsetAsync(K->avals.p, 0, sizeof(double) * (K->annz + 1), s));
+  K->avals.alloc(static_cast<size_t>(K->annz) + kGuard);  // tail guard: gn_debug_kkt_guard
+  GN_CK(cudaMemsetAsync(K->avals.p, 0, sizeof(double) * (K->annz + kGuard), s));
   // ---- pair offsets
   DBuf<int64_t> cnt, poff;
   cnt.alloc(static_cast<size_t>(m) + 1);
@@ -221,9 +221,9 @@ void kkt_build(gn_kkt* K, const int32_t* jr, const int32_t* jc, const int32_t* h
     compress_keys(key.p, total, n, n, K->M, s);
   }
   K->mnnz = K->M.nnz;
-  K->dvals.alloc(static_cast<size_t>(m) + 1);
-  K->mvals.alloc(static_cast<size_t>(K->mnnz) + 1);
-  GN_CK(cudaMemsetAsync(K->mvals.p, 0, sizeof(double) * (K->mnnz + 1), s));
+  K->dvals.alloc(static_cast<size_t>(m) + kGuard);
+  K->mvals.alloc(static_cast<size_t>(K->mnnz) + kGuard);
+  GN_CK(cudaMemsetAsync(K->mvals.p, 0, sizeof(double) * (K->mnnz + kGuard), s));
   GN_CK(cudaGetLastError());
   GN_CK(cudaStreamSynchronize(s));
 }

@@ -4,6 +4,9 @@
 namespace gnb {
 
 struct OpfKkt;
+// doubles allocated after A / M / d values: a guard band that no kernel may touch
+// (gn_debug_kkt_guard fills and checks it)
+constexpr int64_t kGuard = 512;
 
 // A compressed (CSC-ordered) pattern plus its scatter/gather maps.
 struct Csc {
