@@ -753,6 +753,9 @@ def run_ours(args, rank, world, local_rank, dist):
     dropin = None
     if rank == 0 and world == 1 and args.dropin:
         dropin = dropin_ipm()
+    seam = None
+    if rank == 0 and world == 1 and not args.no_seam:
+        seam = dropin_seam(raw, net, scale)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -799,6 +802,7 @@ def run_ours(args, rank, world, local_rank, dist):
         "e2e_contract": e2e_contract,
         "cpu_baseline": cpu,
         "dropin_ipm": dropin,
+        "dropin_seam": seam,
         "libraries_loaded": loaded_libraries(),
     }
     if args.traffic_json and Path(args.traffic_json).exists():
@@ -1002,6 +1006,33 @@ def cpu_port(config, budget_s=15.0, periods=2):
                       f"(oracle/gn_oracle.c), one thread"}
 
 
+def dropin_seam(raw, net, scale, units=3):
+    """The hot-path unit through the reference's own seams (oracle/_ref/seam_bench): the
+    unmodified LiftedProblem over gridnlp_b200::CudaOpfNlp, then the CondensedKkt the
+    IpmSolver builds from the lifted COO arrays (the shim, recognised as the OPF problem),
+    with pageable std::vector spans -- the drop-in integration as a user of the reference
+    gets it, at the bench configuration (VERDICT r1 next #4)."""
+    import subprocess
+    import tempfile
+    from oracle import bindings as B
+    exe = B.HERE / "_ref" / "seam_bench"
+    if not exe.exists():
+        return None
+    with tempfile.TemporaryDirectory() as d:
+        path = Path(d) / "net.bin"
+        B.write_network_bin(path, net, scale.shape[0], scale)
+        out = subprocess.run([str(exe), str(path), "cuda", str(units)], capture_output=True,
+                             text=True, timeout=1200)
+    if out.returncode != 0:
+        return {"error": out.stderr.strip()[-300:]}
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    r["value"] = r["nnz_per_unit"] / (r["ms_per_unit"] * 1e-3)
+    r["unit"] = UNIT
+    r["path"] = ("reference LiftedProblem (host gathers) + CudaOpfNlp callbacks (GN_MEM_HOST) + "
+                 "shim CondensedKkt set_jacobian / assemble, pageable std::vector spans")
+    return r
+
+
 def dropin_ipm(periods=24):
     """The UNMODIFIED reference interior-point solver end to end, twice on the same problem
     (synthetic case118-size x `periods`): with the reference's own callbacks and
@@ -1089,6 +1120,8 @@ def main():
                     help="also time whole reference-IPM solves, reference vs drop-in (host-"
                          "LDL^T-bound, noisy: median of 3 each)")
     ap.add_argument("--no-dropin", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--no-seam", action="store_true",
+                    help="skip the drop-in seam timing (oracle/_ref/seam_bench)")
     ap.add_argument("--no-trial", action="store_true",
                     help="skip the line-search trial (gn_eval_fg) measurement")
     ap.add_argument("--no-ipm-ops", action="store_true",
