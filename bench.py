@@ -809,6 +809,15 @@ def run_ours(args, rank, world, local_rank, dist):
         tr = json.loads(Path(args.traffic_json).read_text())
         key = dom.split("<")[0] if dom not in tr else dom
         line["roofline"]["traffic"] = tr.get(dom, tr.get(key))
+        # measured DRAM bytes of the whole step: ncu bytes per launch x launches per step
+        # (the bus3 classes are "k_fz_bus3" and "k_fz_bus3 #2" in the capture)
+        if world == 1 and args.config == CONFIG and T_rank == PERIODS_PER_RANK:
+            dram = sum(v for k, v in tr.items())
+            line["unit_roofline"].update(
+                dram_bytes=dram, dram_achieved=dram / (ms * 1e-3) / 1e9,
+                dram_frac=dram / (ms * 1e-3) / 1e9 / peak,
+                dram_source=f"{args.traffic_json} (ncu --set full, per launch; one launch "
+                            f"per kernel per step)")
     if rank == 0:
         print(json.dumps(line), flush=True)
 
