@@ -412,78 +412,10 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 #define GN_SJW 8
 #endif
 constexpr int kSJW = GN_SJW;  // warps per CTA
-constexpr int kSJR = kSJW * 32;  // flow records per record block (one per thread)
-constexpr int kSJSmem = (kSJR * 5 + 2 > kSJW * 5 * 33) ? kSJR * 5 + 2 : kSJW * 5 * 33;
-
-// Flow rows as record blocks (one thread per (line, period) record, like the J callback):
-// the flow_p rows of records r0 .. r0+nb-1 are consecutive CSR rows, i.e. one contiguous
-// span of A; each thread stages its row (its J values at their CSR positions) in shared
-// memory and one thread hands the span to the TMA bulk-copy engine (UBLKCP), as
-// stage_out does in the callbacks -- the per-element store and index work of the
-// warp-span flush leaves the SMs.  Then the same for the flow_q rows.
-__device__ __forceinline__ void sj_span_out(double* sm, double* __restrict__ A, int64_t base,
-                                            int64_t total, int shift) {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic -> async proxy
-  __syncthreads();
-  if (threadIdx.x == 0 && total > 0) {
-    const int head = shift;  // dst 8 mod 16: one element stored directly
-    if (head) A[base] = sm[shift];
-    const int64_t rest = total - head, body = rest & ~1LL;
-    if (body > 0) {
-      const unsigned src = static_cast<unsigned>(__cvta_generic_to_shared(sm + shift + head));
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                   :: "l"(A + base + head), "r"(src), "r"((unsigned)(body * 8)) : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-    }
-    if (rest & 1) A[base + total - 1] = sm[shift + total - 1];
-    if (body > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ void sj_flow_records(int64_t blk, const OpfKktTab& t,
-                                                const double* __restrict__ x,
-                                                double* __restrict__ A, double* sm) {
-  const int32_t T = t.T;
-  const int64_t nrec = (int64_t)t.L * T, r0 = blk * kSJR, r = r0 + threadIdx.x;
-  const bool valid = r < nrec;
-  const int64_t rl = valid ? r : r0;  // idle threads mirror the first record (never stored)
-  const int32_t l = (int32_t)(rl / T), tt = (int32_t)(rl - (int64_t)l * T);
-  const int4 d0 = __ldg(t.ldesc0 + l);
-  const int32_t len = 1 + __popc(d0.w & 15);
-  const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
-  const LineState s = line_state(G, B, x[t.v0 + d0.x * T + tt], x[t.v0 + d0.y * T + tt],
-                                 x[t.th0 + d0.x * T + tt], x[t.th0 + d0.y * T + tt]);
-  int pos[5];
-#pragma unroll
-  for (int fl = 0; fl < 5; ++fl) pos[fl] = __ldg(t.fpos + 5 * l + fl);
-  // the block's first and last records: span base and length (uniform loads)
-  const int32_t l0 = (int32_t)(r0 / T), t0 = (int32_t)(r0 - (int64_t)l0 * T);
-  const int64_t rlast = (r0 + kSJR < nrec ? r0 + kSJR : nrec) - 1;
-  const int32_t l1 = (int32_t)(rlast / T), t1 = (int32_t)(rlast - (int64_t)l1 * T);
-  const int32_t len0 = 1 + __popc(__ldg(t.ldesc0 + l0).w & 15);
-  const int32_t len1 = 1 + __popc(__ldg(t.ldesc0 + l1).w & 15);
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    const int32_t* rb = t.rbase + 2 * t.N + q * t.L;
-    const int64_t base = __ldg(rb + l0) + (int64_t)t0 * len0;
-    const int64_t total = __ldg(rb + l1) + (int64_t)t1 * len1 + len1 - base;
-    const int shift = ((reinterpret_cast<uintptr_t>(A + base)) & 15) ? 1 : 0;
-    if (valid) {
-      const int64_t off = __ldg(rb + l) + (int64_t)tt * len - base;
-      double* o = sm + shift + off;
-#pragma unroll
-      for (int fl = 0; fl < 5; ++fl)
-        if (pos[fl] >= 0) o[pos[fl]] = 0.0 + (q ? j_flow_q(s, G, B, fl) : j_flow_p(s, G, B, fl));
-    }
-    sj_span_out(sm, A, base, total, shift);
-  }
-}
-
 __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t, int32_t m,
                                              const double* __restrict__ x,
-                                             double* __restrict__ A, int skip_flow,
-                                             double* stg_all) {
+                                             double* __restrict__ A, int skip_flow) {
+  __shared__ double stg_all[kSJW * 5 * 33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t T = t.T, tch = t.tchunks;
   const int32_t LT = (t.ang0 - t.therm0) / (T > 0 ? T : 1);
@@ -585,33 +517,19 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
   }
 }
 
-// virtual blocks [0, nflow): flow record blocks (GN_SJ_RECORDS); the rest: warp tasks
-#ifndef GN_SJ_RECORDS
-#define GN_SJ_RECORDS 1
-#endif
-__device__ __forceinline__ void set_jac_vblock(int64_t vb, int64_t nflow, const OpfKktTab& t,
-                                               int32_t m, const double* __restrict__ x,
-                                               double* __restrict__ A, int skip_flow,
-                                               double* sm) {
-  if (vb < nflow) sj_flow_records(vb, t, x, A, sm);
-  else set_jac_body(vb - nflow, t, m, x, A, skip_flow || GN_SJ_RECORDS, sm);
-}
 __global__ void __launch_bounds__(kSJW * 32, GN_SJ_MINB) k_opf_set_jac_fused(OpfKktTab t, int64_t nvb,
-                                                                int64_t nflow, int32_t m,
+                                                                int32_t m,
                                                                 const double* __restrict__ x,
                                                                 double* __restrict__ A,
                                                                 int skip_flow) {
-  __shared__ __align__(16) double sm[kSJSmem];
-  set_jac_vblock(blockIdx.x, nflow, t, m, x, A, skip_flow, sm);
+  set_jac_body(blockIdx.x, t, m, x, A, skip_flow);
 }
 __global__ void __launch_bounds__(kSJW * 32, GN_SJ_GS_MINB) k_opf_set_jac_fused_gs(OpfKktTab t, int64_t nvb,
-                                                                   int64_t nflow, int32_t m,
+                                                                   int32_t m,
                                                                    const double* __restrict__ x,
                                                                    double* __restrict__ A,
                                                                    int skip_flow) {
-  __shared__ __align__(16) double sm[kSJSmem];
-  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x)
-    set_jac_vblock(vb, nflow, t, m, x, A, skip_flow, sm);
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) set_jac_body(vb, t, m, x, A, skip_flow);
 }
 
 // ------------------------------------------------------------------ host
@@ -740,16 +658,14 @@ static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream
   {
     KTimer kt(skip_flow ? "k_opf_set_jac_fused<noflow>" : "k_opf_set_jac_fused", st);
     const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
-    const bool rec = GN_SJ_RECORDS && !skip_flow;  // flow rows as TMA record blocks
-    const int64_t nflow = rec ? ((int64_t)t.L * t.T + kSJR - 1) / kSJR : 0;
-    const int64_t warps = 2ll * t.N + ((skip_flow || rec) ? 0 : (int64_t)t.L * t.tchunks) + LT +
-                          t.L + (K->m - t.ramp0 + 31) / 32;
-    const int64_t nvb = nflow + (warps + kSJW - 1) / kSJW;
+    const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
+                          (K->m - t.ramp0 + 31) / 32;
+    const int64_t nvb = (warps + kSJW - 1) / kSJW;
     const unsigned g = grid_cap(nvb, (GN_SJ_CAP > 0 && t.grid_cap > 0) ? GN_SJ_CAP : t.grid_cap);
     if (g < nvb)
-      k_opf_set_jac_fused_gs<<<g, kSJW * 32, 0, st>>>(t, nvb, nflow, K->m, x, K->avals.p, skip_flow);
+      k_opf_set_jac_fused_gs<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
     else
-      k_opf_set_jac_fused<<<g, kSJW * 32, 0, st>>>(t, nvb, nflow, K->m, x, K->avals.p, skip_flow);
+      k_opf_set_jac_fused<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
   }
   count_launch();
   GN_CK(cudaGetLastError());
