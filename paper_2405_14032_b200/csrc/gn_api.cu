@@ -78,8 +78,10 @@ __global__ void k_gather(int64_t n, const int32_t* __restrict__ pick,
 
 void copy_i32(int32_t* dst, const int32_t* src, int64_t n, int mem, cudaStream_t s) {
   if (!dst || n <= 0) return;
-  GN_CK(cudaMemcpyAsync(dst, src, sizeof(int32_t) * n,
-                        is_device(mem) ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+  if (is_device(mem))
+    GN_CK(cudaMemcpyAsync(dst, src, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, s));
+  else
+    gnb::d2h(dst, src, sizeof(int32_t) * n, s);
 }
 
 }  // namespace
@@ -505,7 +507,7 @@ static int eval(gn_ctx* c, int mode, const double* x, const double* w, double ow
   gnb::launch_eval(mode, d, c->net(), dx, dw, ow, dout, c->fpart.p, c->status.p, s);
   if (is_async(mem)) return ok(err);
   if (!is_device(mem))
-    GN_CK(cudaMemcpyAsync(out, dout, sizeof(double) * nout, cudaMemcpyDeviceToHost, s));
+    gnb::d2h(out, dout, sizeof(double) * nout, s);
   return take_status(c, err);
   API_CATCH(err)
 }
@@ -550,8 +552,8 @@ int gn_eval_fg(gn_ctx* c, const double* x, double* f, double* g, int mem, gn_err
   gnb::launch_eval(gnb::EV_FG, d, c->net(), dx, nullptr, 0.0, dg, c->fpart.p, c->status.p, s, df);
   if (is_async(mem)) return ok(err);
   if (!is_device(mem)) {
-    GN_CK(cudaMemcpyAsync(g, dg, sizeof(double) * d.m, cudaMemcpyDeviceToHost, s));
-    GN_CK(cudaMemcpyAsync(f, df, sizeof(double), cudaMemcpyDeviceToHost, s));
+    gnb::d2h(g, dg, sizeof(double) * d.m, s);
+    gnb::d2h(f, df, sizeof(double), s);
   }
   return take_status(c, err);
   API_CATCH(err)
@@ -623,7 +625,7 @@ static int lifted_gather(gn_ctx* c, bool jac, const double* in, double* out, int
     k_gather<<<(unsigned)((nl + 255) / 256), 256, 0, s>>>(nl, pick, din, dout);
     gnb::count_launch();
   }
-  if (!is_device(mem)) GN_CK(cudaMemcpyAsync(out, dout, sizeof(double) * nl, cudaMemcpyDeviceToHost, s));
+  if (!is_device(mem)) gnb::d2h(out, dout, sizeof(double) * nl, s);
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(s));
   return GN_OK;
   API_CATCH(nullptr)
@@ -875,9 +877,15 @@ int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
   API_TRY
   set_device(K->device);
   // device modes accept any UVA-addressable destination (device or pinned host memory)
-  const auto kind = is_device(mem) ? cudaMemcpyDefault : cudaMemcpyDeviceToHost;
-  if (av && K->annz) GN_CK(cudaMemcpyAsync(av, K->avals.p, sizeof(double) * K->annz, kind, K->stream));
-  if (mv && K->mnnz) GN_CK(cudaMemcpyAsync(mv, K->mvals.p, sizeof(double) * K->mnnz, kind, K->stream));
+  if (is_device(mem)) {
+    if (av && K->annz)
+      GN_CK(cudaMemcpyAsync(av, K->avals.p, sizeof(double) * K->annz, cudaMemcpyDefault, K->stream));
+    if (mv && K->mnnz)
+      GN_CK(cudaMemcpyAsync(mv, K->mvals.p, sizeof(double) * K->mnnz, cudaMemcpyDefault, K->stream));
+  } else {
+    if (av && K->annz) gnb::d2h(av, K->avals.p, sizeof(double) * K->annz, K->stream);
+    if (mv && K->mnnz) gnb::d2h(mv, K->mvals.p, sizeof(double) * K->mnnz, K->stream);
+  }
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
   return GN_OK;
   API_CATCH(nullptr)

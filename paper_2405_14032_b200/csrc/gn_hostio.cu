@@ -1,0 +1,189 @@
+// Host-memory transfers of the GN_MEM_HOST calls -- the reference's std::span seams hand the
+// library pageable std::vector storage (solver.hpp:143-146, lifted.hpp).  A cudaMemcpy from
+// or to pageable memory is staged by the driver through its own small pinned buffers, one
+// CPU thread at a time; here it goes through two pinned bounce buffers in chunks instead:
+// the host-side copies are split over a few threads and overlap the DMA of the neighbouring
+// chunk (PCIe is not idle while the CPU copies).  Caller memory that is already pinned
+// (cudaHostAlloc / cudaHostRegister) is DMA'd directly.  Both calls return when the copy is
+// complete, as the host modes require.
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+#include "gn_internal.cuh"
+
+namespace gnb {
+namespace {
+
+constexpr size_t kChunk = 16u << 20;      // bytes per bounce buffer
+constexpr size_t kDirect = 1u << 20;      // below this: one plain cudaMemcpyAsync
+
+// A fixed pool of host threads for the bounce copies.
+class CopyPool {
+ public:
+  CopyPool() {
+    const unsigned hw = std::thread::hardware_concurrency();
+    n_ = hw >= 16 ? 8 : (hw >= 4 ? hw / 2 : 1);
+    for (unsigned i = 1; i < n_; ++i) th_.emplace_back([this, i] { run(i); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  // memcpy(dst, src, bytes) split over the pool (the calling thread takes part 0)
+  void copy(void* dst, const void* src, size_t bytes) {
+    if (n_ == 1 || bytes < (1u << 20)) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> op(op_);  // one split copy at a time
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      pending_ = n_ - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    part(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void part(unsigned i) {
+    const size_t per = (bytes_ / n_ + 63) & ~size_t(63);
+    const size_t a = std::min(bytes_, per * i), b = std::min(bytes_, per * (i + 1));
+    if (b > a) std::memcpy(dst_ + a, src_ + a, b - a);
+  }
+  void run(unsigned i) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+      }
+      part(i);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  unsigned n_ = 1;
+  std::vector<std::thread> th_;
+  std::mutex mu_, op_;
+  std::condition_variable cv_, done_;
+  uint64_t gen_ = 0;
+  unsigned pending_ = 0;
+  bool stop_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+struct Bounce {
+  std::mutex mu;  // one transfer at a time owns the buffers
+  char* buf[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  int device = -1;
+};
+
+CopyPool& pool() {
+  static CopyPool p;
+  return p;
+}
+Bounce& bounce_for(int dev) {
+  static std::mutex mu;
+  static std::vector<Bounce*> per;
+  std::lock_guard<std::mutex> lk(mu);
+  if (static_cast<size_t>(dev) >= per.size()) per.resize(static_cast<size_t>(dev) + 1, nullptr);
+  if (!per[dev]) {
+    auto* b = new Bounce();  // process lifetime (pinned memory is freed at exit)
+    b->device = dev;
+    for (int i = 0; i < 2; ++i) {
+      GN_CK(cudaHostAlloc(reinterpret_cast<void**>(&b->buf[i]), kChunk, cudaHostAllocDefault));
+      GN_CK(cudaEventCreateWithFlags(&b->ev[i], cudaEventDisableTiming));
+    }
+    per[dev] = b;
+  }
+  return *per[dev];
+}
+
+bool pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  if (bytes <= kDirect || pinned(src)) {
+    GN_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    GN_CK(cudaStreamSynchronize(s));
+    return;
+  }
+  int dev = 0;
+  GN_CK(cudaGetDevice(&dev));
+  Bounce& b = bounce_for(dev);
+  std::lock_guard<std::mutex> lk(b.mu);
+  const char* in = static_cast<const char*>(src);
+  char* out = static_cast<char*>(dst);
+  bool used[2] = {false, false};
+  for (size_t off = 0, i = 0; off < bytes; off += kChunk, ++i) {
+    const int k = static_cast<int>(i & 1);
+    const size_t n = std::min(kChunk, bytes - off);
+    if (used[k]) GN_CK(cudaEventSynchronize(b.ev[k]));  // its previous DMA has read it
+    pool().copy(b.buf[k], in + off, n);                  // overlaps the other buffer's DMA
+    GN_CK(cudaMemcpyAsync(out + off, b.buf[k], n, cudaMemcpyHostToDevice, s));
+    GN_CK(cudaEventRecord(b.ev[k], s));
+    used[k] = true;
+  }
+  GN_CK(cudaStreamSynchronize(s));
+}
+
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return;
+  if (bytes <= kDirect || pinned(dst)) {
+    GN_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+    GN_CK(cudaStreamSynchronize(s));
+    return;
+  }
+  int dev = 0;
+  GN_CK(cudaGetDevice(&dev));
+  Bounce& b = bounce_for(dev);
+  std::lock_guard<std::mutex> lk(b.mu);
+  const char* in = static_cast<const char*>(src);
+  char* out = static_cast<char*>(dst);
+  const size_t nch = (bytes + kChunk - 1) / kChunk;
+  auto issue = [&](size_t i) {
+    const size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+    GN_CK(cudaMemcpyAsync(b.buf[i & 1], in + off, n, cudaMemcpyDeviceToHost, s));
+    GN_CK(cudaEventRecord(b.ev[i & 1], s));
+  };
+  issue(0);
+  for (size_t i = 0; i < nch; ++i) {
+    if (i + 1 < nch) issue(i + 1);  // the next chunk's DMA runs while this one is copied out
+    GN_CK(cudaEventSynchronize(b.ev[i & 1]));
+    const size_t off = i * kChunk, n = std::min(kChunk, bytes - off);
+    pool().copy(out + off, b.buf[i & 1], n);
+  }
+}
+
+}  // namespace gnb

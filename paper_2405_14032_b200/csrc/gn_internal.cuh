@@ -29,6 +29,11 @@ struct Error : std::runtime_error {
 
 void count_launch(int n = 1);
 
+// Host <-> device copies of the host-memory modes (gn_hostio.cu): pinned bounce buffers and
+// parallel host copies for pageable caller memory; both return when the copy is complete.
+void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s);
+void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s);
+
 // Optional per-kernel CUDA-event timing (gn_profile_*): RAII around a launch.
 struct KTimer {
   int idx = -1;
@@ -60,7 +65,7 @@ struct DBuf {
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
     alloc(count);
-    if (count) GN_CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    if (count) h2d(p, h, count * sizeof(T), s);
   }
   std::vector<T> download(cudaStream_t s) const {
     std::vector<T> h(n);
