@@ -49,6 +49,22 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Wait until *f >= s.  A peer that never arrives (a crashed rank, mismatched step counts)
+// must not hang the GPU: after kHaloTimeoutNs the kernel traps, which fails this rank's
+// context loudly instead of spinning forever.
+constexpr unsigned long long kHaloTimeoutNs = 30ull * 1000 * 1000 * 1000;
+__device__ __forceinline__ void wait_flag(const unsigned long long* f, unsigned long long s) {
+  const unsigned long long t0 = globaltimer_ns();
+  while (ld_acquire_sys(f) < s) {
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > kHaloTimeoutNs) __trap();
+  }
+}
 __device__ __forceinline__ unsigned long long* flag(double* region, const HaloView& h, int i) {
   return reinterpret_cast<unsigned long long*>(region + h.flags) + 16 * i;  // 128-byte apart
 }
@@ -86,8 +102,8 @@ __device__ void halo_body(const HaloView& h, double* __restrict__ x, double* __r
   }
   if (phase & PH_RECV) {
     if (tid == 0) {
-      if (h.prev) while (ld_acquire_sys(flag(mine, h, 0)) < s) __nanosleep(64);
-      if (h.next) while (ld_acquire_sys(flag(mine, h, 1)) < s) __nanosleep(64);
+      if (h.prev) wait_flag(flag(mine, h, 0), s);
+      if (h.next) wait_flag(flag(mine, h, 1), s);
     }
     __syncthreads();
     for (int k = tid; k < h.GR; k += nt) {  // L2 reads (__ldcg): never a stale L1 line
@@ -115,8 +131,7 @@ __device__ void fsum_body(const HaloView& h, const double* __restrict__ f_local,
   }
   if (phase & PH_RECV) {
     double* mine = h.regions[h.rank];
-    if (tid < h.world)
-      while (ld_acquire_sys(flag(mine, h, 2 + tid)) < s) __nanosleep(64);
+    if (tid < h.world) wait_flag(flag(mine, h, 2 + tid), s);
     __syncthreads();
     if (tid == 0) {  // rank order: the same value on every rank, run to run
       double tot = __ldcg(mine + h.fpart + buf);
