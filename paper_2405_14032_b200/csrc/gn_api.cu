@@ -461,12 +461,14 @@ static int structure(gn_ctx* c, bool jac, int32_t* rows, int32_t* cols, int mem)
   API_TRY
   set_device(c->device);
   const auto& d = c->d;
-  DBuf<int32_t> jr, jc, hr, hc;
-  jr.alloc(d.nj + 1); jc.alloc(d.nj + 1); hr.alloc(d.nh + 1); hc.alloc(d.nh + 1);
-  gnb::build_structure(c, jr.p, jc.p, hr.p, hc.p);
+  DBuf<int32_t> r, k;  // only the requested structure is built
   const int64_t n = jac ? d.nj : d.nh;
-  copy_i32(rows, jac ? jr.p : hr.p, n, mem, c->stream);
-  copy_i32(cols, jac ? jc.p : hc.p, n, mem, c->stream);
+  r.alloc(n + 1);
+  k.alloc(n + 1);
+  if (jac) gnb::build_structure(c, r.p, k.p, nullptr, nullptr);
+  else gnb::build_structure(c, nullptr, nullptr, r.p, k.p);
+  copy_i32(rows, r.p, n, mem, c->stream);
+  copy_i32(cols, k.p, n, mem, c->stream);
   GN_CK(cudaStreamSynchronize(c->stream));
   return GN_OK;
   API_CATCH(nullptr)

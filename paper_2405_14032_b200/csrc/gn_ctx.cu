@@ -160,10 +160,19 @@ OpfDims make_dims(int32_t T, int32_t N, int32_t L, int32_t G, int32_t D, int32_t
 }
 
 // --------------------------------------------------------------- structure
+// (a null jr / hr: that structure is not wanted by this call -- gn_jac_structure and
+// gn_hess_structure each build only their own)
 __device__ __forceinline__ void put_h(int32_t* hr, int32_t* hc, int64_t s, int32_t a,
                                       int32_t b) {
+  if (!hr) return;
   hr[s] = a > b ? a : b;
   hc[s] = a < b ? a : b;
+}
+__device__ __forceinline__ void put_j(int32_t* jr, int32_t* jc, int64_t s, int32_t row,
+                                      int32_t col) {
+  if (!jr) return;
+  jr[s] = row;
+  jc[s] = col;
 }
 
 // Per (l,t): patterns 1, 2 (balance flows), 7, 8 (flow definitions), 10 (angle).
@@ -178,11 +187,11 @@ __global__ void k_struct_line(OpfDims d, DevNet net, int32_t* jr, int32_t* jc, i
   const int32_t af = d.th0 + f * d.T + t, at = d.th0 + to * d.T + t;
   // balance flows: to-record (s=+1) then from-record (s=-1), opf.hpp:254-257
   int64_t s = d.jac_off[K_BAL_P_FLOW] + 2 * r;
-  jr[s] = d.bal_p0 + to * d.T + t; jc[s] = p;
-  jr[s + 1] = d.bal_p0 + f * d.T + t; jc[s + 1] = p;
+  put_j(jr, jc, s, d.bal_p0 + to * d.T + t, p);
+  put_j(jr, jc, s + 1, d.bal_p0 + f * d.T + t, p);
   s = d.jac_off[K_BAL_Q_FLOW] + 2 * r;
-  jr[s] = d.bal_q0 + to * d.T + t; jc[s] = q;
-  jr[s + 1] = d.bal_q0 + f * d.T + t; jc[s + 1] = q;
+  put_j(jr, jc, s, d.bal_q0 + to * d.T + t, q);
+  put_j(jr, jc, s + 1, d.bal_q0 + f * d.T + t, q);
   s = d.hess_off[K_BAL_P_FLOW] + 2 * r;
   put_h(hr, hc, s, p, p); put_h(hr, hc, s + 1, p, p);
   s = d.hess_off[K_BAL_Q_FLOW] + 2 * r;
@@ -194,15 +203,15 @@ __global__ void k_struct_line(OpfDims d, DevNet net, int32_t* jr, int32_t* jc, i
     const int32_t* fv = kind == K_FLOW_P ? fp : fq;
     const int32_t row = (kind == K_FLOW_P ? d.flow_p0 : d.flow_q0) + (int32_t)r;
     int64_t js = d.jac_off[kind] + 5 * r;
-    for (int i = 0; i < 5; ++i) { jr[js + i] = row; jc[js + i] = fv[i]; }
+    for (int i = 0; i < 5; ++i) { put_j(jr, jc, js + i, row, fv[i]); }
     int64_t hs = d.hess_off[kind] + 15 * r;
     for (int j = 0; j < 5; ++j)
       for (int i = j; i < 5; ++i) put_h(hr, hc, hs++, fv[i], fv[j]);
   }
   // angle spread [th_f, th_t]
   s = d.jac_off[K_ANGLE] + 2 * r;
-  jr[s] = d.ang0 + (int32_t)r; jc[s] = af;
-  jr[s + 1] = d.ang0 + (int32_t)r; jc[s + 1] = at;
+  put_j(jr, jc, s, d.ang0 + (int32_t)r, af);
+  put_j(jr, jc, s + 1, d.ang0 + (int32_t)r, at);
   s = d.hess_off[K_ANGLE] + 3 * r;
   put_h(hr, hc, s, af, af); put_h(hr, hc, s + 1, at, af); put_h(hr, hc, s + 2, at, at);
 }
@@ -217,9 +226,9 @@ __global__ void k_struct_gen(OpfDims d, DevNet net, int32_t* jr, int32_t* jc, in
   const int32_t pg = d.pg0 + (int32_t)r, qg = d.qg0 + (int32_t)r;
   put_h(hr, hc, d.hess_off[K_COST] + r, pg, pg);
   int64_t s = d.jac_off[K_BAL_P_INJ] + r;
-  jr[s] = d.bal_p0 + bus * d.T + t; jc[s] = pg;
+  put_j(jr, jc, s, d.bal_p0 + bus * d.T + t, pg);
   s = d.jac_off[K_BAL_Q_INJ] + r;
-  jr[s] = d.bal_q0 + bus * d.T + t; jc[s] = qg;
+  put_j(jr, jc, s, d.bal_q0 + bus * d.T + t, qg);
   put_h(hr, hc, d.hess_off[K_BAL_P_INJ] + r, pg, pg);
   put_h(hr, hc, d.hess_off[K_BAL_Q_INJ] + r, qg, qg);
 }
@@ -233,8 +242,8 @@ __global__ void k_struct_thermal(OpfDims d, DevNet net, int32_t* jr, int32_t* jc
   const int32_t l = net.th_line[k];
   const int32_t p = d.p0 + l * d.T + t, q = d.q0 + l * d.T + t;
   const int64_t s = d.jac_off[K_THERMAL] + 2 * r;
-  jr[s] = d.therm0 + (int32_t)r; jc[s] = p;
-  jr[s + 1] = d.therm0 + (int32_t)r; jc[s + 1] = q;
+  put_j(jr, jc, s, d.therm0 + (int32_t)r, p);
+  put_j(jr, jc, s + 1, d.therm0 + (int32_t)r, q);
   const int64_t h = d.hess_off[K_THERMAL] + 3 * r;
   put_h(hr, hc, h, p, p); put_h(hr, hc, h + 1, q, p); put_h(hr, hc, h + 2, q, q);
 }
@@ -249,8 +258,8 @@ __global__ void k_struct_ramp(OpfDims d, DevNet net, int32_t* jr, int32_t* jc, i
   const int32_t g = net.ramp_gen[k];
   const int32_t a = ramp_var(d, g, k, d.s_lo + st, true), b = ramp_var(d, g, k, d.s_lo + st, false);
   const int64_t s = d.jac_off[K_RAMP] + 2 * r;
-  jr[s] = d.ramp0 + (int32_t)r; jc[s] = a;
-  jr[s + 1] = d.ramp0 + (int32_t)r; jc[s + 1] = b;
+  put_j(jr, jc, s, d.ramp0 + (int32_t)r, a);
+  put_j(jr, jc, s + 1, d.ramp0 + (int32_t)r, b);
   const int64_t h = d.hess_off[K_RAMP] + 3 * r;
   put_h(hr, hc, h, a, a); put_h(hr, hc, h + 1, b, a); put_h(hr, hc, h + 2, b, b);
 }

@@ -65,7 +65,7 @@ struct Ctx {
     s.sn = q[160];
     return s;
   }
-  __device__ double d(int32_t row) const { return dv[row]; }
+  __device__ double d(int32_t row) const { return dval(t, dv, row); }
   __device__ double wt(int32_t row) const { return in.w[row]; }
   __device__ int32_t col(int32_t off, int32_t e) const {
     const int32_t k = f_lent(t, off, e);
@@ -244,15 +244,17 @@ __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
   const double vf = x[t.v0 + f * T + ts], vt = x[t.v0 + to * T + ts];
   const double thf = x[t.th0 + f * T + ts], tht = x[t.th0 + to * T + ts];
   const double xp = x[t.p0 + r], xq = x[t.q0 + r];
-  const double dfp = dv[t.flow_p0 + r], dfq = dv[t.flow_q0 + r];
-  const double dbp_lo = dv[t.bal_p0 + blo * T + ts], dbp_hi = dv[t.bal_p0 + bhi * T + ts];
-  const double dbq_lo = dv[t.bal_q0 + blo * T + ts], dbq_hi = dv[t.bal_q0 + bhi * T + ts];
+  const double dfp = dval(t, dv, t.flow_p0 + r), dfq = dval(t, dv, t.flow_q0 + r);
+  const double dbp_lo = dval(t, dv, t.bal_p0 + blo * T + ts),
+               dbp_hi = dval(t, dv, t.bal_p0 + bhi * T + ts);
+  const double dbq_lo = dval(t, dv, t.bal_q0 + blo * T + ts),
+               dbq_hi = dval(t, dv, t.bal_q0 + bhi * T + ts);
   const int32_t cps = d1.z * T + ts, cqs = d1.w * T + ts;
   const double sxp = sx[cps], sxq = sx[cqs];
   double wth = 0.0, dth = 0.0;
   if (k >= 0) {
     wth = w[t.therm0 + k * T + ts];
-    dth = dv[t.therm0 + k * T + ts];
+    dth = dval(t, dv, t.therm0 + k * T + ts);
   }
   const int2 cb = __ldg(t.lcb + l);
   const int64_t basep = cb.x + (int64_t)c0 * lenp, baseq = cb.y + (int64_t)c0 * lenq;
@@ -648,8 +650,14 @@ void launch_dvec(gn_kkt* K, const double* ss, double dw, double dc) {
 void opf_assemble_fused(gn_kkt* K, const double* x, const double* w, double ow, const double* sx,
                         const double* ss, double dw, double dc) {
   FIn in{x, w, ow, sx, ss, dw, dc};
+  K->opf->t.kdw = dw;
+  K->opf->t.kdc = dc;
+#if GN_DV_INLINE
+  launch_fused<false>(K, in, ss, K->mvals.p, nullptr, nullptr);
+#else
   launch_dvec(K, ss, dw, dc);
   launch_fused<false>(K, in, K->dvals.p, K->mvals.p, nullptr, nullptr);
+#endif
 }
 
 static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream_t st) {

@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
       const int32_t l = e.x >> 1, f = (e.x & 1) ? n : e.y, to = (e.x & 1) ? e.y : n;
       const int32_t rl = l * T + tt;
       const double w7 = in.w[t.flow_p0 + rl], w8 = in.w[t.flow_q0 + rl];
-      const double d7 = dv[t.flow_p0 + rl], d8 = dv[t.flow_q0 + rl], d10 = dv[t.ang0 + rl];
+      const double d7 = dval(t, dv, t.flow_p0 + rl), d8 = dval(t, dv, t.flow_q0 + rl),
+                   d10 = dval(t, dv, t.ang0 + rl);
       const LineState s = line_state(gb.x, gb.y, in.x[t.v0 + f * T + tt], in.x[t.v0 + to * T + tt],
                                      in.x[t.th0 + f * T + tt], in.x[t.th0 + to * T + tt]);
       double* q = S + (size_t)i * kSV * 32;
@@ -374,9 +375,9 @@ __device__ __forceinline__ void busr_body(int64_t vblock, const OpfKktTab& t,
     xtt[i] = in.x[t.th0 + to * T + tt];
     w7[i] = in.w[t.flow_p0 + rl];
     w8[i] = in.w[t.flow_q0 + rl];
-    d7[i] = dv[t.flow_p0 + rl];
-    d8[i] = dv[t.flow_q0 + rl];
-    d10[i] = dv[t.ang0 + rl];
+    d7[i] = dval(t, dv, t.flow_p0 + rl);
+    d8[i] = dval(t, dv, t.flow_q0 + rl);
+    d10[i] = dval(t, dv, t.ang0 + rl);
   }
   const double sxv = cv >= 0 ? in.sx[cv] : 0.0, sxt = ct >= 0 ? in.sx[ct] : 0.0;
   LineState st[DEG];

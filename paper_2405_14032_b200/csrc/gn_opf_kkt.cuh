@@ -70,7 +70,26 @@ struct OpfKktTab {
   const int2* lcb;                      // [L] M column start at t = 0 of p(l), q(l)
   const int32_t* bprog_ptr;             // [N+1] per-bus slot programs of the v(n)/th(n) columns
   const unsigned long long* bprog;      // (row entity << 35 | type << 32 | lane mask)
+  double kdw, kdc;                      // delta_w, delta_c of the assembly in flight (dval)
 };
+
+// d_r of the fused kernels: read from the k_fz_dvec vector, or (GN_DV_INLINE, tuning builds)
+// recomputed from sigma_s by each consumer -- `dv` is then sigma_s itself.
+#ifndef GN_DV_INLINE
+#define GN_DV_INLINE 0
+#endif
+#ifdef __CUDACC__
+__device__ __forceinline__ double dval(const OpfKktTab& t, const double* __restrict__ dv,
+                                       int64_t r) {
+#if GN_DV_INLINE
+  const double sd = dv[r] + t.kdw;  // condensed.hpp:112-116 (gn_opf_math.cuh dvec)
+  const double c = 1.0 / (1.0 + t.kdc * sd);
+  return sd * c;
+#else
+  return dv[r];
+#endif
+}
+#endif
 
 // Inputs of the fused (recompute-from-x) assembly.
 struct FIn {
