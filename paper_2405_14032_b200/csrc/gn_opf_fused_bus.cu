@@ -316,17 +316,21 @@ __device__ __forceinline__ void busr_body(int64_t vblock, const OpfKktTab& t,
   const int32_t T = t.T;
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
   if (tt >= T) return;
-  const int4 bd0 = __ldg(buses + kBusDesc * n64), bd1 = __ldg(buses + kBusDesc * n64 + 1);
-  const int4 bd2 = __ldg(buses + kBusDesc * n64 + 2);
-  const int32_t n = bd0.x, b0 = bd0.y, boff = bd0.w;
-  const int32_t cv = bd1.x < 0 ? -1 : bd1.x * T + tt, ct = bd1.y < 0 ? -1 : bd1.y * T + tt;
+  const int4* bd = buses + (int64_t)bus_desc_stride(DEG - 1) * n64;
+  const int4 bd0 = __ldg(bd), bd1 = __ldg(bd + 1), bd2 = __ldg(bd + 2);
   int2 e[DEG];
   int32_t pp[DEG];
+  double2 gb[DEG];
 #pragma unroll
-  for (int i = 0; i < DEG; ++i) {
-    e[i] = __ldg(t.blx + b0 + i);
-    pp[i] = __ldg(t.bpos + b0 + i);
+  for (int i = 0; i < DEG; ++i) {  // the lines inline in the descriptor: no dependent level
+    const int4 q = __ldg(bd + kBusDesc + i);
+    e[i] = make_int2(q.x, q.y);
+    pp[i] = q.z;
+    const int4 g = __ldg(bd + kBusDesc + DEG + i);
+    gb[i] = make_double2(__hiloint2double(g.y, g.x), __hiloint2double(g.w, g.z));
   }
+  const int32_t n = bd0.x, boff = bd0.w;
+  const int32_t cv = bd1.x < 0 ? -1 : bd1.x * T + tt, ct = bd1.y < 0 ? -1 : bd1.y * T + tt;
   const int64_t posv = cv >= 0 ? (int64_t)bd2.x + (int64_t)tt * bd2.y : 0;
   const int64_t post = ct >= 0 ? (int64_t)bd2.z + (int64_t)tt * bd2.w : 0;
   if constexpr (STRUCT) {
@@ -361,11 +365,9 @@ __device__ __forceinline__ void busr_body(int64_t vblock, const OpfKktTab& t,
     return;
   }
   // ---- loads (all independent), then the line states
-  double2 gb[DEG];
   double xvf[DEG], xvt[DEG], xtf[DEG], xtt[DEG], w7[DEG], w8[DEG], d7[DEG], d8[DEG], d10[DEG];
 #pragma unroll
   for (int i = 0; i < DEG; ++i) {
-    gb[i] = __ldg(t.blgb + b0 + i);
     const bool fr = e[i].x & 1;
     const int32_t l = e[i].x >> 1, o = e[i].y, f = fr ? n : o, to = fr ? o : n;
     const int32_t rl = l * T + tt;

@@ -16,6 +16,7 @@
 // (opf_kkt_prepare): if any column's rows differ, the specialised path is
 // disabled and the generic kernels are used.
 #include <algorithm>
+#include <cstring>
 #include <numeric>
 
 #include <type_traits>
@@ -870,12 +871,23 @@ bool opf_kkt_prepare(gn_kkt* K) {
       colspan(kt, bt, lt);
       v.push_back(make_int4(kv, kt, 0, 0));
       v.push_back(make_int4(bv, lv, bt, lt));
+      if (simple) {  // register classes: the incident lines inline (one level of loads)
+        for (int32_t i = 0; i < deg; ++i) {
+          const int2 e = blx[bl_ptr[n] + i];
+          v.push_back(make_int4(e.x, e.y, bpos[bl_ptr[n] + i], 0));
+        }
+        for (int32_t i = 0; i < deg; ++i) {
+          int4 gbits;
+          std::memcpy(&gbits, &blgb[bl_ptr[n] + i], sizeof gbits);  // (G, B) as 16 bytes
+          v.push_back(gbits);
+        }
+      }
     }
     up(X->bpos, bpos, s);
     for (int k = 0; k < kBusClasses; ++k) {
       up(X->bus_cls[k], cls[k], s);
       if (cls[k].empty()) X->bus_cls[k].alloc(kBusDesc);
-      X->n_bus_cls[k] = static_cast<int32_t>(cls[k].size() / kBusDesc);
+      X->n_bus_cls[k] = static_cast<int32_t>(cls[k].size() / bus_desc_stride(k));
     }
     int32_t md = 0;
     for (size_t i = 0; i < cls[kBusClasses - 1].size(); i += kBusDesc)

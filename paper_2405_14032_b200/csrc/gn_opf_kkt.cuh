@@ -116,6 +116,10 @@ constexpr int kBusRegMax = 6;
 // M start of th(n, t=0), th column length)
 constexpr int kBusDesc = 3;
 constexpr int kBusClasses = kBusRegMax + 2;
+// descriptor int4s per bus of class k: the register classes (k < kBusRegMax, degree k + 1)
+// also carry their lines inline -- (l << 1 | is_from, other bus, neighbour-slot offsets) and
+// (G, B) per line -- so every load of a warp depends on its bus index only
+__host__ __device__ constexpr int bus_desc_stride(int k) { return k < kBusRegMax ? kBusDesc + 2 * (k + 1) : kBusDesc; }
 bool fz_bus_fits(int32_t maxdeg);  // one warp's shared memory fits (else: no fused path)
 
 struct OpfKkt {
