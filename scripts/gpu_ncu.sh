@@ -1,6 +1,6 @@
 tag=$1
 mkdir -p gpurun_out
-C="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ipm-ops --no-trial --graph 0 --streams 1"
+C="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-ipm-ops --no-trial --no-seam --graph 0 --streams 1"
 $C > gpurun_out/plain_launch_$tag.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches_$tag.csv $C > gpurun_out/ncu_launch_$tag.log 2>&1
 echo "launch list rc=$?"
