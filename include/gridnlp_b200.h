@@ -42,7 +42,7 @@ enum {
   GN_ERR_INVALID = 1,     /* bad shape/argument: the reference throws gridnlp::Error */
   GN_ERR_EVAL = 2,        /* domain / non-finite result: the reference returns false */
   GN_ERR_CUDA = 3,        /* CUDA runtime failure (no GPU, OOM, ...) */
-  GN_ERR_UNSUPPORTED = 4  /* input outside the supported OPF dialect (e.g. self-loop line) */
+  GN_ERR_UNSUPPORTED = 4  /* e.g. the fused assembly on a network it cannot enumerate */
 };
 
 enum { GN_MEM_HOST = 0, GN_MEM_DEVICE = 1, GN_MEM_DEVICE_ASYNC = 2, GN_IN_FULL = 16 };

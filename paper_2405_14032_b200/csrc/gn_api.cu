@@ -192,9 +192,6 @@ static int ctx_create(const gn_network* net, int32_t periods_total, int32_t firs
   for (int32_t l = 0; l < L; ++l) {
     const int32_t f = c->line_from[l], t = c->line_to[l];
     if (f < 0 || f >= N || t < 0 || t >= N) throw Error(GN_ERR_INVALID, "line references unknown bus");
-    if (f == t)
-      throw Error(GN_ERR_UNSUPPORTED,
-                  "line " + std::to_string(l) + " is a self-loop (from == to), not supported");
     if (c->line_amin[l] > c->line_amax[l])
       throw Error(GN_ERR_INVALID, "constraint block angle: lower above upper");
   }

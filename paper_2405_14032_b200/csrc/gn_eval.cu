@@ -113,9 +113,11 @@ __device__ __forceinline__ void line_body(const OpfDims& d, const DevNet& net,
   const bool valid = r < nrec;
   double p = 0, q = 0, G = 0, B = 0, vf = 0, vt = 0, thf = 0, tht = 0;
   int64_t rk = -1;  // record of the line's thermal pattern (12: p^2 + q^2 <= smax^2), if rated
+  bool loop = false;  // a self-loop line (from == to)
   if (valid) {
     const int32_t l = (int32_t)(r / d.T), t = (int32_t)(r - (int64_t)l * d.T);
     const int32_t f = __ldg(net.lf + l), to = __ldg(net.lt + l);
+    loop = f == to;
     const int32_t k = __ldg(net.l_therm + l);
     if (k >= 0) rk = (int64_t)k * d.T + t;
     G = __ldg(net.lg + l);
@@ -192,6 +194,14 @@ __device__ __forceinline__ void line_body(const OpfDims& d, const DevNet& net,
     for (int i = 0; i < 15; ++i) {
       hp[i] = h_flow_p(ls, G, wp, i);
       hq[i] = h_flow_q(ls, B, wq, i);
+    }
+    if (loop) {  // v_f == v_t and th_f == th_t: the mirrored local entries (v_t, v_f) and
+                 // (th_t, th_f) fold onto one diagonal slot -- double_slots, doubled as the
+                 // reference does (pattern_model.hpp:193-197, 433)
+      hp[6] += hp[6];
+      hp[13] += hp[13];
+      hq[6] += hq[6];
+      hq[13] += hq[13];
     }
     if (valid) {
       bool okp = true, okq = true;

@@ -582,6 +582,12 @@ bool opf_kkt_prepare(gn_kkt* K) {
   cudaStream_t s = K->stream;
   auto* X = new OpfKkt();
   K->opf = X;
+  // Self-loop lines (from == to) fold two fields of a record onto one variable; the
+  // topology-walking kernels assume two distinct terminals, so such a network keeps the
+  // generic assembly (any COO structure; bit-identical to the reference as well) and has no
+  // fused path.
+  for (int32_t l = 0; l < d.L; ++l)
+    if (c->line_from[l] == c->line_to[l]) return false;
   OpfKktTab& t = X->t;
   t.T = d.T; t.N = d.N; t.L = d.L; t.G = d.G;
   t.bal_p0 = d.bal_p0; t.bal_q0 = d.bal_q0; t.flow_p0 = d.flow_p0; t.flow_q0 = d.flow_q0;

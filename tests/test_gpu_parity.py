@@ -178,13 +178,74 @@ def test_async_status_and_failure_report(gpu):
     assert ok  # status cleared after a failure
 
 
-def test_self_loop_rejected(gpu):
-    raw = synthetic_case(10, 14, 3, 6, seed=1)
-    net = raw.network()
-    net.line_to[3] = net.line_from[3]
+@pytest.mark.parametrize("T", [1, 4])
+def test_self_loop_lines_match_reference(gpu, T):
+    """Self-loop lines (from == to; the reference parser accepts them, matpower.hpp:245-246):
+    their records name one variable in two fields, so J carries duplicate coordinates and the
+    Hessian's mirrored (v_t, v_f) / (th_t, th_f) entries fold onto one diagonal slot whose value
+    doubles (double_slots, pattern_model.hpp:193-197, 433).  Structures, bounds and the lifted
+    maps bit-exact, callbacks within 1e-12, balance rows bit-exact (to-then-from), and the KKT
+    -- the generic assembly, since the topology kernels need two terminals -- bit-exact against
+    the reference's CondensedKkt fed the same values; the fused path is unavailable (loud)."""
+    from paper_2405_14032_b200.abi import GN_ERR_UNSUPPORTED
+    raw = synthetic_case(40, 64, 10, 30, seed=12, parallel_lines=2)
+    raw.branch[3, 1] = raw.branch[3, 0]
+    raw.branch[20, 0] = raw.branch[20, 1]
+    text = raw.to_matpower()
+    scale = B.ref_load_profile(text, T)
+    ref = B.RefModel(text, T, scale)
+    net = B.ref_parse_matpower(text)
+    nlp = OpfNlp(net, T, scale)
+    s = nlp.sizes
+    assert [s.n_vars, s.n_cons, s.jac_nnz, s.hess_nnz] == ref.sizes[:4]
+    for got, want, k in zip(nlp.bounds(), ref.bounds(), ("xl", "xu", "xs", "rl", "ru")):
+        assert_bitexact(got, want, k)
+    rjr, rjc, rhr, rhc = ref.structure()
+    assert_bitexact(nlp.jac_structure()[0], rjr, "jr")
+    assert_bitexact(nlp.jac_structure()[1], rjc, "jc")
+    assert_bitexact(nlp.hess_structure()[0], rhr, "hr")
+    assert_bitexact(nlp.hess_structure()[1], rhc, "hc")
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, 7)
+    w = row_weights(s.n_cons, 8, zero_every=5)
+    for k in ("grad", "g", "jac"):
+        ok, v = getattr(nlp, "eval_" + k)(x)
+        okr, vr, _ = getattr(ref, "eval_" + k)(x)
+        assert ok and okr
+        assert_close(v, vr, what=k)
+    bal = np.arange(2 * net.n_bus * T)
+    assert_bitexact(nlp.eval_g(x)[1][bal], ref.eval_g(x)[1][bal], "balance rows")
+    ok, H = nlp.eval_hess(x, w, 0.8)
+    okr, Hr, _ = ref.eval_hess(x, w, 0.8)
+    assert ok and okr
+    assert_close(H, Hr, what="hess (double_slots)")
+    nlp.lift(1e-4)
+    lift = ref.lift(1e-4)
+    L = nlp.lifted_structure()
+    for k in ("free_to_full", "jac_rows", "jac_cols", "hess_rows", "hess_cols"):
+        assert_bitexact(L[k], lift[k], k)
+    K = CondensedKkt(nlp=nlp)
+    assert K.opf_ready == 0 and K.fused_ready == 0
+    ref.kkt_create()
+    for got, want, k in zip(K.structure(), ref.kkt_structure(), ("rowptr", "colidx", "colptr", "rowidx")):
+        assert_bitexact(got, want, k)
+    okj, jr_ = ref.eval_jac(x)[:2]
+    okh, hr_ = ref.eval_hess(x, w, 0.8)[:2]
+    jl, hl = jr_[L["jac_pick"]], hr_[L["hess_pick"]]
+    sx, ss = sigmas(nlp.sizes.n_free, s.n_cons, 9)
+    ref.kkt_set_jacobian(jl)
+    K.set_jacobian(jl)
+    for dw, dc in DELTAS:
+        ref.kkt_assemble(hl, sx, ss, dw, dc)
+        K.assemble(hl, sx, ss, dw, dc)
+        a, m = K.values()
+        ar, mr = ref.kkt_values()
+        assert_bitexact(a, ar, "A")
+        assert_bitexact(m, mr, f"M dw={dw}")
     with pytest.raises(GridError) as e:
-        OpfNlp(net, 2, np.ones((2, net.n_load)))
-    assert e.value.code == 4
+        K.update_x(x, w, 1.0, sx, ss, 0.0, 0.0)
+    assert e.value.code == GN_ERR_UNSUPPORTED
+    K.close()
 
 
 def test_compress_to_csc_known_answer_gpu(gpu):
