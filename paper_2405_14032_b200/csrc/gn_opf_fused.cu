@@ -187,8 +187,14 @@ __global__ void __launch_bounds__(256) k_fz_dvec(int32_t m, const double* __rest
 #define GN_FLW 4
 #endif
 constexpr int kFLW = GN_FLW;  // warps per CTA
+// flow-column kernel: flat (line, period) lanes when T is not a multiple of 32 (no idle lanes:
+// 9241 x 48 -12%, a 21-period shard -16%), a warp per (line, 32 periods) otherwise (flat costs
+// 2% at 96 periods: prefix sums, per-lane descriptors).  GN_FL_FLAT=0: never flat.
+#ifndef GN_FL_FLAT
+#define GN_FL_FLAT 1
+#endif
 constexpr int kFLCap = 16;  // staged slots per column (longer columns are written in place)
-template <bool STRUCT>
+template <bool STRUCT, bool FLAT = false>
 __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
                                              const double* __restrict__ x,
                                              const double* __restrict__ w,
@@ -201,11 +207,24 @@ __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t T = t.T;
   const int64_t wg = vblock * kFLW + warp;
-  const int32_t l = (int32_t)(wg / t.tchunks);
-  if (l >= t.L) return;  // warp-uniform
-  const int32_t c0 = (int32_t)(wg - (int64_t)l * t.tchunks) * 32;
-  const int32_t tt = c0 + lane, nt = min(32, T - c0);
-  const bool valid = lane < nt;
+  constexpr bool flat = !STRUCT && FLAT;
+  int32_t l, tt, c0 = 0, nt = 0;
+  bool valid;
+  if constexpr (flat) {  // lane = item 32 wg + lane of the flat (line, period) order
+    const int64_t nitems = (int64_t)t.L * T, item = wg * 32 + lane;
+    if (wg * 32 >= nitems) return;  // warp-uniform
+    valid = item < nitems;
+    const int64_t it = valid ? item : nitems - 1;
+    l = (int32_t)(it / T);
+    tt = (int32_t)(it - (int64_t)l * T);
+  } else {
+    l = (int32_t)(wg / t.tchunks);
+    if (l >= t.L) return;  // warp-uniform
+    c0 = (int32_t)(wg - (int64_t)l * t.tchunks) * 32;
+    tt = c0 + lane;
+    nt = min(32, T - c0);
+    valid = lane < nt;
+  }
   const int4 d0 = __ldg(t.ldesc0 + l), d1 = __ldg(t.ldesc1 + l);
   const int32_t f = d0.x, to = d0.y, k = d0.z, fl = d0.w;
   const int32_t blo = min(f, to), bhi = max(f, to);
@@ -238,8 +257,8 @@ __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
     return;
   }
   double* stg = stg_all + warp * (kFLCap * 33);
-  // ---- loads (every lane; invalid lanes clamp to the chunk's first period)
-  const int32_t ts = valid ? tt : c0, r = l * T + ts;
+  // ---- loads (every lane; invalid lanes clamp to the chunk's first period / the last item)
+  const int32_t ts = (flat || valid) ? tt : c0, r = l * T + ts;
   const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
   const double vf = x[t.v0 + f * T + ts], vt = x[t.v0 + to * T + ts];
   const double thf = x[t.th0 + f * T + ts], tht = x[t.th0 + to * T + ts];
@@ -257,7 +276,32 @@ __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
     dth = dval(t, dv, t.therm0 + k * T + ts);
   }
   const int2 cb = __ldg(t.lcb + l);
-  const int64_t basep = cb.x + (int64_t)c0 * lenp, baseq = cb.y + (int64_t)c0 * lenq;
+  int64_t basep = cb.x + (int64_t)c0 * lenp, baseq = cb.y + (int64_t)c0 * lenq;
+  // flat lanes: the warp's p (q) columns are still one contiguous span of M (the columns of
+  // consecutive (line, period) items are consecutive), with per-lane lengths -- staged in
+  // output order at an exclusive prefix sum of the lengths, flushed as one stream
+  int32_t offp = 0, offq = 0, totp = 0, totq = 0;
+  bool staged = lenp <= kFLCap && lenq <= kFLCap;
+  if constexpr (flat) {
+    constexpr unsigned kAll = 0xffffffffu;
+    const int32_t lp = valid ? lenp : 0, lq = valid ? lenq : 0;
+    int32_t sp = lp, sq = lq;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const int32_t a = __shfl_up_sync(kAll, sp, dd), b = __shfl_up_sync(kAll, sq, dd);
+      if (lane >= dd) {
+        sp += a;
+        sq += b;
+      }
+    }
+    offp = sp - lp;
+    offq = sq - lq;
+    totp = __shfl_sync(kAll, sp, 31);
+    totq = __shfl_sync(kAll, sq, 31);
+    basep = __shfl_sync(kAll, cb.x + (int64_t)tt * lenp, 0);
+    baseq = __shfl_sync(kAll, cb.y + (int64_t)tt * lenq, 0);
+    staged = __all_sync(kAll, staged);
+  }
   const LineState s = line_state(G, B, vf, vt, thf, tht);
   const double jtp = j_thermal(xp), jtq = j_thermal(xq);
   // ---- values, slot by slot; column p, then column q.  Staged (the common case:
@@ -267,8 +311,13 @@ __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
     for (int Q = 0; Q < 2; ++Q) {
       const int64_t pos = ST ? 0 : (valid ? (int64_t)__ldg(t.colptr + (Q ? cqs : cps)) : 0);
       auto put = [&](int32_t j, double v) {
-        if constexpr (ST) stg[j * 33 + lane] = v;
-        else if (valid) M[pos + j] = v;
+        if constexpr (ST && flat) {
+          if (valid) stg[(Q ? offq : offp) + j] = v;
+        } else if constexpr (ST) {
+          stg[j * 33 + lane] = v;
+        } else if (valid) {
+          M[pos + j] = v;
+        }
       };
       const double dlo = Q ? dbq_lo : dbp_lo, dhi = Q ? dbq_hi : dbp_hi, dfl = Q ? dfq : dfp;
       const double jt = Q ? jtq : jtp;
@@ -305,16 +354,24 @@ __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
         acc += pair_term(dfl, Q ? j_flow_q(s, G, B, field) : j_flow_p(s, G, B, field), 1.0);
         put(j++, acc);
       }
-      if constexpr (ST) warp_span_flush(M, Q ? baseq : basep, stg, Q ? lenq : lenp, nt, lane);
+      if constexpr (ST && flat) {
+        __syncwarp();
+        const int32_t tot = Q ? totq : totp;
+        double* o = M + (Q ? baseq : basep);
+        for (int32_t e = lane; e < tot; e += 32) o[e] = stg[e];
+        __syncwarp();
+      } else if constexpr (ST) {
+        warp_span_flush(M, Q ? baseq : basep, stg, Q ? lenq : lenp, nt, lane);
+      }
     }
   };
-  if (lenp <= kFLCap && lenq <= kFLCap) columns(std::true_type{});
+  if (staged) columns(std::true_type{});
   else columns(std::false_type{});
 }
 
 // Grid-stride wrapper: `nvb` virtual CTAs on at most gridDim.x resident CTAs (the grid can be
 // capped so that the latency-bound KKT kernels leave SM room for the callback stream).
-template <bool STRUCT>
+template <bool STRUCT, bool FLAT>
 __global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, int64_t nvb,
                                                       const double* __restrict__ x,
                                                       const double* __restrict__ w,
@@ -323,9 +380,9 @@ __global__ void __launch_bounds__(kFLW * 32) k_fz_line(OpfKktTab t, int64_t nvb,
                                                       double* __restrict__ M,
                                                       int32_t* __restrict__ rows,
                                                       int32_t* __restrict__ bad) {
-  fz_line_body<STRUCT>(blockIdx.x, t, x, w, sx, dw, dv, M, rows, bad);
+  fz_line_body<STRUCT, FLAT>(blockIdx.x, t, x, w, sx, dw, dv, M, rows, bad);
 }
-template <bool STRUCT>
+template <bool STRUCT, bool FLAT>
 __global__ void __launch_bounds__(kFLW * 32, GN_FL_GS_MINB) k_fz_line_gs(OpfKktTab t, int64_t nvb,
                                                          const double* __restrict__ x,
                                                          const double* __restrict__ w,
@@ -335,7 +392,7 @@ __global__ void __launch_bounds__(kFLW * 32, GN_FL_GS_MINB) k_fz_line_gs(OpfKktT
                                                          int32_t* __restrict__ rows,
                                                          int32_t* __restrict__ bad) {
   for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x)
-    fz_line_body<STRUCT>(vb, t, x, w, sx, dw, dv, M, rows, bad);
+    fz_line_body<STRUCT, FLAT>(vb, t, x, w, sx, dw, dv, M, rows, bad);
 }
 
 template <bool STRUCT>
@@ -414,6 +471,7 @@ __device__ __forceinline__ void sj_row(const OpfKktTab& t, int32_t r, const doub
 #define GN_SJW 8
 #endif
 constexpr int kSJW = GN_SJW;  // warps per CTA
+template <bool FLAT>
 __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t, int32_t m,
                                              const double* __restrict__ x,
                                              double* __restrict__ A, int skip_flow) {
@@ -442,8 +500,48 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
     return;
   }
   wg -= 2ll * t.N;
-  const int64_t nflow = skip_flow ? 0 : (int64_t)t.L * tch;
-  if (wg < nflow) {  // flow_p / flow_q rows of (line, 32 periods)
+  const int64_t nflow = skip_flow ? 0 : (FLAT ? ((int64_t)t.L * T + 31) / 32 : (int64_t)t.L * tch);
+  if (FLAT && wg < nflow) {  // flow_p / flow_q rows of 32 flat (line, period) items
+    constexpr unsigned kAll = 0xffffffffu;
+    double* stg = stg_all + warp * (5 * 33);
+    const int64_t nitems = (int64_t)t.L * T, item = wg * 32 + lane;
+    const bool valid = item < nitems;
+    const int64_t it = valid ? item : nitems - 1;
+    const int32_t l = (int32_t)(it / T), ts = (int32_t)(it - (int64_t)l * T);
+    const int4 d0 = __ldg(t.ldesc0 + l);
+    const int32_t f = d0.x, to = d0.y, len = 1 + __popc(d0.w & 15);
+    const double G = __ldg(t.lg + l), B = __ldg(t.lb + l);
+    const LineState s = line_state(G, B, x[t.v0 + f * T + ts], x[t.v0 + to * T + ts],
+                                   x[t.th0 + f * T + ts], x[t.th0 + to * T + ts]);
+    // consecutive items are consecutive CSR rows: one span per row type, per-lane lengths
+    const int32_t lv = valid ? len : 0;
+    int32_t sc = lv;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const int32_t a = __shfl_up_sync(kAll, sc, dd);
+      if (lane >= dd) sc += a;
+    }
+    const int32_t off = sc - lv, tot = __shfl_sync(kAll, sc, 31);
+    const int64_t bp = __shfl_sync(kAll, __ldg(t.rbase + 2 * t.N + l) + (int64_t)ts * len, 0);
+    const int64_t bq = __shfl_sync(kAll, __ldg(t.rbase + 2 * t.N + t.L + l) + (int64_t)ts * len, 0);
+    int pos[5];
+#pragma unroll
+    for (int fl = 0; fl < 5; ++fl) pos[fl] = __ldg(t.fpos + 5 * l + fl);
+#pragma unroll
+    for (int Q = 0; Q < 2; ++Q) {
+      if (valid) {
+#pragma unroll
+        for (int fl = 0; fl < 5; ++fl)
+          if (pos[fl] >= 0) stg[off + pos[fl]] = 0.0 + (Q ? j_flow_q(s, G, B, fl) : j_flow_p(s, G, B, fl));
+      }
+      __syncwarp();
+      double* o = A + (Q ? bq : bp);
+      for (int32_t e = lane; e < tot; e += 32) o[e] = stg[e];
+      __syncwarp();
+    }
+    return;
+  }
+  if (!FLAT && wg < nflow) {  // flow_p / flow_q rows of (line, 32 periods)
     double* stg = stg_all + warp * (5 * 33);
     const int32_t l = (int32_t)(wg / tch), c0 = (int32_t)(wg - (int64_t)l * tch) * 32;
     const int32_t nt = min(32, T - c0), ts = lane < nt ? c0 + lane : c0;
@@ -468,7 +566,19 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
     return;
   }
   wg -= nflow;
-  if (wg < LT) {  // thermal rows of thermal slot k, all periods: [p, q] -> (2p, 2q)
+  const int64_t nth = FLAT ? ((int64_t)LT * T + 31) / 32 : LT;
+  if (FLAT && wg < nth) {  // thermal rows of 32 flat (slot, period) items: (2p, 2q) each
+    const int64_t item = wg * 32 + lane;
+    if (item >= (int64_t)LT * T) return;
+    const int32_t k = (int32_t)(item / T), tt = (int32_t)(item - (int64_t)k * T);
+    const int32_t l = __ldg(t.th_line + k);
+    const double pv = x[t.p0 + (int64_t)l * T + tt], qv = x[t.q0 + (int64_t)l * T + tt];
+    double* dst = A + __ldg(t.rbase + 2 * t.N + 2 * t.L + k) + 2LL * tt;
+    dst[0] = 0.0 + j_thermal(pv);
+    dst[1] = 0.0 + j_thermal(qv);
+    return;
+  }
+  if (!FLAT && wg < LT) {  // thermal rows of thermal slot k, all periods: [p, q] -> (2p, 2q)
     const int32_t k = (int32_t)wg, l = __ldg(t.th_line + k);
     const int64_t base = __ldg(t.rbase + 2 * t.N + 2 * t.L + k);
     const double* xp = x + t.p0 + l * T;
@@ -493,7 +603,7 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
     }
     return;
   }
-  wg -= LT;
+  wg -= nth;
   if (wg < t.L) {  // angle rows of line l, all periods: [th_f, th_t] -> (1, -1)
     const int32_t l = (int32_t)wg;
     const int pf = __ldg(t.apos + 2 * l), pt = __ldg(t.apos + 2 * l + 1);
@@ -519,19 +629,21 @@ __device__ __forceinline__ void set_jac_body(int64_t vblock, const OpfKktTab& t,
   }
 }
 
+template <bool FLAT>
 __global__ void __launch_bounds__(kSJW * 32, GN_SJ_MINB) k_opf_set_jac_fused(OpfKktTab t, int64_t nvb,
                                                                 int32_t m,
                                                                 const double* __restrict__ x,
                                                                 double* __restrict__ A,
                                                                 int skip_flow) {
-  set_jac_body(blockIdx.x, t, m, x, A, skip_flow);
+  set_jac_body<FLAT>(blockIdx.x, t, m, x, A, skip_flow);
 }
+template <bool FLAT>
 __global__ void __launch_bounds__(kSJW * 32, GN_SJ_GS_MINB) k_opf_set_jac_fused_gs(OpfKktTab t, int64_t nvb,
                                                                    int32_t m,
                                                                    const double* __restrict__ x,
                                                                    double* __restrict__ A,
                                                                    int skip_flow) {
-  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) set_jac_body(vb, t, m, x, A, skip_flow);
+  for (int64_t vb = blockIdx.x; vb < nvb; vb += gridDim.x) set_jac_body<FLAT>(vb, t, m, x, A, skip_flow);
 }
 
 // ------------------------------------------------------------------ host
@@ -605,13 +717,21 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
   const int64_t nl = (int64_t)t.L * t.T, ng = (int64_t)t.G * t.T;
   if (nl > 0) {
     KTimer kt("k_fz_line", s);
-    const int64_t warps = (int64_t)t.L * t.tchunks;
+    const bool flat = !STRUCT && GN_FL_FLAT && (t.T % 32) != 0;
+    const int64_t warps = flat ? (nl + 31) / 32 : (int64_t)t.L * t.tchunks;
     const int64_t nvb = (warps + kFLW - 1) / kFLW;
     const unsigned g = grid_cap(nvb, t.grid_cap);
-    if (g < nvb)  // capped grid: the grid-stride variant
-      k_fz_line_gs<STRUCT><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
-    else
-      k_fz_line<STRUCT><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
+    if (flat) {
+      if (g < nvb)  // capped grid: the grid-stride variant
+        k_fz_line_gs<STRUCT, true><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
+      else
+        k_fz_line<STRUCT, true><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
+    } else {
+      if (g < nvb)
+        k_fz_line_gs<STRUCT, false><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
+      else
+        k_fz_line<STRUCT, false><<<g, kFLW * 32, 0, s>>>(t, nvb, in.x, in.w, in.sx, in.dw, dv, M, rows, bad);
+    }
     count_launch();
   }
   // the generator columns: on their own auxiliary lane beside the flow-column kernel for
@@ -666,14 +786,25 @@ static void set_jac_launch(gn_kkt* K, const double* x, int skip_flow, cudaStream
   {
     KTimer kt(skip_flow ? "k_opf_set_jac_fused<noflow>" : "k_opf_set_jac_fused", st);
     const int64_t LT = t.T > 0 ? (t.ang0 - t.therm0) / t.T : 0;
-    const int64_t warps = 2ll * t.N + (skip_flow ? 0 : (int64_t)t.L * t.tchunks) + LT + t.L +
-                          (K->m - t.ramp0 + 31) / 32;
+    // flat (entity, period) lanes for the flow and thermal rows when T leaves lanes idle
+    const bool flat = GN_FL_FLAT && (t.T % 32) != 0;
+    const int64_t nflow = skip_flow ? 0 : (flat ? ((int64_t)t.L * t.T + 31) / 32
+                                                : (int64_t)t.L * t.tchunks);
+    const int64_t nth = flat ? (LT * t.T + 31) / 32 : LT;
+    const int64_t warps = 2ll * t.N + nflow + nth + t.L + (K->m - t.ramp0 + 31) / 32;
     const int64_t nvb = (warps + kSJW - 1) / kSJW;
     const unsigned g = grid_cap(nvb, (GN_SJ_CAP > 0 && t.grid_cap > 0) ? GN_SJ_CAP : t.grid_cap);
-    if (g < nvb)
-      k_opf_set_jac_fused_gs<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
-    else
-      k_opf_set_jac_fused<<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
+    if (flat) {
+      if (g < nvb)
+        k_opf_set_jac_fused_gs<true><<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
+      else
+        k_opf_set_jac_fused<true><<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
+    } else {
+      if (g < nvb)
+        k_opf_set_jac_fused_gs<false><<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
+      else
+        k_opf_set_jac_fused<false><<<g, kSJW * 32, 0, st>>>(t, nvb, K->m, x, K->avals.p, skip_flow);
+    }
   }
   count_launch();
   GN_CK(cudaGetLastError());

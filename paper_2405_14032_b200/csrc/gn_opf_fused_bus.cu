@@ -37,6 +37,9 @@ namespace gnb {
 #ifndef GN_BW3
 #define GN_BW3 4
 #endif
+#ifndef GN_BUSR_FLAT
+#define GN_BUSR_FLAT 1  // register classes: flat (bus, period) lanes; 0: a warp per (bus, 32 t)
+#endif
 constexpr int kBW3 = GN_BW3;  // warps per CTA
 // resident CTAs per SM the register allocation of k_fz_busr<DEG> must allow
 // (per degree: overridable one by one in tuning builds, GN_BUSR_MINB_D<k>)
@@ -311,11 +314,20 @@ __device__ __forceinline__ void busr_body(int64_t vblock, const OpfKktTab& t,
                                           int32_t* __restrict__ bad) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t w = vblock * kBW3 + warp;
+  const int32_t T = t.T;
+#if GN_BUSR_FLAT
+  // flat (bus, period) items: lane i of warp w takes item 32 w + i, so no lane idles when T
+  // is not a multiple of 32 (a period shard of 21, configs[1]'s 24, configs[2]'s 48)
+  const int64_t item = w * 32 + lane;
+  const int64_t n64 = item / T;
+  if (n64 >= n_buses) return;
+  const int32_t tt = (int32_t)(item - n64 * T);
+#else
   const int64_t n64 = w / t.tchunks;
   if (n64 >= n_buses) return;
-  const int32_t T = t.T;
   const int32_t tt = (int32_t)(w - n64 * t.tchunks) * 32 + lane;
   if (tt >= T) return;
+#endif
   const int4* bd = buses + (int64_t)bus_desc_stride(DEG - 1) * n64;
   const int4 bd0 = __ldg(bd), bd1 = __ldg(bd + 1), bd2 = __ldg(bd + 2);
   int2 e[DEG];
@@ -488,7 +500,11 @@ static void launch_busr(const OpfKktTab& t, const int4* buses, int32_t n_buses, 
                         const double* dv, double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
   static const char* names[] = {"", "k_fz_busr<d1>", "k_fz_busr<d2>", "k_fz_busr<d3>",
                                 "k_fz_busr<d4>", "k_fz_busr<d5>", "k_fz_busr<d6>"};
+#if GN_BUSR_FLAT
+  const int64_t warps = ((int64_t)n_buses * t.T + 31) / 32;
+#else
   const int64_t warps = (int64_t)n_buses * t.tchunks;
+#endif
   const int64_t nvb = (warps + kBW3 - 1) / kBW3;
   KTimer kt(names[DEG], s);
   if (rows)
