@@ -25,6 +25,12 @@
 
 namespace gnb {
 
+// one slot-program launch for every bus the register classes do not take (parallel lines,
+// degree > 6): its ~20 us latency floor is paid once, not per class (0: <= 8 / rest split)
+#ifndef GN_BUS3_MERGE
+#define GN_BUS3_MERGE 1
+#endif
+
 constexpr int kMB = 128;  // threads (columns) per CTA
 
 struct In {
@@ -867,10 +873,11 @@ bool opf_kkt_prepare(gn_kkt* K) {
       if (simple) {
         cls[deg - 1].push_back(make_int4(n, bl_ptr[n], deg, boff_n));
       } else {
-        cls[deg <= 8 ? kBusClasses - 2 : kBusClasses - 1].push_back(
+        cls[(deg <= 8 && !GN_BUS3_MERGE) ? kBusClasses - 2 : kBusClasses - 1].push_back(
             make_int4(n, bl_ptr[n], deg | (np << 8), bprog_ptr[n]));
       }
-      auto& v = simple ? cls[deg - 1] : cls[deg <= 8 ? kBusClasses - 2 : kBusClasses - 1];
+      auto& v = simple ? cls[deg - 1]
+                       : cls[(deg <= 8 && !GN_BUS3_MERGE) ? kBusClasses - 2 : kBusClasses - 1];
       const int32_t kv = lent[offs[C_V] + n], kt = lent[offs[C_TH] + n];
       int32_t bv, lv, bt, lt;
       colspan(kv, bv, lv);
