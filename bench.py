@@ -487,15 +487,15 @@ def run_ours(args, rank, world, local_rank, dist):
             else:
                 nlp.eval_device(name, dx, {"f": f, "grad": grad, "g": g, "jac": J}[name],
                                 sync=False)
+            if name == "f" and world > 1:  # the global objective: shard partials in rank
+                with torch.cuda.stream(stream):  # order, right behind f (off the tail)
+                    if peer is not None:
+                        peer.objective(f, f_global, DeviceHalo.BOTH, stream.cuda_stream)
+                    else:
+                        from paper_2405_14032_b200.shard import global_objective
+                        f_global.copy_(global_objective(f, world))
             if name in cb_mark:
                 mark(cb_mark[name])
-        if world > 1:  # the global objective: shard partials added in rank order
-            with torch.cuda.stream(stream):
-                if peer is not None:
-                    peer.objective(f, f_global, DeviceHalo.BOTH, stream.cuda_stream)
-                else:
-                    from paper_2405_14032_b200.shard import global_objective
-                    f_global.copy_(global_objective(f, world))
         if after_cb is not None:
             after_cb()
         if fused and ks is not stream:
