@@ -4,7 +4,7 @@
 // CPU thread at a time; here it goes through two pinned bounce buffers in chunks instead:
 // the host-side copies are split over a few threads and overlap the DMA of the neighbouring
 // chunk (PCIe is not idle while the CPU copies).  Caller memory that is already pinned
-// (cudaHostAlloc / cudaHostRegister) is DMA'd directly.  Both calls return when the copy is
+// (cudaHostAlloc / cudaHostRegister), or device memory, is copied directly.  Both calls return when the copy is
 // complete, as the host modes require.
 #include <condition_variable>
 #include <cstring>
@@ -121,21 +121,23 @@ Bounce& bounce_for(int dev) {
   return *per[dev];
 }
 
-bool pinned(const void* p) {
+// Memory the copy engine can address directly: pinned host, device or managed memory (a
+// device pointer handed to a host mode by mistake is then still copied correctly).
+bool direct(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
     cudaGetLastError();
     return false;
   }
-  return a.type == cudaMemoryTypeHost;
+  return a.type != cudaMemoryTypeUnregistered;
 }
 
 }  // namespace
 
 void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
-  if (bytes <= kDirect || pinned(src)) {
-    GN_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+  if (bytes <= kDirect || direct(src)) {
+    GN_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
     GN_CK(cudaStreamSynchronize(s));
     return;
   }
@@ -160,8 +162,8 @@ void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 
 void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
   if (bytes == 0) return;
-  if (bytes <= kDirect || pinned(dst)) {
-    GN_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+  if (bytes <= kDirect || direct(dst)) {
+    GN_CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s));
     GN_CK(cudaStreamSynchronize(s));
     return;
   }
