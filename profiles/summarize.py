@@ -48,9 +48,9 @@ def pretty(name: str) -> str:
     if mm:
         return f"k_fz_busr<d{mm.group(1)}>"
     for k in ("k_fz_bus3", "k_fz_line", "k_fz_gen", "k_opf_assemble"):
-        if n == k + "<0>":
+        if n == k + "<0>" or n.startswith(k + "<0, "):  # (k_fz_line<STRUCT, FLAT>)
             return k
-        if n == k + "<1>":
+        if n == k + "<1>" or n.startswith(k + "<1, "):
             return k + " (structure check)"
     return n
 
@@ -103,7 +103,8 @@ def full(rep: str, out: str, traffic_json: str | None = None):
     for r in rows[2:]:
         name = pretty(short(r[head.index("Kernel Name")]))
         seen[name] = seen.get(name, 0) + 1
-        if seen[name] > 1:  # e.g. one launch per degree class
+        first = seen[name] == 1
+        if not first:  # the capture window reached into the next step: table only
             name = f"{name} #{seen[name]}"
         cells = []
         for key, _ in KEYS:
@@ -116,7 +117,8 @@ def full(rep: str, out: str, traffic_json: str | None = None):
         try:
             rd = float(r[head.index("dram__bytes_read.sum")]) * _scale(units[head.index("dram__bytes_read.sum")])
             wr = float(r[head.index("dram__bytes_write.sum")]) * _scale(units[head.index("dram__bytes_write.sum")])
-            traffic[name] = rd + wr
+            if first:
+                traffic[name] = rd + wr
         except (ValueError, IndexError):
             pass
     open(out, "w").write("\n".join(lines) + "\n")
