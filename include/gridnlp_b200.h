@@ -29,6 +29,7 @@
 #ifndef GRIDNLP_B200_H
 #define GRIDNLP_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -229,6 +230,22 @@ int gn_lifted_structure(gn_ctx* ctx, int32_t* free_to_full, int32_t* jac_rows,
 int gn_lifted_gather_jac(gn_ctx* ctx, const double* jac_full, double* jac_lifted, int mem);
 int gn_lifted_gather_hess(gn_ctx* ctx, const double* hess_full, double* hess_lifted,
                           int mem);
+/* LiftedProblem::eval_f / eval_grad / eval_g / eval_jac / eval_hess (lifted.hpp:128-159)
+ * in one call each: x is the FREE-variable vector [n_free]; it is staged into the full
+ * space on the device (fixed entries at their pinned values, lifted.hpp:35-45, 165-168),
+ * the callback runs, and grad [n_free], J [jac_nnz_lifted] and H [hess_nnz_lifted] come
+ * back already gathered (f and g [n_cons] are not lifted).  Errors as gn_eval_*.  The
+ * shim LiftedProblem (include/gridnlp_b200/shim/gridnlp/ipm/lifted.hpp) calls these for a
+ * CudaOpfNlp.  A period shard returns GN_ERR_UNSUPPORTED (its ghost set-points hold halo
+ * values: use the full-space calls). */
+int gn_lifted_eval_f(gn_ctx* ctx, const double* x_free, double* out, int mem, gn_error* err);
+int gn_lifted_eval_grad(gn_ctx* ctx, const double* x_free, double* out, int mem, gn_error* err);
+int gn_lifted_eval_g(gn_ctx* ctx, const double* x_free, double* out, int mem, gn_error* err);
+int gn_lifted_eval_jac(gn_ctx* ctx, const double* x_free, double* out, int mem, gn_error* err);
+int gn_lifted_eval_hess(gn_ctx* ctx, const double* x_free, const double* row_weights,
+                        double obj_weight, double* out, int mem, gn_error* err);
+int gn_lifted_eval_fg(gn_ctx* ctx, const double* x_free, double* f, double* g, int mem,
+                      gn_error* err);
 
 /* ------------------------------------------------------------ condensed KKT */
 /* CondensedKkt constructor structure (condensed.hpp:29-90) on an arbitrary
@@ -362,6 +379,12 @@ int gn_kkt_solve_finish(gn_ipm* ipm, const double* dx, const double* qs, const d
  * still holding the pattern (never written), A guard words changed (overrun), the same for
  * M}.  An assembly between the two calls must leave {0, 0, 0, 0}. */
 int gn_debug_kkt_guard(gn_kkt* kkt, int fill, uint64_t pattern, int64_t* out4);
+
+/* Page-locked host memory for host-mode outputs and inputs (cudaHostAlloc, portable):
+ * GN_MEM_HOST transfers from / to it run as direct DMA, without the bounce-buffer copy
+ * pageable memory needs.  The shim CondensedKkt keeps its A and M values in it. */
+int gn_host_alloc(size_t bytes, void** out);
+int gn_host_free(void* p);
 
 #ifdef __cplusplus
 }

@@ -161,6 +161,61 @@ class CudaOpfNlp final : public gridnlp::ipm::NlpProblem {
     return record(gn_eval_hess(ctx_, x.data(), w.data(), ow, out.data(), GN_MEM_HOST, &err_));
   }
 
+  // ---- the lifted problem on the device, for the shim ipm::LiftedProblem
+  // (shim/gridnlp/ipm/lifted.hpp): the fixed-variable filter of lifted.hpp:25-100 is
+  // built by the library; x is the free-variable vector and J / H come back lifted.
+  struct Lifted {
+    std::vector<gridnlp::index_t> free_to_full, jac_rows, jac_cols, hess_rows, hess_cols;
+  };
+  Lifted lift(double relax) {
+    gn_error err{};
+    if (gn_lifted_create(ctx_, relax, &err) != GN_OK)
+      throw gridnlp::Error(std::string("gn_lifted_create: ") + err.message);
+    gn_sizes s{};
+    gn_ctx_sizes(ctx_, &s);
+    nf_ = static_cast<size_t>(s.n_free);
+    njl_ = static_cast<size_t>(s.jac_nnz_lifted);
+    nhl_ = static_cast<size_t>(s.hess_nnz_lifted);
+    Lifted L;
+    L.free_to_full.resize(nf_);
+    L.jac_rows.resize(njl_);
+    L.jac_cols.resize(njl_);
+    L.hess_rows.resize(nhl_);
+    L.hess_cols.resize(nhl_);
+    if (gn_lifted_structure(ctx_, L.free_to_full.data(), L.jac_rows.data(), L.jac_cols.data(),
+                            nullptr, L.hess_rows.data(), L.hess_cols.data(), nullptr, nullptr,
+                            nullptr, GN_MEM_HOST) != GN_OK)
+      throw gridnlp::Error("gn_lifted_structure failed");
+    return L;
+  }
+  bool lifted_eval_f(std::span<const double> x, double& out) {
+    check(x.size(), nf_, "lifted eval_f: bad x size");
+    return record(gn_lifted_eval_f(ctx_, x.data(), &out, GN_MEM_HOST, &err_));
+  }
+  bool lifted_eval_grad(std::span<const double> x, std::span<double> out) {
+    check(x.size(), nf_, "lifted eval_grad: bad x size");
+    check(out.size(), nf_, "lifted eval_grad: bad output size");
+    return record(gn_lifted_eval_grad(ctx_, x.data(), out.data(), GN_MEM_HOST, &err_));
+  }
+  bool lifted_eval_g(std::span<const double> x, std::span<double> out) {
+    check(x.size(), nf_, "lifted eval_g: bad x size");
+    check(out.size(), m_, "lifted eval_g: bad output size");
+    return record(gn_lifted_eval_g(ctx_, x.data(), out.data(), GN_MEM_HOST, &err_));
+  }
+  bool lifted_eval_jac(std::span<const double> x, std::span<double> out) {
+    check(x.size(), nf_, "lifted eval_jac: bad x size");
+    check(out.size(), njl_, "lifted eval_jac: bad output size");
+    return record(gn_lifted_eval_jac(ctx_, x.data(), out.data(), GN_MEM_HOST, &err_));
+  }
+  bool lifted_eval_hess(std::span<const double> x, std::span<const double> w, double ow,
+                        std::span<double> out) {
+    check(x.size(), nf_, "lifted eval_hess: bad x size");
+    check(w.size(), m_, "lifted eval_hess: bad weight size");
+    check(out.size(), nhl_, "lifted eval_hess: bad output size");
+    return record(gn_lifted_eval_hess(ctx_, x.data(), w.data(), ow, out.data(), GN_MEM_HOST,
+                                      &err_));
+  }
+
   // Diagnostic for the most recent failed evaluation (pattern_nlp.hpp:51-58).
   const std::string& last_failure() const { return last_failure_; }
   int last_failure_pattern() const { return err_.pattern; }
@@ -183,6 +238,7 @@ class CudaOpfNlp final : public gridnlp::ipm::NlpProblem {
   gn_ctx* ctx_ = nullptr;
   gn_error err_{};
   gridnlp::index_t n_ = 0, m_ = 0;
+  size_t nf_ = 0, njl_ = 0, nhl_ = 0;  // lifted sizes (after lift())
   std::vector<double> xl_, xu_, xs_, rl_, ru_;
   std::vector<gridnlp::index_t> jr_, jc_, hr_, hc_;
   std::vector<double> bus_vmin_, bus_vmax_, lg_, lb_, ls_, la_, lA_;

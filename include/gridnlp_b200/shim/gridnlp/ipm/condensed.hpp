@@ -22,6 +22,7 @@
 #include <optional>
 #include <span>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "gridnlp/common.hpp"
@@ -36,6 +37,49 @@ namespace gridnlp::ipm {
 
 // (not in the reference) KKTs built by this process: [generic, OPF-specialised]
 inline long b200_kkt_counts[2] = {0, 0};
+
+// (not in the reference) the A and M values the GPU returns every iteration, kept in
+// page-locked memory (gn_host_alloc) so their device->host copies are direct DMA; plain
+// heap memory when the pinned allocation fails (same values, slower copies).
+class B200HostValues {
+ public:
+  B200HostValues() = default;
+  explicit B200HostValues(size_t n) : n_(n) {
+    void* p = nullptr;
+    if (n && gn_host_alloc(n * sizeof(double), &p) == GN_OK && p) {
+      p_ = static_cast<double*>(p);
+      pinned_ = true;
+    } else if (n) {
+      p_ = new double[n];
+    }
+    std::fill(p_, p_ + n_, 0.0);
+  }
+  ~B200HostValues() { release(); }
+  B200HostValues(const B200HostValues&) = delete;
+  B200HostValues& operator=(const B200HostValues&) = delete;
+  B200HostValues& operator=(B200HostValues&& o) noexcept {
+    release();
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    std::swap(pinned_, o.pinned_);
+    return *this;
+  }
+  double* data() { return p_; }
+  size_t size() const { return n_; }
+  operator std::span<const double>() const { return {p_, n_}; }
+
+ private:
+  void release() {
+    if (pinned_) gn_host_free(p_);
+    else delete[] p_;
+    p_ = nullptr;
+    n_ = 0;
+    pinned_ = false;
+  }
+  double* p_ = nullptr;
+  size_t n_ = 0;
+  bool pinned_ = false;
+};
 
 class CondensedKkt {
  public:
@@ -60,8 +104,8 @@ class CondensedKkt {
     mpat_.rowidx.resize(static_cast<size_t>(dims[2]));
     gn_kkt_structure(kkt_, a_.rowptr.data(), a_.colidx.data(), mpat_.colptr.data(),
                      mpat_.rowidx.data(), GN_MEM_HOST);
-    a_vals_.assign(a_.colidx.size(), 0.0);
-    mvals_.assign(mpat_.rowidx.size(), 0.0);
+    a_vals_ = B200HostValues(a_.colidx.size());
+    mvals_ = B200HostValues(mpat_.rowidx.size());
     ldlt_opts_ = ldlt_opts;
     int64_t d2[9] = {};
     gn_kkt_dims(kkt_, d2);
@@ -88,9 +132,9 @@ class CondensedKkt {
 
   // A = scatter(J) on the GPU; the values come back for the host solves.
   void set_jacobian(std::span<const double> jac_vals) {
-    if (gn_kkt_set_jacobian(kkt_, jac_vals.data(), GN_MEM_HOST) != GN_OK)
+    if (gn_kkt_set_jacobian(kkt_, jac_vals.data(), GN_MEM_HOST) != GN_OK ||
+        gn_kkt_values(kkt_, a_vals_.data(), nullptr, GN_MEM_HOST) != GN_OK)
       throw Error("CondensedKkt::set_jacobian (gridnlp_b200) failed");
-    gn_kkt_values(kkt_, a_vals_.data(), nullptr, GN_MEM_HOST);
   }
 
   // M = W + dw I + Sx + At D A on the GPU; the per-row C/D factors the solve
@@ -98,6 +142,13 @@ class CondensedKkt {
   void assemble(std::span<const double> hess_vals, std::span<const double> sigma_x,
                 std::span<const double> sigma_s, double delta_w, double delta_c) {
     delta_c_ = delta_c;
+    // the GPU call (uploads, assembly, M back) runs beside the host's per-row factors
+    int rc = GN_OK;
+    std::thread gpu([&] {
+      rc = gn_kkt_assemble(kkt_, hess_vals.data(), sigma_x.data(), sigma_s.data(), delta_w,
+                           delta_c, GN_MEM_HOST);
+      if (rc == GN_OK) rc = gn_kkt_values(kkt_, nullptr, mvals_.data(), GN_MEM_HOST);
+    });
     for (index_t i = 0; i < m_; ++i) {
       const size_t u = static_cast<size_t>(i);
       const double sd = sigma_s[u] + delta_w;
@@ -106,10 +157,8 @@ class CondensedKkt {
       dvec_[u] = sd * c;
       sig_dw_[u] = sd;
     }
-    if (gn_kkt_assemble(kkt_, hess_vals.data(), sigma_x.data(), sigma_s.data(), delta_w,
-                        delta_c, GN_MEM_HOST) != GN_OK)
-      throw Error("CondensedKkt::assemble (gridnlp_b200) failed");
-    gn_kkt_values(kkt_, nullptr, mvals_.data(), GN_MEM_HOST);
+    gpu.join();
+    if (rc != GN_OK) throw Error("CondensedKkt::assemble (gridnlp_b200) failed");
   }
 
   bool factorize() {
@@ -159,9 +208,9 @@ class CondensedKkt {
   sparse::LdltOptions ldlt_opts_{};
   index_t n_, m_;
   sparse::CsrPattern a_;
-  std::vector<double> a_vals_;
+  B200HostValues a_vals_;
   sparse::CscPattern mpat_;
-  std::vector<double> mvals_;
+  B200HostValues mvals_;
   mutable std::optional<sparse::LdltSolver> ldlt_;
   std::vector<double> cvec_, dvec_, sig_dw_, tm_, rhs_;
   double delta_c_ = 0.0;

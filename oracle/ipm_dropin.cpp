@@ -7,7 +7,9 @@
 //   --nlp ref  : the reference's PatternNlp (CPU tape callbacks)
 // In both cases the condensed KKT is the shim CondensedKkt
 // (include/gridnlp_b200/shim, found first on the include path), i.e. the B200
-// set_jacobian/assemble feeding the reference LDL^T.  Prints one JSON line.
+// set_jacobian/assemble feeding the reference LDL^T, and the lifted problem is the shim
+// LiftedProblem (device gathers over CudaOpfNlp; the reference's own class over
+// PatternNlp and the restoration problem).  Prints one JSON line.
 //
 // Input: a binary network file written by tests/test_dropin.py (SoA arrays
 // in the order of gn_network, then the T x n_load demand table).
@@ -30,6 +32,9 @@
 
 #ifndef GRIDNLP_B200_CONDENSED_SHIM
 #error "the shim condensed.hpp must shadow the reference header"
+#endif
+#ifndef GRIDNLP_B200_LIFTED_SHIM
+#error "the shim lifted.hpp must shadow the reference header"
 #endif
 
 using namespace gridnlp;
@@ -70,9 +75,11 @@ int main(int argc, char** argv) {
     }
     std::printf("{\"nlp\": \"%s\", \"iterations\": %d, \"objective\": %.17g, \"status\": \"%s\", "
                 "\"restorations\": %d, \"seconds\": %.6f, \"warm_seconds\": %.6f, "
-                "\"kkt_generic\": %ld, \"kkt_specialised\": %ld}\n",
+                "\"kkt_generic\": %ld, \"kkt_specialised\": %ld, \"lifted_host\": %ld, "
+                "\"lifted_device\": %ld}\n",
                 which.c_str(), r.iterations, r.objective, ipm::to_string(r.status),
-                r.restorations, secs, warm, ipm::b200_kkt_counts[0], ipm::b200_kkt_counts[1]);
+                r.restorations, secs, warm, ipm::b200_kkt_counts[0], ipm::b200_kkt_counts[1],
+                ipm::b200_lifted_counts[0], ipm::b200_lifted_counts[1]);
     return 0;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());

@@ -1,9 +1,10 @@
 // oracle/seam_bench.cpp -- time the drop-in seams themselves (bench infrastructure).
 //
 // One IPM iteration's hot-path unit through the reference's OWN interfaces, exactly as
-// ipm::IpmSolver drives them (solver.hpp:139-141, 157-158, 200-228): the unmodified
-// LiftedProblem (lifted.hpp) over the NlpProblem, then the CondensedKkt the solver
-// constructs from the lifted COO arrays --
+// ipm::IpmSolver drives them (solver.hpp:139-141, 157-158, 200-228): the LiftedProblem
+// (the shim: device gathers over CudaOpfNlp; with GRIDNLP_B200_HOST_LIFTED=1 the
+// reference's own class, host gathers) over the NlpProblem, then the CondensedKkt the
+// solver constructs from the lifted COO arrays --
 //     lifted.eval_f / eval_grad / eval_g / eval_jac / eval_hess(x, -y, 1)
 //     kkt.set_jacobian(J_l); kkt.assemble(H_l, Sigma_x, Sigma_s, dw, dc)
 // with std::vector (pageable host) spans, as the reference passes them.  The problem is
@@ -30,6 +31,9 @@
 
 #ifndef GRIDNLP_B200_CONDENSED_SHIM
 #error "the shim condensed.hpp must shadow the reference header"
+#endif
+#ifndef GRIDNLP_B200_LIFTED_SHIM
+#error "the shim lifted.hpp must shadow the reference header"
 #endif
 
 using namespace gridnlp;
@@ -92,9 +96,10 @@ static int run(Nlp& nlp, const char* which, int units) {
                   mn = static_cast<long long>(kkt.values().size());
   std::printf("{\"nlp\": \"%s\", \"units\": %d, \"ms_per_unit\": %.6f, \"callbacks_ms\": %.6f, "
               "\"kkt_ms\": %.6f, \"setup_s\": %.3f, \"nnz_per_unit\": %lld, \"J\": %lld, "
-              "\"H\": %lld, \"M\": %lld, \"kkt_specialised\": %d}\n",
+              "\"H\": %lld, \"M\": %lld, \"kkt_specialised\": %d, \"lifted_device\": %d}\n",
               which, units, 1e3 * med(tu), 1e3 * med(tcb), 1e3 * med(tkkt), setup,
-              nj + nh + mn, nj, nh, mn, kkt.b200_specialised() ? 1 : 0);
+              nj + nh + mn, nj, nh, mn, kkt.b200_specialised() ? 1 : 0,
+              lifted.b200_device() ? 1 : 0);
   return 0;
 }
 

@@ -85,6 +85,8 @@ _SIGS = {
     "gn_ctx_destroy": (C.c_int, [vp]),
     "gn_ctx_publish": (C.c_int, [vp, C.c_int]),
     "gn_debug_kkt_guard": (C.c_int, [vp, C.c_int, C.c_uint64, i64p]),
+    "gn_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
+    "gn_host_free": (C.c_int, [vp]),
     "gn_halo_create": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp), C.POINTER(GnError)]),
     "gn_halo_ipc_handle": (C.c_int, [vp, vp]),
     "gn_halo_open": (C.c_int, [vp, vp]),
@@ -134,6 +136,13 @@ _SIGS = {
                                       f64p, C.c_int]),
     "gn_lifted_gather_jac": (C.c_int, [vp, f64p, f64p, C.c_int]),
     "gn_lifted_gather_hess": (C.c_int, [vp, f64p, f64p, C.c_int]),
+    "gn_lifted_eval_f": (C.c_int, [vp, f64p, f64p, C.c_int, C.POINTER(GnError)]),
+    "gn_lifted_eval_grad": (C.c_int, [vp, f64p, f64p, C.c_int, C.POINTER(GnError)]),
+    "gn_lifted_eval_g": (C.c_int, [vp, f64p, f64p, C.c_int, C.POINTER(GnError)]),
+    "gn_lifted_eval_jac": (C.c_int, [vp, f64p, f64p, C.c_int, C.POINTER(GnError)]),
+    "gn_lifted_eval_hess": (C.c_int, [vp, f64p, f64p, C.c_double, f64p, C.c_int,
+                                      C.POINTER(GnError)]),
+    "gn_lifted_eval_fg": (C.c_int, [vp, f64p, f64p, f64p, C.c_int, C.POINTER(GnError)]),
     "gn_kkt_create": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, i32p, i32p, C.c_int64, i32p,
                                 i32p, C.c_int32, C.POINTER(vp), C.POINTER(GnError)]),
     "gn_kkt_create_lifted": (C.c_int, [vp, C.POINTER(vp), C.POINTER(GnError)]),

@@ -563,7 +563,9 @@ int gn_lifted_create(gn_ctx* c, double relax, gn_error* err) {
   if (!c) return fail(err, GN_ERR_INVALID, "null context");
   API_TRY
   set_device(c->device);
-  gnb::build_lifted(c);
+  // the filter does not depend on relax (only the slack boxes do): built once, so KKTs
+  // already built on this context's lifted arrays (gn_ctx_publish) keep them
+  if (!c->lifted) gnb::build_lifted(c);
   c->relax = relax;
   return ok(err);
   API_CATCH(err)
@@ -634,6 +636,111 @@ int gn_lifted_gather_jac(gn_ctx* c, const double* in, double* out, int mem) {
 }
 int gn_lifted_gather_hess(gn_ctx* c, const double* in, double* out, int mem) {
   return lifted_gather(c, false, in, out, mem);
+}
+
+// x_full[full_of_free[k]] = x_free[k]: LiftedProblem::stage (lifted.hpp:165-168) on the device
+__global__ void k_lift_stage(int64_t n, const int32_t* __restrict__ full_of_free,
+                             const double* __restrict__ x_free, double* __restrict__ x_full) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) x_full[full_of_free[k]] = x_free[k];
+}
+
+// LiftedProblem::eval_* (lifted.hpp:128-159) in one call on the device: the free-variable
+// point is staged into the full space (fixed entries at their pinned values, the
+// reference's fixed_value_), the full-space callback runs, and the lifted outputs are
+// gathered on the device -- only lifted-size arrays cross PCIe in the host modes.
+static int lifted_eval(gn_ctx* c, int mode, const double* x, const double* w, double ow,
+                       double* out, double* fout, int mem, gn_error* err) {
+  if (!c) return fail(err, GN_ERR_INVALID, "null context");
+  if (!c->lifted) return fail(err, GN_ERR_INVALID, "gn_lifted_create must run first");
+  if (!x || !out || (mode == gnb::EV_H && !w) || (mode == gnb::EV_FG && !fout))
+    return fail(err, GN_ERR_INVALID, "null array");
+  if (c->d.n != c->d.n_base)  // ghost set-points hold halo values the staging cannot know
+    return fail(err, GN_ERR_UNSUPPORTED,
+                "lifted evaluation of a period shard: use the full-space calls with the halo");
+  API_TRY
+  set_device(c->device);
+  const auto& d = c->d;
+  cudaStream_t s = c->stream;
+  if (!c->lx_ready) {  // fixed_value_: xl where xl == xu (lifted.hpp:35-45), else overwritten
+    std::vector<double> xl(d.n), xu(d.n);
+    gnb::host_bounds(c, xl.data(), xu.data(), nullptr, nullptr, nullptr);
+    for (int64_t i = 0; i < d.n; ++i) xl[i] = xl[i] == xu[i] ? xl[i] : 0.0;
+    c->lx.upload(xl.data(), d.n, s);
+    c->lx_ready = true;
+  }
+  const int64_t nf = c->n_free;
+  const double* dxf = x;
+  if (!is_device(mem)) {
+    c->lxin.upload(x, nf, s);
+    dxf = c->lxin.p;
+  }
+  if (nf) {
+    k_lift_stage<<<(unsigned)((nf + 255) / 256), 256, 0, s>>>(nf, c->full_of_free.p, dxf, c->lx.p);
+    gnb::count_launch();
+  }
+  const double* dw = w;
+  if (mode == gnb::EV_H && !is_device(mem)) {
+    c->sw.upload(w, d.m, s);
+    dw = c->sw.p;
+  }
+  // full-space output; f and g are not lifted (rows keep their numbering)
+  const bool gathered = mode == gnb::EV_GRAD || mode == gnb::EV_J || mode == gnb::EV_H;
+  const int64_t nfull = mode == gnb::EV_F ? 1 : mode == gnb::EV_GRAD ? d.n
+                        : mode == gnb::EV_J ? d.nj : mode == gnb::EV_H ? d.nh : d.m + 1;
+  const int64_t nout = mode == gnb::EV_GRAD ? nf : mode == gnb::EV_J ? c->nj_l
+                       : mode == gnb::EV_H ? c->nh_l : mode == gnb::EV_F ? 1 : d.m;
+  double* dfull = out;
+  if (gathered || !is_device(mem)) {
+    if (c->sout.n < static_cast<size_t>(nfull)) c->sout.alloc(nfull);
+    dfull = c->sout.p;
+  }
+  double* df = mode == gnb::EV_FG ? (is_device(mem) ? fout : c->sout.p + d.m) : nullptr;
+  if (!is_async(mem))
+    GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof(unsigned long long), s));
+  gnb::launch_eval(mode, d, c->net(), c->lx.p, dw, ow, dfull, c->fpart.p, c->status.p, s, df);
+  double* dout = dfull;
+  if (gathered) {
+    const int32_t* pick = mode == gnb::EV_GRAD ? c->full_of_free.p
+                          : mode == gnb::EV_J ? c->jpick.p : c->hpick.p;
+    dout = out;
+    if (!is_device(mem)) {
+      if (c->lout.n < static_cast<size_t>(nout) + 1) c->lout.alloc(nout + 1);
+      dout = c->lout.p;
+    }
+    if (nout) {
+      k_gather<<<(unsigned)((nout + 255) / 256), 256, 0, s>>>(nout, pick, dfull, dout);
+      gnb::count_launch();
+    }
+  }
+  if (is_async(mem)) return ok(err);
+  if (!is_device(mem)) {
+    gnb::d2h(out, dout, sizeof(double) * nout, s);
+    if (mode == gnb::EV_FG) gnb::d2h(fout, df, sizeof(double), s);
+  }
+  return take_status(c, err);
+  API_CATCH(err)
+}
+
+int gn_lifted_eval_f(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return lifted_eval(c, gnb::EV_F, x, nullptr, 0.0, out, nullptr, mem, err);
+}
+int gn_lifted_eval_grad(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return lifted_eval(c, gnb::EV_GRAD, x, nullptr, 0.0, out, nullptr, mem, err);
+}
+int gn_lifted_eval_g(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return lifted_eval(c, gnb::EV_G, x, nullptr, 0.0, out, nullptr, mem, err);
+}
+int gn_lifted_eval_jac(gn_ctx* c, const double* x, double* out, int mem, gn_error* err) {
+  return lifted_eval(c, gnb::EV_J, x, nullptr, 0.0, out, nullptr, mem, err);
+}
+int gn_lifted_eval_hess(gn_ctx* c, const double* x, const double* w, double ow, double* out,
+                        int mem, gn_error* err) {
+  return lifted_eval(c, gnb::EV_H, x, w, ow, out, nullptr, mem, err);
+}
+int gn_lifted_eval_fg(gn_ctx* c, const double* x, double* f, double* g, int mem,
+                      gn_error* err) {
+  return lifted_eval(c, gnb::EV_FG, x, nullptr, 0.0, g, f, mem, err);
 }
 
 // --------------------------------------------------------------------- KKT
@@ -904,6 +1011,25 @@ __global__ void k_guard_count(int64_t n, int64_t body, const unsigned long long*
   if (i >= body && p[i] != v) atomicAdd(out + 1, 1ull);   // guard band touched
 }
 }  // namespace
+
+int gn_host_alloc(size_t bytes, void** out) {
+  if (!out) return GN_ERR_INVALID;
+  *out = nullptr;
+  if (bytes == 0) return GN_OK;
+  if (cudaHostAlloc(out, bytes, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    *out = nullptr;
+    return GN_ERR_CUDA;
+  }
+  return GN_OK;
+}
+int gn_host_free(void* p) {
+  if (p && cudaFreeHost(p) != cudaSuccess) {
+    cudaGetLastError();
+    return GN_ERR_CUDA;
+  }
+  return GN_OK;
+}
 
 int gn_debug_kkt_guard(gn_kkt* K, int fill, uint64_t pattern, int64_t* out4) {
   if (!K || (!fill && !out4)) return GN_ERR_INVALID;

@@ -172,5 +172,9 @@ struct gn_ctx {
   int32_t n_free = 0;
   int64_t nj_l = 0, nh_l = 0;
   gnb::DBuf<int32_t> free_of_full, full_of_free, jr_l, jc_l, jpick, hr_l, hc_l, hpick;
+  // lifted evaluations (gn_lifted_eval_*): the full-space point with the fixed entries at
+  // their pinned values (filled once), the free-variable upload and the lifted output
+  gnb::DBuf<double> lx, lxin, lout;
+  bool lx_ready = false;
   gnb::DevNet net() const;
 };

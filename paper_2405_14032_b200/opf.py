@@ -297,6 +297,32 @@ class OpfNlp:
         _check(fn(self.h, _f64(full), _f64(out), mem))
         return out
 
+    def lifted_eval(self, which: str, x_free, w=None, ow: float = 1.0, out=None,
+                    mem: int = GN_MEM_HOST):
+        """LiftedProblem::eval_* (lifted.hpp:128-159) on the device: x_free [n_free] ->
+        f, grad [n_free], g [m], jac / hess lifted values; "fg" returns (f, g).  Returns
+        (ok, out) like the full-space calls (evaluation failures -> ok False)."""
+        s = self.sizes
+        L = self.lib
+        err = GnError()
+        size = {"f": 1, "grad": s.n_free, "g": s.n_cons, "jac": s.jac_nnz_lifted,
+                "hess": s.hess_nnz_lifted, "fg": s.n_cons}[which]
+        if out is None:
+            out = np.empty(size)
+        if which == "hess":
+            rc = L.gn_lifted_eval_hess(self.h, _f64(x_free), _f64(w), float(ow), _f64(out), mem,
+                                       C.byref(err))
+        elif which == "fg":
+            f = np.empty(1) if mem == GN_MEM_HOST else out[1]
+            g = out if mem == GN_MEM_HOST else out[0]
+            rc = L.gn_lifted_eval_fg(self.h, _f64(x_free), _f64(f), _f64(g), mem, C.byref(err))
+            ok = self._record(rc, err)
+            return ok, ((float(f[0]), g) if mem == GN_MEM_HOST else out)
+        else:
+            fn = getattr(L, f"gn_lifted_eval_{which}")
+            rc = fn(self.h, _f64(x_free), _f64(out), mem, C.byref(err))
+        return self._record(rc, err), out
+
 
 class CondensedKkt:
     """ipm::CondensedKkt structure + set_jacobian + assemble on the device."""

@@ -47,6 +47,12 @@ def texts():
     # at 0.3 x demand it solves (36 iterations, ~47 s on this container's host)
     t["case1354s"] = synthetic_case(*CONFIG_SIZES["case1354pegase"], seed=1,
                                     load_scale=0.3).to_matpower()
+    # self-loop lines (from bus == to bus; MATPOWER accepts them and the reference models
+    # them as ordinary lines whose two voltage ends coincide)
+    loop = synthetic_case(60, 95, 15, 45, seed=8, load_scale=0.5)
+    loop.branch[5, 1] = loop.branch[5, 0]
+    loop.branch[30, 0] = loop.branch[30, 1]
+    t["synthloop"] = loop.to_matpower()
     return t
 
 
@@ -57,6 +63,7 @@ SOLVES = {
     "case118_T24": ("case118", 24, 60.0),
     "case118_T168": ("case118", 168, 60.0),        # 40 iterations
     "case1354s_T24": ("case1354s", 24, 60.0),      # SURVEY §7 step 7 (configs[1] size)
+    "synthloop_T4": ("synthloop", 4, 60.0),        # two self-loop lines
 }
 
 
