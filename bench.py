@@ -816,10 +816,18 @@ def run_ours(args, rank, world, local_rank, dist):
             line["unit_roofline"].update(
                 dram_bytes=dram, dram_achieved=dram / (ms * 1e-3) / 1e9,
                 dram_frac=dram / (ms * 1e-3) / 1e9 / peak,
-                dram_source=f"{args.traffic_json} (ncu --set full, per launch; one launch "
-                            f"per kernel per step)")
+                dram_source=f"{_rel(args.traffic_json)} (ncu --set full, per launch; one "
+                            f"launch per kernel per step)")
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _rel(path) -> str:
+    """A path relative to the repository root when it is inside it."""
+    try:
+        return str(Path(path).resolve().relative_to(ROOT.resolve()))
+    except ValueError:
+        return str(path)
 
 
 # ------------------------------------------------------------- reference CPU
