@@ -706,10 +706,10 @@ static void launch_fused(gn_kkt* K, const FIn& in, const double* dv, double* M, 
     GN_CK(cudaEventRecord(X->ev_fork, s));
     for (int a = 0; a < nlanes; ++a) GN_CK(cudaStreamWaitEvent(X->aux[a], X->ev_fork, 0));
   }
-  // degree classes 1..6, le8, rest: round-robin over the lanes, largest first
-  static const int order[kBusClasses] = {2, 3, 1, 4, 5, 6, 7, 0};
+  // degree classes 1..kBusRegMax, le8, rest: round-robin over the lanes, largest first
+  // (d3, d4, d2, d5 .. rest, then d1)
   for (int i = 0; i < kBusClasses; ++i) {
-    const int k = order[i];
+    const int k = i < 3 ? (i == 0 ? 2 : i == 1 ? 3 : 1) : (i == kBusClasses - 1 ? 0 : i + 1);
     launch_fz_bus(t, X->bus_cls[k].p, X->n_bus_cls[k],
                   k < kBusRegMax ? k + 1 : (k == kBusRegMax ? 8 : X->maxdeg_rest), k, in, dv, M,
                   rows, bad, fork ? X->aux[i % nlanes] : s);

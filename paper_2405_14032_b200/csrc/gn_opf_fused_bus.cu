@@ -61,8 +61,12 @@ constexpr int kBW3 = GN_BW3;  // warps per CTA
 #ifndef GN_BUSR_MINB_D6
 #define GN_BUSR_MINB_D6 2
 #endif
-constexpr int kBusrMinBlocks[7] = {1, GN_BUSR_MINB_D1, GN_BUSR_MINB_D2, GN_BUSR_MINB_D3,
-                                   GN_BUSR_MINB_D4, GN_BUSR_MINB_D5, GN_BUSR_MINB_D6};
+#ifndef GN_BUSR_MINB_D7
+#define GN_BUSR_MINB_D7 1
+#endif
+constexpr int kBusrMinBlocks[10] = {1, GN_BUSR_MINB_D1, GN_BUSR_MINB_D2, GN_BUSR_MINB_D3,
+                                    GN_BUSR_MINB_D4, GN_BUSR_MINB_D5, GN_BUSR_MINB_D6,
+                                    GN_BUSR_MINB_D7, GN_BUSR_MINB_D7, GN_BUSR_MINB_D7};
 constexpr int kSV = 11;
 constexpr int kBusSmemMax = 200 * 1024;  // dynamic shared memory cap of the bus kernel  // shared doubles per (line, lane): Cs Sn cs sn vf vt w7 w8 d7 d8 d10
 
@@ -499,7 +503,8 @@ template <int DEG>
 static void launch_busr(const OpfKktTab& t, const int4* buses, int32_t n_buses, const FIn& in,
                         const double* dv, double* M, int32_t* rows, int32_t* bad, cudaStream_t s) {
   static const char* names[] = {"", "k_fz_busr<d1>", "k_fz_busr<d2>", "k_fz_busr<d3>",
-                                "k_fz_busr<d4>", "k_fz_busr<d5>", "k_fz_busr<d6>"};
+                                "k_fz_busr<d4>", "k_fz_busr<d5>", "k_fz_busr<d6>",
+                                "k_fz_busr<d7>", "k_fz_busr<d8>", "k_fz_busr<d9>"};
 #if GN_BUSR_FLAT
   const int64_t warps = ((int64_t)n_buses * t.T + 31) / 32;
 #else
@@ -525,15 +530,22 @@ void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows, int32_t* bad,
                    cudaStream_t s) {
   if (n_buses <= 0) return;
-  static_assert(kBusRegMax == 6, "register classes d1..d6");
-  switch (klass) {
-    case 0: return launch_busr<1>(t, buses, n_buses, in, dv, M, rows, bad, s);
-    case 1: return launch_busr<2>(t, buses, n_buses, in, dv, M, rows, bad, s);
-    case 2: return launch_busr<3>(t, buses, n_buses, in, dv, M, rows, bad, s);
-    case 3: return launch_busr<4>(t, buses, n_buses, in, dv, M, rows, bad, s);
-    case 4: return launch_busr<5>(t, buses, n_buses, in, dv, M, rows, bad, s);
-    case 5: return launch_busr<6>(t, buses, n_buses, in, dv, M, rows, bad, s);
-    default: break;
+  if (klass < kBusRegMax) {
+    switch (klass) {
+      case 0: return launch_busr<1>(t, buses, n_buses, in, dv, M, rows, bad, s);
+      case 1: return launch_busr<2>(t, buses, n_buses, in, dv, M, rows, bad, s);
+      case 2: return launch_busr<3>(t, buses, n_buses, in, dv, M, rows, bad, s);
+      case 3: return launch_busr<4>(t, buses, n_buses, in, dv, M, rows, bad, s);
+      case 4: return launch_busr<5>(t, buses, n_buses, in, dv, M, rows, bad, s);
+      case 5: return launch_busr<6>(t, buses, n_buses, in, dv, M, rows, bad, s);
+      case 6: if constexpr (kBusRegMax > 6) return launch_busr<7>(t, buses, n_buses, in, dv, M, rows, bad, s);
+              break;
+      case 7: if constexpr (kBusRegMax > 7) return launch_busr<8>(t, buses, n_buses, in, dv, M, rows, bad, s);
+              break;
+      case 8: if constexpr (kBusRegMax > 8) return launch_busr<9>(t, buses, n_buses, in, dv, M, rows, bad, s);
+              break;
+      default: break;
+    }
   }
   const int64_t warps = (int64_t)n_buses * t.tchunks;
   const int md = maxdeg > 0 ? maxdeg : 1;

@@ -103,14 +103,20 @@ struct FIn {
 
 // Bus-column kernel (v(n), th(n) columns): one warp per (bus, period chunk);
 // lanes = (32/P periods) x (P incident-line slots), P = next pow2 >= degree.
-// Bus-column kernel over one class of buses.  klass 0..5: buses of exactly klass+1
-// lines without parallel lines (line state in registers); klass 6: the other buses
-// of at most 8 lines, klass 7: the rest (slot-program kernel, line state in shared
-// memory sized by maxdeg).
+// Bus-column kernel over one class of buses.  klass 0..kBusRegMax-1: buses of exactly
+// klass+1 lines without parallel lines (line state in registers); klass kBusRegMax: the
+// other buses of at most 8 lines (empty when GN_BUS3_MERGE), klass kBusRegMax+1: the rest
+// (slot-program kernel, line state in shared memory sized by maxdeg).  Degree 7 joined the
+// register classes in round 2 (case1354 x 24 -6%: its only slot-program buses were two of
+// degree 7); 8 and 9 spill and measured slower than the slot program (9241 x 48 +2.4%).
 void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32_t maxdeg,
                    int klass, const FIn& in, const double* dv, double* M, int32_t* rows,
                    int32_t* bad, cudaStream_t s);
-constexpr int kBusRegMax = 6;
+#ifndef GN_BUS_REGMAX
+#define GN_BUS_REGMAX 7  // register-resident classes d1..d<GN_BUS_REGMAX> (6..9; 8 and 9 spill)
+#endif
+constexpr int kBusRegMax = GN_BUS_REGMAX;
+static_assert(kBusRegMax >= 6 && kBusRegMax <= 9, "register classes d1..d6 .. d1..d9");
 // per bus: (n, bl begin, deg [| program length << 8], boff | program begin),
 // (lifted v rank, lifted th rank, 0, 0), (M start of v(n, t=0), v column length,
 // M start of th(n, t=0), th column length)
