@@ -53,6 +53,9 @@ def texts():
     loop.branch[5, 1] = loop.branch[5, 0]
     loop.branch[30, 0] = loop.branch[30, 1]
     t["synthloop"] = loop.to_matpower()
+    # overloaded (1.3 x demand): the reference IPM enters feasibility restoration and ends
+    # "infeasible" -- the restoration problem runs over the same seams
+    t["synthinf"] = synthetic_case(40, 70, 12, 30, seed=1, load_scale=1.3).to_matpower()
     return t
 
 
@@ -64,6 +67,7 @@ SOLVES = {
     "case118_T168": ("case118", 168, 60.0),        # 40 iterations
     "case1354s_T24": ("case1354s", 24, 60.0),      # SURVEY §7 step 7 (configs[1] size)
     "synthloop_T4": ("synthloop", 4, 60.0),        # two self-loop lines
+    "synthinf_T3": ("synthinf", 3, 60.0),          # restoration, ends infeasible
 }
 
 
