@@ -130,3 +130,57 @@ def test_lifted_eval_rejects_period_shard(gpu):
     with pytest.raises(GridError) as e:
         nlp.lifted_eval("g", np.zeros(nlp.sizes.n_free))
     assert e.value.code == GN_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_lifted_eval_randomised_fixed_variables(gpu, seed):
+    """Random networks with fixed generators (pmin == pmax > 0) and fixed voltages, so the
+    pinned values enter g, J and H: the lifted calls on the free-variable vector equal the
+    bit-exact C restatement's full-space evaluation at the pinned point, gathered by its
+    own lifted picks (grad bit-exact, the rest within the 1e-12 bar)."""
+    from oracle import bindings as B
+    from helpers import interior_point, row_weights
+    from paper_2405_14032_b200.network import synthetic_case
+    from paper_2405_14032_b200.opf import load_profile
+    rng = np.random.default_rng(500 + seed)
+    N = int(rng.integers(20, 150))
+    raw = synthetic_case(N, N + int(rng.integers(N // 3, N)), int(rng.integers(4, 20)),
+                         int(rng.integers(N // 3, N)), seed=int(rng.integers(1, 10_000)),
+                         parallel_lines=int(rng.integers(0, 3)))
+    net = raw.network()
+    for g in rng.choice(net.n_gen, size=min(3, net.n_gen), replace=False):
+        net.gen_pmin[g] = net.gen_pmax[g] = max(net.gen_pmax[g], 0.3)
+    for b in rng.choice(net.n_bus, size=3, replace=False):
+        if b != net.reference_bus:
+            net.bus_vmin[b] = net.bus_vmax[b] = 1.02
+    T = int(rng.integers(1, 40))
+    scale = load_profile(net.n_load, T)
+    nlp = OpfNlp(net, T, scale).lift(1e-4)
+    orc = B.OracleModel(net, T, scale)
+    lo = orc.lift(1e-4)
+    ours = nlp.lifted_structure()
+    assert_bitexact(ours["free_to_full"], lo["free_to_full"], "free_to_full")
+    xl, xu, xs, _, _ = nlp.bounds()
+    x = interior_point(xl, xu, xs, seed)
+    fixed = xl == xu
+    assert fixed.sum() > 3 * T  # generators and voltages pinned, not only th_ref
+    x[fixed] = xl[fixed]  # the pinned point
+    xf = x[lo["free_to_full"]]
+    w = row_weights(nlp.sizes.n_cons, seed + 3)
+    ow = float(rng.uniform(0.2, 2.0))
+    ok, g = nlp.lifted_eval("g", xf)
+    okg, go, _ = orc.eval_g(x)
+    assert ok and okg
+    assert_close(g, go, what="lifted g")
+    ok, gr = nlp.lifted_eval("grad", xf)
+    okg, gro, _ = orc.eval_grad(x)
+    assert ok and okg
+    assert_bitexact(gr, gro[lo["free_to_full"]], "lifted grad")
+    ok, jl = nlp.lifted_eval("jac", xf)
+    okj, jo, _ = orc.eval_jac(x)
+    assert ok and okj
+    assert_close(jl, jo[lo["jac_pick"]], what="lifted jac")
+    ok, hl = nlp.lifted_eval("hess", xf, w=w, ow=ow)
+    okh, ho, _ = orc.eval_hess(x, w, ow)
+    assert ok and okh
+    assert_close(hl, ho[lo["hess_pick"]], what="lifted hess")
