@@ -301,6 +301,12 @@ int gn_kkt_update_x(gn_kkt* kkt, const double* x, const double* row_weights, dou
  * destinations may be any UVA-addressable memory: device buffers or pinned host
  * buffers (an asynchronous read-back overlapping later work on the stream). */
 int gn_kkt_values(gn_kkt* kkt, double* a_vals, double* m_vals, int mem);
+/* The device addresses of the KKT's own A and M value arrays (CSR / CSC-lower order, valid
+ * until gn_kkt_destroy), for device-resident consumers that read them in place -- a device
+ * factorization, or a copy engine on another stream that returns A to the host while M is
+ * still being assembled.  Their contents change with the next set_jacobian / assemble call
+ * on the KKT's stream: order such reads after it with an event. */
+int gn_kkt_values_ptr(gn_kkt* kkt, const double** a_vals, const double** m_vals);
 /* Selects the assembly algorithm: 0 = auto, 1 = generic contributor lists,
  * 2 = OPF-specialised (lifted KKTs only). */
 /* Cap the fused/specialised KKT kernels at `ctas_per_sm` resident CTAs per SM (grid-stride;

@@ -997,6 +997,13 @@ int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
   API_CATCH(nullptr)
 }
 
+int gn_kkt_values_ptr(gn_kkt* K, const double** av, const double** mv) {
+  if (!K) return GN_ERR_INVALID;
+  if (av) *av = K->avals.p;
+  if (mv) *mv = K->mvals.p;
+  return GN_OK;
+}
+
 // ------------------------------------------------------------ test support
 namespace {
 __global__ void k_guard_fill(int64_t n, unsigned long long* p, unsigned long long v) {

@@ -425,6 +425,12 @@ class CondensedKkt:
         _check(self.lib.gn_kkt_values(self.h, _f64(a), _f64(m), GN_MEM_HOST))
         return a, m
 
+    def values_ptr(self):
+        """Device addresses (ints) of the KKT's own A and M value arrays (gn_kkt_values_ptr)."""
+        a, m = C.c_void_p(), C.c_void_p()
+        _check(self.lib.gn_kkt_values_ptr(self.h, C.byref(a), C.byref(m)))
+        return a.value or 0, m.value or 0
+
     def values_device(self, a_out, m_out, sync: bool = True):
         _check(self.lib.gn_kkt_values(self.h, _f64(a_out), _f64(m_out),
                                       GN_MEM_DEVICE if sync else GN_MEM_DEVICE_ASYNC))
