@@ -759,3 +759,26 @@ def test_lifted_gather_matches_reference(gpu, fx, mem):
             nlp.lifted_gather(which, torch.from_numpy(full).to(dev), out=out, mem=GN_MEM_DEVICE)
             got = out.cpu().numpy()
         assert_bitexact(got, lifted, f"lifted {which} gather")
+
+
+def test_values_ptr_views_the_kkt_arrays(gpu):
+    """gn_kkt_values_ptr: zero-copy views of the KKT's own A and M equal gn_kkt_values."""
+    import torch
+
+    class _View:
+        def __init__(self, ptr, n):
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8",
+                                             "data": (ptr, False), "version": 3}
+
+    nlp, z, meta, net = _nlp("case118_T4")
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    dw, dc = DELTAS[1]
+    K.update_x(z["x"], z["w"], float(z["ow"]), z["sx"], z["ss"], dw, dc)
+    a, m = K.values()
+    pa, pm = K.values_ptr()
+    assert pa and pm
+    dev = torch.device("cuda", 0)
+    torch.cuda.synchronize()
+    assert_bitexact(torch.as_tensor(_View(pa, K.a_nnz), device=dev).cpu().numpy(), a, "A view")
+    assert_bitexact(torch.as_tensor(_View(pm, K.m_nnz), device=dev).cpu().numpy(), m, "M view")
