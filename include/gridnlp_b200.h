@@ -214,6 +214,12 @@ int gn_eval_hess(gn_ctx* ctx, const double* x, const double* row_weights,
  * eval_f and eval_g in one call, no derivative work, one status (the
  * lexicographically first failing (pattern, record) over both). */
 int gn_eval_fg(gn_ctx* ctx, const double* x, double* f, double* g, int mem, gn_error* err);
+/* One IPM iteration's callbacks (solver.hpp:157-158 and 202: eval_f, eval_grad, eval_g,
+ * eval_jac and eval_hess(w, ow) at the same x) in ONE kernel launch: outputs bit-identical
+ * to the five calls above, the lexicographically first failure over all five reported. */
+int gn_eval_all(gn_ctx* ctx, const double* x, const double* row_weights, double obj_weight,
+                double* f, double* grad, double* g, double* jac, double* hess, int mem,
+                gn_error* err);
 
 /* ---------------------------------------------------------------- lifted */
 /* LiftedProblem constructor filter (lifted.hpp:25-100): free map, slack

@@ -111,6 +111,8 @@ _SIGS = {
     "gn_eval_hess": (C.c_int, [vp, f64p, f64p, C.c_double, f64p, C.c_int,
                                C.POINTER(GnError)]),
     "gn_eval_fg": (C.c_int, [vp, f64p, f64p, f64p, C.c_int, C.POINTER(GnError)]),
+    "gn_eval_all": (C.c_int, [vp, f64p, f64p, C.c_double, f64p, f64p, f64p, f64p, f64p, C.c_int,
+                              C.POINTER(GnError)]),
     "gn_ipm_create": (C.c_int, [vp, vp, vp, vp, vp, C.c_int, C.POINTER(vp), C.POINTER(GnError)]),
     "gn_ipm_destroy": (C.c_int, [vp]),
     "gn_ipm_jac_transpose_multiply": (C.c_int, [vp, vp, vp, vp, C.c_int]),

@@ -528,6 +528,47 @@ int gn_eval_hess(gn_ctx* c, const double* x, const double* w, double ow, double*
   return eval(c, gnb::EV_H, x, w, ow, out, mem, err);
 }
 
+// One IPM iteration's callbacks (solver.hpp:157-158, 202: eval_f, eval_grad, eval_g,
+// eval_jac, then eval_hess at the same x) in one kernel launch; outputs bit-identical to
+// the five gn_eval_* calls, one status word for all five.
+int gn_eval_all(gn_ctx* c, const double* x, const double* w, double ow, double* f,
+                double* grad, double* g, double* jac, double* hess, int mem, gn_error* err) {
+  if (!c) return fail(err, GN_ERR_INVALID, "null context");
+  if (!x || !w || !f || !grad || !g || !jac || !hess) return fail(err, GN_ERR_INVALID, "null array");
+  API_TRY
+  set_device(c->device);
+  const auto& d = c->d;
+  cudaStream_t s = c->stream;
+  const double *dx = x, *dw = w;
+  double *df = f, *dgr = grad, *dg = g, *dj = jac, *dh = hess;
+  if (!is_device(mem)) {
+    c->sx.upload(x, d.n, s);
+    c->sw.upload(w, d.m, s);
+    dx = c->sx.p;
+    dw = c->sw.p;
+    const size_t need = static_cast<size_t>(1 + d.n + d.m + d.nj + d.nh);
+    if (c->sout.n < need) c->sout.alloc(need);
+    df = c->sout.p;
+    dgr = df + 1;
+    dg = dgr + d.n;
+    dj = dg + d.m;
+    dh = dj + d.nj;
+  }
+  if (!is_async(mem))
+    GN_CK(cudaMemsetAsync(c->status.p, 0xff, sizeof(unsigned long long), s));
+  gnb::launch_eval_all(d, c->net(), dx, dw, ow, df, dgr, dg, dj, dh, c->fpart.p, c->status.p, s);
+  if (is_async(mem)) return ok(err);
+  if (!is_device(mem)) {
+    gnb::d2h(f, df, sizeof(double), s);
+    gnb::d2h(grad, dgr, sizeof(double) * d.n, s);
+    gnb::d2h(g, dg, sizeof(double) * d.m, s);
+    gnb::d2h(jac, dj, sizeof(double) * d.nj, s);
+    gnb::d2h(hess, dh, sizeof(double) * d.nh, s);
+  }
+  return take_status(c, err);
+  API_CATCH(err)
+}
+
 // Line-search trial point (solver.hpp:267-304): the objective and
 // the constraint values only -- no derivative kernels -- under one status word.
 int gn_eval_fg(gn_ctx* c, const double* x, double* f, double* g, int mem, gn_error* err) {

@@ -242,8 +242,6 @@ __device__ __forceinline__ void gen_body(const OpfDims& d, const DevNet& net,
                                          double* __restrict__ out, double* __restrict__ fpart,
                                          unsigned int* cnt, unsigned long long* st, int64_t blk,
                                          int64_t nblk_gen) {
-  __shared__ double red[kBS];
-  __shared__ bool last;
   const int64_t nrec = (int64_t)d.G * d.T;
   const int64_t r0 = blk * kBS;
   const int64_t r = r0 + threadIdx.x;
@@ -258,6 +256,8 @@ __device__ __forceinline__ void gen_body(const OpfDims& d, const DevNet& net,
     c0 = __ldg(net.c0 + g);
   }
   if constexpr (MODE == EV_F) {
+    __shared__ double red[kBS];
+    __shared__ bool last;
     // ((c2*pg^2) + (c1*pg)) + c0, opf.hpp:245; partial sums in a fixed tree
     double v = 0.0;
     if (valid) {
@@ -455,6 +455,57 @@ __global__ void __launch_bounds__(kBS) k_eval(OpfDims d, DevNet net, const doubl
   else if constexpr (MODE != EV_G) gen_body<MODE>(d, net, x, ow, out, fpart, cnt, st, b, sg.gen);
 }
 
+// All five callbacks of an IPM iteration in ONE launch (gn_eval_all): the block ranges of
+// k_eval<H>, <J>, <G>, <GRAD>, <F> concatenated (heavy line streams first, the short
+// generator / ramp / zero-fill blocks in the tail), one shared staging buffer for the J and
+// H record blocks.  Same bodies, so every output is bit-identical to the five launches.
+struct AllSegs {
+  int64_t hl, jl, gl, gb, hr, jr, gr, hg, jg, dg, fg, dz;
+};
+struct AllOut {
+  double *f, *grad, *g, *jac, *hess;
+};
+constexpr int kZeroPerBlock = kBS * 8;  // grad zero-fill: doubles per block
+// the single launch up to this many blocks (1354 x 24: ~1.7k blocks, step -12%; 9241 x 48:
+// ~17k, five launches better)
+#ifndef GN_EVAL_ALL_MAXBLK
+#define GN_EVAL_ALL_MAXBLK 6000
+#endif
+__global__ void __launch_bounds__(kBS) k_eval_all(OpfDims d, DevNet net,
+                                                  const double* __restrict__ x,
+                                                  const double* __restrict__ w, double ow,
+                                                  AllOut o, double* __restrict__ fpart,
+                                                  unsigned int* cnt, unsigned long long* st,
+                                                  AllSegs sg) {
+  __shared__ __align__(16) double sm[kBS * 15 + 2];
+  int64_t b = blockIdx.x;
+  if (b < sg.hl) return line_body<EV_H>(d, net, x, w, o.hess, st, b, sm);
+  b -= sg.hl;
+  if (b < sg.jl) return line_body<EV_J>(d, net, x, w, o.jac, st, b, sm);
+  b -= sg.jl;
+  if (b < sg.gl) return line_body<EV_G>(d, net, x, w, o.g, st, b, nullptr);
+  b -= sg.gl;
+  if (b < sg.gb) return bus_body(d, net, x, o.g, st, b);
+  b -= sg.gb;
+  if (b < sg.hr) return ramp_body<EV_H>(d, net, x, o.hess, st, b);
+  b -= sg.hr;
+  if (b < sg.jr) return ramp_body<EV_J>(d, net, x, o.jac, st, b);
+  b -= sg.jr;
+  if (b < sg.gr) return ramp_body<EV_G>(d, net, x, o.g, st, b);
+  b -= sg.gr;
+  if (b < sg.hg) return gen_body<EV_H>(d, net, x, ow, o.hess, fpart, cnt, st, b, sg.hg);
+  b -= sg.hg;
+  if (b < sg.jg) return gen_body<EV_J>(d, net, x, ow, o.jac, fpart, cnt, st, b, sg.jg);
+  b -= sg.jg;
+  if (b < sg.dg) return gen_body<EV_GRAD>(d, net, x, ow, o.grad, fpart, cnt, st, b, sg.dg);
+  b -= sg.dg;
+  if (b < sg.fg) return gen_body<EV_F>(d, net, x, ow, o.f, fpart, cnt, st, b, sg.fg);
+  b -= sg.fg;
+  // the gradient's non-generator blocks are zero (pattern_model.hpp:336 zero-fills)
+  const int64_t z0 = d.qg0 + b * kZeroPerBlock, z1 = min((int64_t)d.n, z0 + kZeroPerBlock);
+  for (int64_t i = z0 + threadIdx.x; i < z1; i += kBS) o.grad[i] = 0.0;
+}
+
 // ------------------------------------------------------------------ driver
 static unsigned nblk(int64_t n) { return (unsigned)((n + kBS - 1) / kBS); }
 
@@ -505,6 +556,40 @@ void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
       case EV_H: k_eval<EV_H><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
       default: k_eval<EV_FG><<<grid, kBS, 0, s>>>(d, net, x, w, ow, out, fout, fpart, cnt, st, sg); break;
     }
+    count_launch();
+  }
+  GN_CK(cudaGetLastError());
+}
+
+void launch_eval_all(const OpfDims& d, const DevNet& net, const double* x, const double* w,
+                     double ow, double* f, double* grad, double* g, double* jac, double* hess,
+                     double* fpart, unsigned long long* st, cudaStream_t s) {
+  const int64_t nl = (int64_t)d.L * d.T, ng = (int64_t)d.G * d.T,
+                nr = d.pid[K_RAMP] >= 0 ? (int64_t)d.GR * d.R : 0,
+                nb = (int64_t)d.N * d.T;
+  AllSegs sg{};
+  sg.hl = sg.jl = sg.gl = nblk(nl);
+  sg.gb = nblk(nb);
+  sg.hr = sg.jr = sg.gr = nblk(nr);
+  sg.hg = sg.jg = sg.dg = sg.fg = nblk(ng);
+  sg.dz = d.n > d.qg0 ? (d.n - d.qg0 + kZeroPerBlock - 1) / kZeroPerBlock : 0;
+  const int64_t blocks = sg.hl + sg.jl + sg.gl + sg.gb + sg.hr + sg.jr + sg.gr + sg.hg + sg.jg +
+                         sg.dg + sg.fg + sg.dz;
+  if (blocks > GN_EVAL_ALL_MAXBLK) {
+    // large problems: the five launches (each callback's own occupancy; the single launch
+    // gives every block the J / H staging buffer: 30k x 96 +3.6%, 9241 x 48 +0.4%)
+    launch_eval(EV_F, d, net, x, w, ow, f, fpart, st, s);
+    launch_eval(EV_GRAD, d, net, x, w, ow, grad, fpart, st, s);
+    launch_eval(EV_G, d, net, x, w, ow, g, fpart, st, s);
+    launch_eval(EV_J, d, net, x, w, ow, jac, fpart, st, s);
+    launch_eval(EV_H, d, net, x, w, ow, hess, fpart, st, s);
+    return;
+  }
+  if (!sg.fg) GN_CK(cudaMemsetAsync(f, 0, sizeof(double), s));  // no generators
+  if (blocks) {
+    KTimer kt("k_eval<ALL>", s);
+    k_eval_all<<<(unsigned)blocks, kBS, 0, s>>>(d, net, x, w, ow, AllOut{f, grad, g, jac, hess},
+                                                fpart, fcount(d, fpart), st, sg);
     count_launch();
   }
   GN_CK(cudaGetLastError());

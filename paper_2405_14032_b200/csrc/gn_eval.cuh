@@ -12,6 +12,10 @@ void launch_eval(int mode, const OpfDims& d, const DevNet& net, const double* x,
                  const double* w, double ow, double* out, double* fpart,
                  unsigned long long* st, cudaStream_t s, double* fout = nullptr);
 size_t fpart_size(const OpfDims& d);
+// f, grad, g, J and H(w, ow) in one launch (gn_eval_all), bit-identical to five launch_eval
+void launch_eval_all(const OpfDims& d, const DevNet& net, const double* x, const double* w,
+                     double ow, double* f, double* grad, double* g, double* jac, double* hess,
+                     double* fpart, unsigned long long* st, cudaStream_t s);
 
 void build_structure(gn_ctx* c, int32_t* jr, int32_t* jc, int32_t* hr, int32_t* hc);
 void build_lifted(gn_ctx* c);

@@ -212,6 +212,19 @@ class OpfNlp:
                                                 C.byref(err)), err)
         return ok, out
 
+    def eval_all(self, x, row_weights, obj_weight: float, outs=None, mem: int = GN_MEM_HOST):
+        """f, grad, g, J, H in one call / one launch (gn_eval_all).  outs = (f[1], grad, g,
+        jac, hess) host arrays or device tensors; returns (ok, outs)."""
+        s = self.sizes
+        if outs is None:
+            outs = (np.zeros(1), np.empty(s.n_vars), np.empty(s.n_cons), np.empty(s.jac_nnz),
+                    np.empty(s.hess_nnz))
+        err = GnError()
+        ok = self._record(self.lib.gn_eval_all(self.h, _f64(x), _f64(row_weights),
+                                               float(obj_weight), *map(_f64, outs), mem,
+                                               C.byref(err)), err)
+        return ok, outs
+
     # ---- device-resident variants (pointers to device memory)
     def eval_device(self, which: str, x, out, w=None, ow: float = 1.0, sync: bool = True):
         mem = GN_MEM_DEVICE if sync else GN_MEM_DEVICE_ASYNC

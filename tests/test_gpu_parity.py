@@ -782,3 +782,31 @@ def test_values_ptr_views_the_kkt_arrays(gpu):
     torch.cuda.synchronize()
     assert_bitexact(torch.as_tensor(_View(pa, K.a_nnz), device=dev).cpu().numpy(), a, "A view")
     assert_bitexact(torch.as_tensor(_View(pm, K.m_nnz), device=dev).cpu().numpy(), m, "M view")
+
+
+@pytest.mark.parametrize("fx", ["case9_T2", "case118_T4", "synth_T3"])
+def test_eval_all_equals_the_five_callbacks(gpu, fx):
+    """gn_eval_all (one launch) writes exactly what eval_f / grad / g / jac / hess write, and
+    reports the same first failure."""
+    nlp, z, meta, net = _nlp(fx)
+    x, w, ow = z["x"], z["w"], float(z["ow"])
+    ok, (f, grad, g, jac, hess) = nlp.eval_all(x, w, ow)
+    assert ok
+    assert f[0] == nlp.eval_f(x)[1]
+    assert_bitexact(grad, nlp.eval_grad(x)[1], "grad")
+    assert_bitexact(g, nlp.eval_g(x)[1], "g")
+    assert_bitexact(jac, nlp.eval_jac(x)[1], "jac")
+    assert_bitexact(hess, nlp.eval_hess(x, w, ow)[1], "hess")
+    assert_close(hess, z["hess"], what="hess vs reference")
+    xb = x.copy()
+    xb[len(x) // 2] = np.nan
+    firsts = []
+    for name, args in [("eval_f", (xb,)), ("eval_grad", (xb,)), ("eval_g", (xb,)),
+                       ("eval_jac", (xb,)), ("eval_hess", (xb, w, ow))]:
+        okc, _ = getattr(nlp, name)(*args)
+        if not okc:
+            firsts.append(nlp.last_error)
+    ok, _ = nlp.eval_all(xb, w, ow)
+    assert ok == (not firsts)
+    if firsts:
+        assert nlp.last_error == min(firsts)
