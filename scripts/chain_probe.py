@@ -41,12 +41,8 @@ A = GN_MEM_DEVICE_ASYNC
 ev0, ev1 = torch.cuda.Event(), torch.cuda.Event()
 
 
-def callbacks():
-    nlp.eval_device("f", dx, f, sync=False)
-    nlp.eval_device("grad", dx, grad, sync=False)
-    nlp.eval_device("g", dx, g, sync=False)
-    nlp.eval_device("jac", dx, J, sync=False)
-    nlp.eval_device("hess", dx, H, w=dw, ow=1.0, sync=False)
+def callbacks():  # as the one-GPU bench step: gn_eval_all
+    nlp.eval_all(dx, dw, 1.0, outs=(f, grad, g, J, H), mem=A)
 
 
 def kkt_only():
