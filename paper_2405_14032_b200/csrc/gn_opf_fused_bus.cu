@@ -305,6 +305,205 @@ __global__ void __launch_bounds__(kBW3 * 32, 3) k_fz_bus3(OpfKktTab t, const int
   }
 }
 
+// Cooperative value pass of the slot-program class (GN_BUS3_COOP): one CTA of kB3C warps per
+// (bus, 32 periods) instead of one warp.  The bus's line states are computed by the warps in
+// parallel (line i by warp i mod kB3C) into the CTA's shared memory; after one barrier warp 0
+// runs the fused own-slot sweep and writes the three own slots while the other warps take
+// the neighbour slots round-robin.  Every slot keeps its summation order (each value is still
+// one thread's ordered sum), so M is bit-identical to k_fz_bus3.  These buses are few (degree
+// 8 and up, or parallel lines: ~0.3-1.5% of them) and sit at the end of the bus lane, where
+// their one-warp latency chains were ~20 us.
+#ifndef GN_BUS3_COOP
+#define GN_BUS3_COOP 1
+#endif
+constexpr int kB3C = 4;
+__global__ void __launch_bounds__(kB3C * 32) k_fz_bus3c(OpfKktTab t, const int4* __restrict__ buses,
+                                                        int32_t n_buses, int32_t maxdeg, FIn in,
+                                                        const double* __restrict__ dv,
+                                                        double* __restrict__ M) {
+  extern __shared__ double bsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n64 = blockIdx.x / t.tchunks;
+  if (n64 >= n_buses) return;  // block-uniform
+  const int4 bd0 = __ldg(buses + kBusDesc * n64), bd1 = __ldg(buses + kBusDesc * n64 + 1);
+  const int4 bd2 = __ldg(buses + kBusDesc * n64 + 2);
+  const int32_t n = bd0.x, b0 = bd0.y, deg = bd0.z & 255, T = t.T;
+  const int32_t tt = (int32_t)(blockIdx.x - n64 * t.tchunks) * 32 + lane;
+  const bool live = tt < T;
+  const int32_t ts = live ? tt : T - 1;  // idle lanes load a valid period, write nothing
+  double* S = bsm + lane;  // [line][field][lane]
+  struct LU {
+    double G, B;
+    int32_t l, fr;
+  };
+  LU* U = reinterpret_cast<LU*>(bsm + (size_t)maxdeg * kSV * 32);
+  if (threadIdx.x < deg) {
+    const int2 e = __ldg(t.blx + b0 + threadIdx.x);
+    const double2 gb = __ldg(t.blgb + b0 + threadIdx.x);
+    U[threadIdx.x] = LU{gb.x, gb.y, e.x >> 1, e.x & 1};
+  }
+  for (int i = warp; i < deg; i += kB3C) {  // phase 1: line states, in parallel over warps
+    const int2 e = __ldg(t.blx + b0 + i);
+    const double2 gb = __ldg(t.blgb + b0 + i);
+    const int32_t l = e.x >> 1, f = (e.x & 1) ? n : e.y, to = (e.x & 1) ? e.y : n;
+    const int32_t rl = l * T + ts;
+    const LineState st = line_state(gb.x, gb.y, in.x[t.v0 + f * T + ts], in.x[t.v0 + to * T + ts],
+                                    in.x[t.th0 + f * T + ts], in.x[t.th0 + to * T + ts]);
+    double* q = S + (size_t)i * kSV * 32;
+    q[0 * 32] = st.Cs;
+    q[1 * 32] = st.Sn;
+    q[2 * 32] = st.cs;
+    q[3 * 32] = st.sn;
+    q[4 * 32] = st.vf;
+    q[5 * 32] = st.vt;
+    q[6 * 32] = in.w[t.flow_p0 + rl];
+    q[7 * 32] = in.w[t.flow_q0 + rl];
+    q[8 * 32] = dval(t, dv, t.flow_p0 + rl);
+    q[9 * 32] = dval(t, dv, t.flow_q0 + rl);
+    q[10 * 32] = dval(t, dv, t.ang0 + rl);
+  }
+  __syncthreads();
+  struct LV {
+    LineState s;
+    double G, B;
+    double w7, w8, d7, d8, d10;
+    int32_t l, fr;
+  };
+  auto lv = [&](int k) {
+    LV r;
+    const LU u = U[k];
+    r.l = u.l;
+    r.fr = u.fr;
+    r.G = u.G;
+    r.B = u.B;
+    const double* q = S + (size_t)k * kSV * 32;
+    r.s.Cs = q[0 * 32];
+    r.s.Sn = q[1 * 32];
+    r.s.cs = q[2 * 32];
+    r.s.sn = q[3 * 32];
+    r.s.vf = q[4 * 32];
+    r.s.vt = q[5 * 32];
+    r.s.vfvt = r.s.vf * r.s.vt;
+    r.w7 = q[6 * 32];
+    r.w8 = q[7 * 32];
+    r.d7 = q[8 * 32];
+    r.d8 = q[9 * 32];
+    r.d10 = q[10 * 32];
+    return r;
+  };
+  auto JP = [&](const LV& r, bool other, bool theta) {
+    const int f = theta ? ((r.fr ^ other) ? 3 : 4) : ((r.fr ^ other) ? 1 : 2);
+    return j_flow_p(r.s, r.G, r.B, f);
+  };
+  auto JQ = [&](const LV& r, bool other, bool theta) {
+    const int f = theta ? ((r.fr ^ other) ? 3 : 4) : ((r.fr ^ other) ? 1 : 2);
+    return j_flow_q(r.s, r.G, r.B, f);
+  };
+  const int32_t cv = bd1.x < 0 ? -1 : bd1.x * T + ts, ct = bd1.y < 0 ? -1 : bd1.y * T + ts;
+  const int64_t posv = cv >= 0 ? (int64_t)bd2.x + (int64_t)ts * bd2.y : 0;
+  const int64_t post = ct >= 0 ? (int64_t)bd2.z + (int64_t)ts * bd2.w : 0;
+  const int32_t p0 = bd0.w, p1 = p0 + (bd0.z >> 8);
+  double own0 = 0.0, own2 = 0.0, own4 = 0.0;
+  if (warp == 0) {  // the own slots: one fused pass-major sweep over every incident line
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      own0 += h_flow_p(r.s, r.G, r.w7, r.fr ? 5 : 9);
+      own2 += h_flow_p(r.s, r.G, r.w7, r.fr ? 7 : 11);
+      own4 += h_flow_p(r.s, r.G, r.w7, r.fr ? 12 : 14);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      own0 += h_flow_q(r.s, r.B, r.w8, r.fr ? 5 : 9);
+      own2 += h_flow_q(r.s, r.B, r.w8, r.fr ? 7 : 11);
+      own4 += h_flow_q(r.s, r.B, r.w8, r.fr ? 12 : 14);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      const double jv_ = JP(r, false, false), jt_ = JP(r, false, true);
+      own0 += pair_term(r.d7, jv_, jv_);
+      own2 += pair_term(r.d7, jt_, jv_);
+      own4 += pair_term(r.d7, jt_, jt_);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      const double jv_ = JQ(r, false, false), jt_ = JQ(r, false, true);
+      own0 += pair_term(r.d8, jv_, jv_);
+      own2 += pair_term(r.d8, jt_, jv_);
+      own4 += pair_term(r.d8, jt_, jt_);
+    }
+    for (int k = 0; k < deg; ++k) {
+      const LV r = lv(k);
+      own4 += pair_term(r.d10, r.fr ? 1.0 : -1.0, r.fr ? 1.0 : -1.0);
+    }
+    own0 += in.dw + (cv >= 0 ? in.sx[cv] : 0.0);
+    own4 += in.dw + (ct >= 0 ? in.sx[ct] : 0.0);
+  }
+#define PASS(expr)                                 \
+  for (uint32_t mm = mask; mm; mm &= mm - 1) {     \
+    const LV r = lv(__ffs(mm) - 1);                \
+    acc += (expr);                                 \
+  }
+  int jv = 0, jt = 0, nb = 0;
+  for (int32_t q = p0; q < p1; ++q) {  // every warp walks the program (slot positions)
+    const unsigned long long code = __ldg(t.bprog + q);
+    const uint32_t mask = (uint32_t)code;
+    const int type = (int)((code >> 32) & 7);
+    const bool in_v = type < 4;
+    const int64_t at = in_v ? posv + jv : post + jt;
+    if (in_v) ++jv; else ++jt;
+    const bool own = type == 0 || type == 2 || type == 4;
+    const int owner = own ? 0 : 1 + (nb++ % (kB3C - 1));
+    if (owner != warp) continue;
+    double acc = 0.0;
+    if (own) {
+      acc = type == 0 ? own0 : (type == 2 ? own2 : own4);
+    } else if ((mask & (mask - 1)) == 0) {  // one line to the neighbour: its terms in pass order
+      const LV r = lv(__ffs(mask) - 1);
+      if (type == 1) {
+        acc += h_flow_p(r.s, r.G, r.w7, 6);
+        acc += h_flow_q(r.s, r.B, r.w8, 6);
+        acc += pair_term(r.d7, JP(r, true, false), JP(r, false, false));
+        acc += pair_term(r.d8, JQ(r, true, false), JQ(r, false, false));
+      } else if (type == 3) {
+        acc += h_flow_p(r.s, r.G, r.w7, r.fr ? 8 : 10);
+        acc += h_flow_q(r.s, r.B, r.w8, r.fr ? 8 : 10);
+        acc += pair_term(r.d7, JP(r, true, true), JP(r, false, false));
+        acc += pair_term(r.d8, JQ(r, true, true), JQ(r, false, false));
+      } else {
+        acc += h_flow_p(r.s, r.G, r.w7, 13);
+        acc += h_flow_q(r.s, r.B, r.w8, 13);
+        acc += pair_term(r.d7, JP(r, true, true), JP(r, false, true));
+        acc += pair_term(r.d8, JQ(r, true, true), JQ(r, false, true));
+        acc += pair_term(r.d10, r.fr ? -1.0 : 1.0, r.fr ? 1.0 : -1.0);
+      }
+    } else {  // parallel lines: pass-major over the group
+      switch (type) {
+        case 1:
+          PASS(h_flow_p(r.s, r.G, r.w7, 6));
+          PASS(h_flow_q(r.s, r.B, r.w8, 6));
+          PASS(pair_term(r.d7, JP(r, true, false), JP(r, false, false)));
+          PASS(pair_term(r.d8, JQ(r, true, false), JQ(r, false, false)));
+          break;
+        case 3:
+          PASS(h_flow_p(r.s, r.G, r.w7, r.fr ? 8 : 10));
+          PASS(h_flow_q(r.s, r.B, r.w8, r.fr ? 8 : 10));
+          PASS(pair_term(r.d7, JP(r, true, true), JP(r, false, false)));
+          PASS(pair_term(r.d8, JQ(r, true, true), JQ(r, false, false)));
+          break;
+        default:
+          PASS(h_flow_p(r.s, r.G, r.w7, 13));
+          PASS(h_flow_q(r.s, r.B, r.w8, 13));
+          PASS(pair_term(r.d7, JP(r, true, true), JP(r, false, true)));
+          PASS(pair_term(r.d8, JQ(r, true, true), JQ(r, false, true)));
+          PASS(pair_term(r.d10, r.fr ? -1.0 : 1.0, r.fr ? 1.0 : -1.0));
+          break;
+      }
+    }
+    if (live && (in_v ? cv >= 0 : ct >= 0)) M[at] = acc;
+  }
+#undef PASS
+}
+
 // Register-resident variant for buses of exactly DEG lines and no parallel lines
 // (almost every bus of a transmission network): each lane holds its period's
 // state and row inputs of all DEG lines in registers; the own slots are one
@@ -570,6 +769,28 @@ void launch_fz_bus(const OpfKktTab& t, const int4* buses, int32_t n_buses, int32
     }
   }
   KTimer kt(klass == kBusRegMax ? "k_fz_bus3<le8>" : "k_fz_bus3<rest>", s);
+#if GN_BUS3_COOP
+  if (!rows) {
+    const size_t csmem = (size_t)md * (kSV * 32 * sizeof(double) + 24);
+    static std::mutex cmu;
+    static std::vector<char> cdone;
+    int dev = 0;
+    GN_CK(cudaGetDevice(&dev));
+    {
+      std::lock_guard<std::mutex> lock(cmu);
+      if (static_cast<size_t>(dev) >= cdone.size()) cdone.resize(static_cast<size_t>(dev) + 1, 0);
+      if (!cdone[dev]) {
+        GN_CK(cudaFuncSetAttribute(k_fz_bus3c, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   kBusSmemMax));
+        cdone[dev] = 1;
+      }
+    }
+    k_fz_bus3c<<<(unsigned)((int64_t)n_buses * t.tchunks), kB3C * 32, csmem, s>>>(
+        t, buses, n_buses, md, in, dv, M);
+    count_launch();
+    return;
+  }
+#endif
   if (rows)
     k_fz_bus3<true><<<blocks, nw * 32, smem, s>>>(t, buses, n_buses, md, in, dv, M, rows, bad);
   else
