@@ -10,6 +10,8 @@
  *   include/gridnlp_b200/cuda_opf_nlp.hpp   -> ipm::NlpProblem   (ipm/nlp.hpp:15-39)
  *   include/gridnlp_b200/shim/gridnlp/ipm/condensed.hpp
  *                                           -> ipm::CondensedKkt (ipm/condensed.hpp:27-185)
+ *   include/gridnlp_b200/shim/gridnlp/ipm/lifted.hpp
+ *                                           -> ipm::LiftedProblem (ipm/lifted.hpp:22-200)
  * and INTEGRATION.md shows the bindings a maintainer adds.
  *
  * Memory modes (`mem` argument):
