@@ -315,6 +315,15 @@ int gn_kkt_values(gn_kkt* kkt, double* a_vals, double* m_vals, int mem);
  * still being assembled.  Their contents change with the next set_jacobian / assemble call
  * on the KKT's stream: order such reads after it with an event. */
 int gn_kkt_values_ptr(gn_kkt* kkt, const double** a_vals, const double** m_vals);
+/* Asynchronous read-back for host solvers: start copying A and/or M (NULL skips one) into
+ * page-locked host memory (gn_host_alloc / cudaHostAlloc; pageable memory makes the copy
+ * synchronous) on a side stream, after the KKT's work so far, and return at once -- the copy
+ * overlaps whatever the caller does next, e.g. the next assemble's uploads (PCIe is full
+ * duplex).  gn_kkt_values_wait blocks until it has landed; the KKT's next set_jacobian /
+ * assemble waits for it on the device.  Not for CUDA-graph capture (the side stream is
+ * joined only by that next write). */
+int gn_kkt_values_start(gn_kkt* kkt, double* a_vals, double* m_vals);
+int gn_kkt_values_wait(gn_kkt* kkt);
 /* Selects the assembly algorithm: 0 = auto, 1 = generic contributor lists,
  * 2 = OPF-specialised (lifted KKTs only). */
 /* Cap the fused/specialised KKT kernels at `ctas_per_sm` resident CTAs per SM (grid-stride;

@@ -66,6 +66,7 @@ class B200HostValues {
   }
   double* data() { return p_; }
   size_t size() const { return n_; }
+  bool pinned() const { return pinned_; }
   operator std::span<const double>() const { return {p_, n_}; }
 
  private:
@@ -123,18 +124,30 @@ class CondensedKkt {
 
   index_t dim() const { return n_; }
   const sparse::CsrPattern& jacobian_csr() const { return a_; }
-  std::span<const double> jacobian_values() const { return a_vals_; }
+  std::span<const double> jacobian_values() const {
+    wait_a();
+    return a_vals_;
+  }
   const sparse::CscPattern& pattern() const { return mpat_; }
   std::span<const double> values() const { return mvals_; }
   index_t factor_nnz() const { return ldlt().factor_nnz(); }
   // (not in the reference) true when the OPF-specialised kernels assemble this KKT
   bool b200_specialised() const { return specialised_; }
 
-  // A = scatter(J) on the GPU; the values come back for the host solves.
+  // A = scatter(J) on the GPU; the values come back for the host solves.  Into page-locked
+  // memory the copy runs on a side stream while the IPM carries on (the next assemble's
+  // uploads go the other way over PCIe); every reader of A waits for it first.
   void set_jacobian(std::span<const double> jac_vals) {
-    if (gn_kkt_set_jacobian(kkt_, jac_vals.data(), GN_MEM_HOST) != GN_OK ||
-        gn_kkt_values(kkt_, a_vals_.data(), nullptr, GN_MEM_HOST) != GN_OK)
+    wait_a();
+    if (gn_kkt_set_jacobian(kkt_, jac_vals.data(), GN_MEM_HOST) != GN_OK)
       throw Error("CondensedKkt::set_jacobian (gridnlp_b200) failed");
+    if (a_vals_.pinned()) {
+      if (gn_kkt_values_start(kkt_, a_vals_.data(), nullptr) != GN_OK)
+        throw Error("CondensedKkt::set_jacobian (gridnlp_b200) read-back failed");
+      a_pending_ = true;
+    } else if (gn_kkt_values(kkt_, a_vals_.data(), nullptr, GN_MEM_HOST) != GN_OK) {
+      throw Error("CondensedKkt::set_jacobian (gridnlp_b200) failed");
+    }
   }
 
   // M = W + dw I + Sx + At D A on the GPU; the per-row C/D factors the solve
@@ -173,6 +186,7 @@ class CondensedKkt {
   // dy = -qs - (Ss + dw) ds  (the class comment of condensed.hpp:17-26).
   double solve(std::span<const double> qx, std::span<const double> qs,
                std::span<const double> qy, Direction& d, int refine_passes) {
+    wait_a();
     for (index_t i = 0; i < m_; ++i) {
       const size_t u = static_cast<size_t>(i);
       tm_[u] = cvec_[u] * qs[u] + dvec_[u] * qy[u];
@@ -197,6 +211,11 @@ class CondensedKkt {
   }
 
  private:
+  void wait_a() const {
+    if (!a_pending_) return;
+    if (gn_kkt_values_wait(kkt_) != GN_OK) throw Error("CondensedKkt: A read-back failed");
+    a_pending_ = false;
+  }
   // the reference's LDL^T (AMD + symbolic analysis) on M's pattern, built once on first use
   sparse::LdltSolver& ldlt() const {
     if (!ldlt_) ldlt_.emplace(mpat_, std::vector<index_t>{}, ldlt_opts_);
@@ -209,6 +228,7 @@ class CondensedKkt {
   index_t n_, m_;
   sparse::CsrPattern a_;
   B200HostValues a_vals_;
+  mutable bool a_pending_ = false;  // A still on its way back (set_jacobian)
   sparse::CscPattern mpat_;
   B200HostValues mvals_;
   mutable std::optional<sparse::LdltSolver> ldlt_;

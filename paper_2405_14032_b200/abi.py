@@ -86,6 +86,8 @@ _SIGS = {
     "gn_ctx_publish": (C.c_int, [vp, C.c_int]),
     "gn_debug_kkt_guard": (C.c_int, [vp, C.c_int, C.c_uint64, i64p]),
     "gn_kkt_values_ptr": (C.c_int, [vp, C.POINTER(vp), C.POINTER(vp)]),
+    "gn_kkt_values_start": (C.c_int, [vp, f64p, f64p]),
+    "gn_kkt_values_wait": (C.c_int, [vp]),
     "gn_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(vp)]),
     "gn_host_free": (C.c_int, [vp]),
     "gn_halo_create": (C.c_int, [vp, C.c_int32, C.c_int32, C.POINTER(vp), C.POINTER(GnError)]),

@@ -859,6 +859,12 @@ int gn_kkt_create_lifted(gn_ctx* c, gn_kkt** out, gn_error* err) {
 static void kkt_free(gn_kkt* K) {
   cudaSetDevice(K->device);
   if (K->stream) cudaStreamSynchronize(K->stream);
+  if (K->vstream) {
+    cudaStreamSynchronize(K->vstream);
+    cudaStreamDestroy(K->vstream);
+  }
+  if (K->vstart) cudaEventDestroy(K->vstart);
+  if (K->vdone) cudaEventDestroy(K->vdone);
   cudaStream_t s = K->owned_stream;
   gn_ctx* c = K->ctx;
   gnb::opf_kkt_free(K);
@@ -926,6 +932,15 @@ int gn_kkt_slots(gn_kkt* K, int32_t* js, int32_t* hs, int32_t* ps, int32_t* ds, 
   API_CATCH(nullptr)
 }
 
+// A and M may still be read back on the side stream (gn_kkt_values_start): a kernel that
+// writes one of them first waits for that copy on the device (no host synchronisation).
+// Called after the host-mode uploads, so those overlap the read-back.
+static void order_after_values(gn_kkt* K, bool writes_a, bool writes_m) {
+  if (!((writes_a && K->vpend_a) || (writes_m && K->vpend_m))) return;
+  GN_CK(cudaStreamWaitEvent(K->stream, K->vdone, 0));
+  K->vpend_a = K->vpend_m = false;
+}
+
 int gn_kkt_set_jacobian(gn_kkt* K, const double* jv, int mem) {
   if (!K || !jv) return GN_ERR_INVALID;
   if (is_full(mem) && !K->ctx) return GN_ERR_INVALID;
@@ -937,6 +952,7 @@ int gn_kkt_set_jacobian(gn_kkt* K, const double* jv, int mem) {
     K->sj.upload(jv, n, K->stream);
     dj = K->sj.p;
   }
+  order_after_values(K, true, false);
   gnb::kkt_set_jacobian(K, dj, is_full(mem));
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
   return GN_OK;
@@ -957,6 +973,7 @@ int gn_kkt_assemble(gn_kkt* K, const double* hv, const double* sx, const double*
     K->sss.upload(ss, K->m, K->stream);
     dh = K->sh.p; dsx = K->ssx.p; dss = K->sss.p;
   }
+  order_after_values(K, false, true);
   gnb::kkt_assemble(K, dh, dsx, dss, dw, dc, is_full(mem));
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
   return GN_OK;
@@ -973,6 +990,7 @@ int gn_kkt_set_jacobian_x(gn_kkt* K, const double* x, int mem) {
     K->sj.upload(x, K->ctx->d.n, K->stream);
     dx = K->sj.p;
   }
+  order_after_values(K, true, false);
   gnb::opf_set_jacobian_fused(K, dx);
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
   return GN_OK;
@@ -993,6 +1011,7 @@ int gn_kkt_assemble_x(gn_kkt* K, const double* x, const double* w, double ow, co
     K->sss.upload(ss, K->m, K->stream);
     dx = K->sj.p; dwt = K->sh.p; dsx = K->ssx.p; dss = K->sss.p;
   }
+  order_after_values(K, false, true);
   gnb::opf_assemble_fused(K, dx, dwt, ow, dsx, dss, dw, dc);
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
   return GN_OK;
@@ -1013,6 +1032,7 @@ int gn_kkt_update_x(gn_kkt* K, const double* x, const double* w, double ow, cons
     K->sss.upload(ss, K->m, K->stream);
     dx = K->sj.p; dwt = K->sh.p; dsx = K->ssx.p; dss = K->sss.p;
   }
+  order_after_values(K, true, true);
   gnb::opf_update_fused(K, dx, dwt, ow, dsx, dss, dw, dc);
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
   return GN_OK;
@@ -1034,6 +1054,37 @@ int gn_kkt_values(gn_kkt* K, double* av, double* mv, int mem) {
     if (mv && K->mnnz) gnb::d2h(mv, K->mvals.p, sizeof(double) * K->mnnz, K->stream);
   }
   if (!is_async(mem)) GN_CK(cudaStreamSynchronize(K->stream));
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_values_start(gn_kkt* K, double* av, double* mv) {
+  if (!K) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  if (!K->vstream) {
+    GN_CK(cudaStreamCreateWithFlags(&K->vstream, cudaStreamNonBlocking));
+    GN_CK(cudaEventCreateWithFlags(&K->vstart, cudaEventDisableTiming));
+    GN_CK(cudaEventCreateWithFlags(&K->vdone, cudaEventDisableTiming));
+  }
+  GN_CK(cudaEventRecord(K->vstart, K->stream));
+  GN_CK(cudaStreamWaitEvent(K->vstream, K->vstart, 0));
+  if (av && K->annz)
+    GN_CK(cudaMemcpyAsync(av, K->avals.p, sizeof(double) * K->annz, cudaMemcpyDefault, K->vstream));
+  if (mv && K->mnnz)
+    GN_CK(cudaMemcpyAsync(mv, K->mvals.p, sizeof(double) * K->mnnz, cudaMemcpyDefault, K->vstream));
+  GN_CK(cudaEventRecord(K->vdone, K->vstream));
+  K->vpend_a = K->vpend_a || (av && K->annz);
+  K->vpend_m = K->vpend_m || (mv && K->mnnz);
+  return GN_OK;
+  API_CATCH(nullptr)
+}
+
+int gn_kkt_values_wait(gn_kkt* K) {
+  if (!K) return GN_ERR_INVALID;
+  API_TRY
+  set_device(K->device);
+  if (K->vdone) GN_CK(cudaEventSynchronize(K->vdone));
   return GN_OK;
   API_CATCH(nullptr)
 }

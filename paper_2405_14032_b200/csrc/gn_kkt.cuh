@@ -44,6 +44,10 @@ struct gn_kkt {
   gnb::DBuf<double> sj, sh, ssx, sss;  // host-mode staging
   gnb::DBuf<double> jfull, hfull;      // lifted inputs scattered to the full COO order (OPF kernels)
   gnb::OpfKkt* opf = nullptr;    // OPF-specialised tables (gn_kkt_create_lifted)
+  // gn_kkt_values_start: the read-back on a side stream, ordered before the next write
+  cudaStream_t vstream = nullptr;
+  cudaEvent_t vstart = nullptr, vdone = nullptr;
+  bool vpend_a = false, vpend_m = false;  // which arrays the side-stream copy still reads
 };
 
 namespace gnb {

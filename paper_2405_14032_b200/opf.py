@@ -444,6 +444,14 @@ class CondensedKkt:
         _check(self.lib.gn_kkt_values_ptr(self.h, C.byref(a), C.byref(m)))
         return a.value or 0, m.value or 0
 
+    def values_start(self, a_out=None, m_out=None):
+        """gn_kkt_values_start: A / M into pinned host buffers on a side stream (async)."""
+        _check(self.lib.gn_kkt_values_start(self.h, _f64(a_out) if a_out is not None else None,
+                                            _f64(m_out) if m_out is not None else None))
+
+    def values_wait(self):
+        _check(self.lib.gn_kkt_values_wait(self.h))
+
     def values_device(self, a_out, m_out, sync: bool = True):
         _check(self.lib.gn_kkt_values(self.h, _f64(a_out), _f64(m_out),
                                       GN_MEM_DEVICE if sync else GN_MEM_DEVICE_ASYNC))

@@ -810,3 +810,29 @@ def test_eval_all_equals_the_five_callbacks(gpu, fx):
     assert ok == (not firsts)
     if firsts:
         assert nlp.last_error == min(firsts)
+
+
+def test_values_start_overlaps_and_orders_before_the_next_write(gpu):
+    """gn_kkt_values_start: the side-stream read-back of A / M into pinned memory lands the
+    values of the moment it was started -- the next assemble / set_jacobian waits for it on
+    the device -- and equals the synchronous read-back."""
+    import torch
+    nlp, z, meta, net = _nlp("case118_T4")
+    nlp.lift(1e-4)
+    K = CondensedKkt(nlp=nlp)
+    (dw, dc), (dw2, dc2) = DELTAS[0], DELTAS[1]
+    K.update_x(z["x"], z["w"], float(z["ow"]), z["sx"], z["ss"], dw, dc)
+    a_ref, m_ref = K.values()
+    pa = torch.full((K.a_nnz,), np.nan, dtype=torch.float64).pin_memory()
+    pm = torch.full((K.m_nnz,), np.nan, dtype=torch.float64).pin_memory()
+    K.values_start(pa, pm)
+    # a different assembly right behind it (host inputs): its kernels must not overtake the copy
+    K.update_x(z["x"] * 1.01, z["w"], float(z["ow"]), z["sx"], z["ss"], dw2, dc2)
+    K.values_wait()
+    assert_bitexact(pa.numpy(), a_ref, "A read back before the next write")
+    assert_bitexact(pm.numpy(), m_ref, "M read back before the next write")
+    a2, m2 = K.values()
+    assert not np.array_equal(m2, m_ref)  # the second assembly did change M
+    K.values_start(pa, None)
+    K.values_wait()
+    assert_bitexact(pa.numpy(), a2, "A after the second assembly")
