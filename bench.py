@@ -429,12 +429,27 @@ def run_ours(args, rank, world, local_rank, dist):
     # GPU's memory over NVLink / NVSwitch, one kernel per exchange, capturable in the
     # step's CUDA graph; --halo nccl: torch.distributed point-to-point (eager only).
     halo = peer = None
+    halo_kind = args.halo
     if world > 1:
         from paper_2405_14032_b200.shard import DeviceHalo, ShardMap
-        if args.halo == "peer":
-            peer = DeviceHalo(nlp, rank, world)
-            peer.connect()
-        else:
+        if halo_kind == "peer":
+            # every rank must map every peer region, or none uses them: a rank whose mapping
+            # failed would leave its neighbours' exchange kernels waiting for its flags
+            ok = 1
+            try:
+                peer = DeviceHalo(nlp, rank, world)
+                peer.connect()
+            except Exception as e:  # noqa: BLE001 -- reported, then the NCCL halo instead
+                print(f"rank {rank}: peer-memory halo unavailable ({e}); using the NCCL halo",
+                      file=sys.stderr)
+                ok = 0
+            import torch.distributed as tdist
+            flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+            tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
+            if int(flag.item()) == 0:
+                peer = None
+                halo_kind = "nccl"
+        if halo_kind != "peer":
             info = nlp.shard_info()
             mp_ = ShardMap(net.n_bus, net.n_line, net.n_gen, s.n_thermal, info["ramp_gens"],
                            T_total, first, T_rank)
@@ -851,7 +866,7 @@ def run_ours(args, rank, world, local_rank, dist):
                                "loads": net.n_load},
                    "periods_per_gpu": T_rank, "periods_total": T_total,
                    "parallelism": f"period-shard x{world}",
-                   "halo": None if world == 1 else (f"{args.halo}: " + (
+                   "halo": None if world == 1 else (f"{halo_kind}: " + (
                        "gn_halo peer-memory stores over NVLink, one kernel per exchange, in "
                        "the CUDA graph" if peer is not None else
                        "torch.distributed NCCL point-to-point, eager")),
