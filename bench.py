@@ -460,7 +460,7 @@ def run_ours(args, rank, world, local_rank, dist):
             peer.exchange(dx, dss, DeviceHalo.BOTH, torch.cuda.current_stream().cuda_stream)
         else:
             from paper_2405_14032_b200.shard import exchange_halo
-            exchange_halo(halo, dx, dss, rank)
+            exchange_halo(halo, dx, dss, rank, stage_cpu=halo_kind == "gloo")
 
     # Two streams: the callbacks on `stream`, the KKT on `kstream`.  Given x, w
     # and Sigma, f/grad/g/J/H and the fused A/M are independent (the fused KKT
@@ -869,7 +869,8 @@ def run_ours(args, rank, world, local_rank, dist):
                    "halo": None if world == 1 else (f"{halo_kind}: " + (
                        "gn_halo peer-memory stores over NVLink, one kernel per exchange, in "
                        "the CUDA graph" if peer is not None else
-                       "torch.distributed NCCL point-to-point, eager")),
+                       "torch.distributed NCCL point-to-point, eager" if halo_kind == "nccl"
+                       else "gloo, staged through host memory (functional check only)")),
                    "nnz_per_step_per_gpu": {"J": s.jac_nnz, "H": s.hess_nnz, "M": kkt.m_nnz},
                    "l2": "256 MB buffer rewritten between timed steps (outside step events); "
                          "per-step working set ~5.8 GB >> 126 MB L2",
@@ -1260,7 +1261,7 @@ def main():
     ap.add_argument("--strong", action="store_true",
                     help="strong scaling: --periods is the whole horizon, partitioned over the "
                          "ranks (e.g. configs[3]: --config case13659pegase --periods 168)")
-    ap.add_argument("--halo", choices=["peer", "nccl"], default="peer",
+    ap.add_argument("--halo", choices=["peer", "nccl", "gloo"], default="peer",
                     help="period-shard halo: peer-memory stores (gn_halo) or NCCL p2p")
     ap.add_argument("--traffic-json", default=str(ROOT / "profiles" / "traffic.json"))
     args = ap.parse_args()
@@ -1272,11 +1273,21 @@ def main():
         run_reference(args, rank, world)
         return
     dist = None
+    # GN_BENCH_ONE_GPU=1: a functional check of the multi-rank path on one GPU -- every rank on
+    # cuda:0, a gloo group, the halo staged through host memory (no kernel waits on another
+    # process's kernel); its timings mean nothing
+    one_gpu = world > 1 and os.environ.get("GN_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local_rank = 0
+        args.halo = "gloo"
     if world > 1:
         import torch
         import torch.distributed as tdist
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if one_gpu:
+            tdist.init_process_group("gloo")
+        else:
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         dist = tdist
     try:
         run_ours(args, rank, world, local_rank, dist)

@@ -162,17 +162,19 @@ class ShardMap:
                     GR=self.GR, prev=self.prev, next=self.next)
 
 
-def exchange_halo(plan: dict, x, sigma_s, rank: int):
+def exchange_halo(plan: dict, x, sigma_s, rank: int, stage_cpu: bool = False):
     """One ramp-halo exchange with torch.distributed (NCCL on device tensors in
-    bench.py; gloo on CPU in tests/test_shard_gloo.py): pg(., t1-1) to the next
+    bench.py; gloo on CPU in tests/test_shard_gloo.py; `stage_cpu`: device tensors whose
+    messages go through host memory, for a gloo group): pg(., t1-1) to the next
     rank, pg(., t0) and the boundary rows' sigma_s to the previous rank, written
     into this rank's ghost set-points / ghost rows.  G doubles per message."""
     import torch
     import torch.distributed as tdist
-    kw = dict(dtype=x.dtype, device=x.device)
+    kw = dict(dtype=x.dtype, device="cpu" if stage_cpu else x.device)
+    msg = (lambda t: t.cpu()) if stage_cpu else (lambda t: t)  # noqa: E731
     ops, recv = [], {}
     if plan["next"]:
-        ops.append(tdist.P2POp(tdist.isend, x.index_select(0, plan["pg_last"]), rank + 1))
+        ops.append(tdist.P2POp(tdist.isend, msg(x.index_select(0, plan["pg_last"])), rank + 1))
         recv["xn"] = torch.empty(plan["GR"], **kw)
         recv["sn"] = torch.empty(plan["GR"], **kw)
         ops.append(tdist.P2POp(tdist.irecv, recv["xn"], rank + 1))
@@ -180,16 +182,17 @@ def exchange_halo(plan: dict, x, sigma_s, rank: int):
     if plan["prev"]:
         recv["xp"] = torch.empty(plan["GR"], **kw)
         ops.append(tdist.P2POp(tdist.irecv, recv["xp"], rank - 1))
-        ops.append(tdist.P2POp(tdist.isend, x.index_select(0, plan["pg_first"]), rank - 1))
-        ops.append(tdist.P2POp(tdist.isend, sigma_s.index_select(0, plan["rows_first"]), rank - 1))
+        ops.append(tdist.P2POp(tdist.isend, msg(x.index_select(0, plan["pg_first"])), rank - 1))
+        ops.append(tdist.P2POp(tdist.isend, msg(sigma_s.index_select(0, plan["rows_first"])),
+                               rank - 1))
     if ops:
         for wk in tdist.batch_isend_irecv(ops):
             wk.wait()
     if "xp" in recv:
-        x.index_copy_(0, plan["g_prev"], recv["xp"])
+        x.index_copy_(0, plan["g_prev"], recv["xp"].to(x.device))
     if "xn" in recv:
-        x.index_copy_(0, plan["g_next"], recv["xn"])
-        sigma_s.index_copy_(0, plan["rows_ghost"], recv["sn"])
+        x.index_copy_(0, plan["g_next"], recv["xn"].to(x.device))
+        sigma_s.index_copy_(0, plan["rows_ghost"], recv["sn"].to(x.device))
 
 
 def global_objective(f_local, world: int):
@@ -201,12 +204,13 @@ def global_objective(f_local, world: int):
     device; returns a 1-element tensor."""
     import torch
     import torch.distributed as tdist
-    parts = [torch.empty_like(f_local) for _ in range(world)]
-    tdist.all_gather(parts, f_local)
+    src = f_local.cpu() if tdist.get_backend() == "gloo" else f_local
+    parts = [torch.empty_like(src) for _ in range(world)]
+    tdist.all_gather(parts, src)
     total = parts[0].clone()
     for p in parts[1:]:
         total += p
-    return total
+    return total.to(f_local.device)
 
 
 class DeviceHalo:
