@@ -193,7 +193,10 @@ constexpr int kFLW = GN_FLW;  // warps per CTA
 #ifndef GN_FL_FLAT
 #define GN_FL_FLAT 1
 #endif
-constexpr int kFLCap = 16;  // staged slots per column (longer columns are written in place)
+#ifndef GN_FLCAP
+#define GN_FLCAP 16  // 12: 30k x 96 =, 9241 x 48 +0.5%; 24 (25 KB of staging per CTA): +6-10%
+#endif
+constexpr int kFLCap = GN_FLCAP;  // staged slots per column (longer columns are written in place)
 template <bool STRUCT, bool FLAT = false>
 __device__ __forceinline__ void fz_line_body(int64_t vblock, const OpfKktTab& t,
                                              const double* __restrict__ x,
