@@ -16,12 +16,13 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-@pytest.mark.parametrize("strong", [False, True])
-def test_bench_two_ranks_one_gpu(gpu, strong):
+@pytest.mark.parametrize("strong,ranks", [(False, 3), (True, 2)])
+def test_bench_multirank_one_gpu(gpu, strong, ranks):
+    """weak scaling over three ranks (the middle one has both halo neighbours), strong over two"""
     periods = 24 if not strong else 48
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-           "--master-addr", "127.0.0.1", "--master-port", str(29530 + int(strong)),
-           str(ROOT / "bench.py"), "--gpus", "2", "--steps", "4", "--warmup", "3",
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+           str(ranks), "--master-addr", "127.0.0.1", "--master-port", str(29530 + int(strong)),
+           str(ROOT / "bench.py"), "--gpus", str(ranks), "--steps", "4", "--warmup", "3",
            "--config", "case1354pegase", "--periods", str(periods), "--e2e-steps", "2",
            "--no-ipm-ops", "--no-trial", "--traffic-json", ""]
     if strong:
@@ -32,9 +33,9 @@ def test_bench_two_ranks_one_gpu(gpu, strong):
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1, out.stdout[-2000:]  # rank 0 alone prints
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["value"] > 0 and d["ms_per_step"] > 0
+    assert d["n_gpus"] == ranks and d["value"] > 0 and d["ms_per_step"] > 0
     c = d["config"]
-    assert c["parallelism"] == "period-shard x2" and c["halo"].startswith("gloo")
-    assert c["periods_total"] == (48 if not strong else 48)
+    assert c["parallelism"] == f"period-shard x{ranks}" and c["halo"].startswith("gloo")
+    assert c["periods_total"] == (24 * ranks if not strong else 48)
     assert c["periods_per_gpu"] == 24
     assert d["e2e"]["ms_per_step"] > 0
