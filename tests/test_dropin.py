@@ -65,3 +65,29 @@ def test_reference_ipm_on_b200_path(gpu, tmp_path, key, nlp):
     assert (r["lifted_device"] >= 1) if nlp == "cuda" else (r["lifted_device"] == 0), r
     assert r["lifted_host"] == r["restorations"] + (0 if nlp == "cuda" else 1), r
     assert abs(r["objective"] - g["objective"]) <= 1e-6 * abs(g["objective"]), (r, g)
+
+
+LIFTED_CHECK = ROOT / "oracle" / "_ref" / "lifted_check"
+
+
+@pytest.mark.parametrize("case,periods", [("case118", 24), ("synth", 3), ("case1354s", 4),
+                                          ("synthloop", 4)])
+def test_lifted_shim_matches_the_reference_class(gpu, tmp_path, case, periods):
+    """The shim LiftedProblem over CudaOpfNlp (device mode) against the reference's own
+    LiftedProblem over PatternNlp, relative and absolute relaxation: structures, free map,
+    boxes, slack boxes and to_full bit for bit; the lifted evaluations within the 1e-12 bar
+    (grad bit for bit)."""
+    if not LIFTED_CHECK.exists():
+        pytest.skip("oracle/_ref/lifted_check not built (needs /root/reference at build time)")
+    net = golden_network(case)
+    scale = load_profile(net.n_load, periods, 60.0, seed=1)
+    path = tmp_path / "net.bin"
+    write_bin(path, net, periods, scale)
+    out = subprocess.run([str(LIFTED_CHECK), str(path)], capture_output=True, text=True,
+                         timeout=600)
+    assert out.returncode == 0, out.stderr
+    for r in json.loads(out.stdout.strip().splitlines()[-1]):
+        assert r["device_mode"] == 1 and r["host_mode"] == 1, r
+        assert r["struct_diff"] == 0 and r["boxes_diff"] == 0 and r["to_full_diff"] == 0, r
+        assert r["evals_ok"] == 1 and r["grad_diff"] == 0, r
+        assert r["max_rel_diff"] <= 1e-12, r
