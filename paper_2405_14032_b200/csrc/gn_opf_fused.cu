@@ -681,7 +681,8 @@ static bool ensure_aux(gn_kkt* K) {
 // four when the whole bus sweep is a few thousand warps (the step is then the chain of
 // short latency-bound launches, which parallel lanes shorten).  Measured, step ms for
 // 1 / 2 / 4 / 8 lanes: 1354 x 24: 0.059 / 0.058 / 0.044 / 0.050; 9241 x 48: 0.255 /
-// 0.270 / 0.274 / 0.274; 30k x 96: 1.179 / 1.190 / 1.217 / 1.246.
+// 0.270 / 0.274 / 0.274; 30k x 96: 1.179 / 1.190 / 1.217 / 1.246.  Re-measured on the final
+// kernels: 9241 x 48 1 / 2 / 3 lanes 0.2335 / 0.238 / 0.248; 30k x 96 1 / 2: 1.111 / 1.140.
 // GRIDNLP_B200_BUS_LANES overrides (1 .. kBusClasses).
 static int bus_lanes(const OpfKkt* X) {
   static const int env = [] {
