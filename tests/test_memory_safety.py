@@ -97,6 +97,15 @@ def test_callbacks_guard_bands(gpu, name, net, T, scale):
         torch.cuda.synchronize()
         got = check_out(buf, n, k)
         assert np.array_equal(got, ref[k], equal_nan=False), f"{name} {k}"
+    # the five in one call (gn_eval_all: one launch at these sizes)
+    bufs = {k: guarded_out(n) for k, n in sizes.items()}
+    ok, _ = nlp.eval_all(gx, gw, 0.9, outs=tuple(bufs[k][1] for k in ("f", "grad", "g", "jac",
+                                                                        "hess")),
+                         mem=GN_MEM_DEVICE)
+    assert ok
+    torch.cuda.synchronize()
+    for k, n in sizes.items():
+        assert np.array_equal(check_out(bufs[k][0], n, "all " + k), ref[k]), f"{name} all {k}"
     fb, fo = guarded_out(1)
     gb, go = guarded_out(s.n_cons)
     assert nlp.eval_device("fg", gx, (fo, go))
@@ -112,6 +121,18 @@ def test_callbacks_guard_bands(gpu, name, net, T, scale):
         nlp.lifted_gather(which, gin, out=out, mem=GN_MEM_DEVICE)
         torch.cuda.synchronize()
         assert np.array_equal(check_out(buf, n, "gather " + which), nlp.lifted_gather(which, full))
+    # the lifted evaluations (gn_lifted_eval_*) on a guarded free-variable vector
+    f2f = nlp.lifted_structure()["free_to_full"]
+    _, gxf = guarded_in(x[f2f])
+    for which, n in (("grad", s.n_free), ("g", s.n_cons), ("jac", s.jac_nnz_lifted),
+                     ("hess", s.hess_nnz_lifted)):
+        buf, out = guarded_out(n)
+        ok, _ = nlp.lifted_eval(which, gxf, w=gw, ow=0.9, out=out, mem=GN_MEM_DEVICE)
+        assert ok
+        torch.cuda.synchronize()
+        got = check_out(buf, n, "lifted " + which)
+        want = nlp.lifted_eval(which, x[f2f], w=w, ow=0.9)[1]
+        assert np.array_equal(got, want), f"{name} lifted {which}"
 
 
 def _kkt_guard(K, fill):
